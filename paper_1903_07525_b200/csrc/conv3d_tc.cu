@@ -1,0 +1,401 @@
+// conv3d_tc.cu — direct 3D convolution as a tcgen05/TMEM implicit GEMM.
+//
+// Replaces the reference hot loop _kernels.conv3d (_kernels.pyx:44-179) with
+// its vec8 FMA micro-kernels (convcore.h:19-52).  Semantics follow the
+// reference contract (kernels_py.py:7-10, _kernels.pyx:112-175):
+//     out = act(bias' + [base_scale .] base + sum_{ib,dx,dy,dz,i} in * K')
+// cross-correlation (no flip), stride 1, zero padding virtual.
+//
+// Mapping:
+//   M  = output voxels.  A CTA tile is bx x-slices x 16 (y) x 8 (z); every
+//        x-slice is one 128-row UMMA (rows = y*8 + z) with its own TMEM
+//        accumulator of nt fp32 columns.
+//   N  = output fmaps (nt per tile, padded to 16).
+//   K  = input fmaps x taps, consumed in "steps" of 16 bf16: either two
+//        8-fmap chunks at one tap, or (odd last chunk) one chunk at two
+//        adjacent z taps.
+//   A operand: for each group of <=2 input chunks, one TMA box per chunk
+//        brings the halo tile (bx+kx-1, 16+ky-1, 8+kz-1 voxels, 16 B each)
+//        into shared memory as a dense [x][y][z] array of 16-byte rows.
+//        That is exactly the SWIZZLE_NONE K-major core-matrix layout, so the
+//        operand for tap (dx,dy,dz) is just the descriptor start address
+//        moved by ((dx*hy + dy)*hz + dz)*16 bytes: no im2col, the halo is
+//        read from HBM/L2 once per tile and every tap reuses it from smem.
+//        Out-of-range coordinates are zero-filled by TMA = 'same' padding.
+//   B operand: weights pre-packed on the host into per-step slabs in the
+//        core-matrix layout; streamed with cp.async.bulk (or loaded once and
+//        kept resident when the whole filter bank fits).
+// Warp roles: w0 = TMA producer, w1 = MMA issuer (+TMEM owner), w2..w5 =
+// epilogue (TMEM -> regs -> bias/base/act -> global).  Persistent CTAs walk
+// the tile list; TMEM accumulators are double buffered when they fit so the
+// epilogue of tile i overlaps the MMAs of tile i+1.
+#include <cuda_bf16.h>
+#include "vxb_internal.h"
+#include "vxb_ptx.cuh"
+
+namespace vxb {
+
+struct GroupInfo {
+  int seg, chunk0, nch, steps;
+};
+
+__device__ __forceinline__ GroupInfo group_info(const TcParams &p, int g) {
+  int g0 = (p.seg_chunks[0] + 1) >> 1;
+  int seg = g < g0 ? 0 : 1;
+  int j = seg ? g - g0 : g;
+  int c = p.seg_chunks[seg];
+  int nch = min(2, c - 2 * j);
+  int steps = nch == 2 ? p.kx * p.ky * p.kz : p.kx * p.ky * ((p.kz + 1) >> 1);
+  GroupInfo gi{seg, 2 * j, nch, steps};
+  return gi;
+}
+
+struct TileCoord {
+  int rep, nt, b, x0, y0, z0;
+};
+
+__device__ __forceinline__ TileCoord decode_tile(const TcParams &p, int t) {
+  TileCoord c;
+  int tz = t % p.tiles_z;
+  t /= p.tiles_z;
+  int ty = t % p.tiles_y;
+  t /= p.tiles_y;
+  int tx = t % p.tiles_x;
+  t /= p.tiles_x;
+  c.b = t % p.nb;
+  t /= p.nb;
+  c.nt = t % p.n_tiles;
+  c.rep = t / p.n_tiles;
+  c.x0 = tx * p.bx;
+  c.y0 = ty * TILE_Y;
+  c.z0 = tz * TILE_Z;
+  return c;
+}
+
+__device__ __forceinline__ float apply_act(float v, int act, float alpha) {
+  if (act == VXB_ACT_RELU) return v > 0.f ? v : 0.f;
+  if (act == VXB_ACT_ELU) return v > 0.f ? v : alpha * expm1f(v);
+  if (act == VXB_ACT_SIGMOID) return 1.f / (1.f + expf(-v));
+  return v;
+}
+
+__device__ __forceinline__ void load8(const EpiView &v, long long off, bool blocked_lane_stride1,
+                                      float (&x)[8]) {
+  if (v.dtype == VXB_BF16) {
+    const __nv_bfloat16 *p = static_cast<const __nv_bfloat16 *>(v.data) + off;
+    if (blocked_lane_stride1) {
+      uint4 u = *reinterpret_cast<const uint4 *>(p);
+      const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float2 f = __bfloat1622float2(h[i]);
+        x[2 * i] = f.x;
+        x[2 * i + 1] = f.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = __bfloat162float(p[i * v.s[1]]);
+    }
+  } else {
+    const float *p = static_cast<const float *>(v.data) + off;
+    if (blocked_lane_stride1) {
+      float4 a = *reinterpret_cast<const float4 *>(p);
+      float4 b = *reinterpret_cast<const float4 *>(p + 4);
+      x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+      x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = p[i * v.s[1]];
+    }
+  }
+}
+
+// store lanes [0, nvalid) of one 8-fmap chunk; blocked layouts get all 8
+// lanes (tail lanes are written as zero, ops.py:18-23 zero_tail semantics)
+__device__ __forceinline__ void store8(const EpiView &v, long long off, bool blocked,
+                                       int nvalid, const float (&x)[8]) {
+  if (v.dtype == VXB_BF16) {
+    __nv_bfloat16 *p = static_cast<__nv_bfloat16 *>(v.data) + off;
+    if (blocked) {
+      uint4 u;
+      __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&u);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
+      *reinterpret_cast<uint4 *>(p) = u;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < nvalid) p[i * v.s[1]] = __float2bfloat16_rn(x[i]);
+    }
+  } else {
+    float *p = static_cast<float *>(v.data) + off;
+    if (blocked) {
+      *reinterpret_cast<float4 *>(p) = make_float4(x[0], x[1], x[2], x[3]);
+      *reinterpret_cast<float4 *>(p + 4) = make_float4(x[4], x[5], x[6], x[7]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < nvalid) p[i * v.s[1]] = x[i];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(192, 1)
+    conv3d_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  // smem carve-up: [A stages][B stages][barriers][tmem ptr]
+  uint8_t *a_buf = smem;
+  uint8_t *b_buf = smem + p.na * p.a_stage_bytes;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(b_buf + p.nb_stages * p.b_stage_bytes);
+  uint64_t *a_full = bars;
+  uint64_t *a_empty = a_full + p.na;
+  uint64_t *b_full = a_empty + p.na;
+  uint64_t *b_empty = b_full + p.nb_stages;
+  uint64_t *t_full = b_empty + p.nb_stages;
+  uint64_t *t_empty = t_full + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(t_empty + 2);
+
+  const int acc_cols = p.bx * p.nt;
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < static_cast<uint32_t>(acc_cols * p.acc_stages)) tmem_cols <<= 1;
+
+  // zero the guard bytes behind every chunk array (read, with zero weight,
+  // by the odd-chunk z-pair steps)
+  for (int s = 0; s < p.na; ++s)
+    for (int c = 0; c < p.chunk_slots; ++c) {
+      uint8_t *g = a_buf + s * p.a_stage_bytes + c * p.chunk_stride + p.chunk_bytes;
+      for (int i = threadIdx.x; i < 32; i += blockDim.x) reinterpret_cast<uint32_t *>(g)[i] = 0u;
+    }
+  fence_proxy_async_smem();
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&maps.m[0]);
+    if (p.seg_chunks[1] > 0) prefetch_tmap(&maps.m[1]);
+    for (int i = 0; i < p.na; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < p.nb_stages; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&t_full[i], 1);
+      mbar_init(&t_empty[i], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, tmem_cols);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int a_st = 0, a_ph = 0, b_st = 0, b_ph = 0;
+      bool first = true;
+      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+        TileCoord tc = decode_tile(p, tile);
+        const uint8_t *wbase = p.w + tc.rep * p.w_rep_stride + tc.nt * p.w_ntile_stride;
+        long long step_base = 0;
+        if (p.resident) b_st = 0;
+        for (int g = 0; g < p.n_groups; ++g) {
+          GroupInfo gi = group_info(p, g);
+          mbar_wait(&a_empty[a_st], a_ph ^ 1);
+          mbar_expect_tx(&a_full[a_st], gi.nch * p.chunk_bytes);
+          const int *off = p.seg_off[gi.seg];
+          int cx = tc.x0 - p.pad[0] + off[0];
+          int cy = tc.y0 - p.pad[1] + off[1];
+          int cz = (tc.z0 - p.pad[2] + off[2]) * LANES;
+          for (int ci = 0; ci < gi.nch; ++ci) {
+            int chunk = tc.b * p.seg_bstride[gi.seg] + gi.chunk0 + ci;
+            tma_load_4d(a_buf + a_st * p.a_stage_bytes + ci * p.chunk_stride, &maps.m[gi.seg],
+                        &a_full[a_st], cz, cy, cx, chunk);
+          }
+          if (++a_st == p.na) {
+            a_st = 0;
+            a_ph ^= 1;
+          }
+          if (!p.resident || first) {
+            for (int s0 = 0; s0 < gi.steps; s0 += p.bsteps) {
+              int n = min(p.bsteps, gi.steps - s0);
+              uint32_t bytes = static_cast<uint32_t>(n * p.nt * SLAB_ROW_BYTES);
+              mbar_wait(&b_empty[b_st], b_ph ^ 1);
+              mbar_expect_tx(&b_full[b_st], bytes);
+              bulk_load(b_buf + b_st * p.b_stage_bytes,
+                        wbase + (step_base + s0) * p.nt * SLAB_ROW_BYTES, bytes, &b_full[b_st]);
+              if (++b_st == p.nb_stages) {
+                b_st = 0;
+                b_ph ^= 1;
+              }
+            }
+          }
+          step_base += gi.steps;
+        }
+        first = false;
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16(128, p.nt);
+      const uint32_t a_base0 = smem_u32(a_buf);
+      const uint32_t b_base0 = smem_u32(b_buf);
+      const uint32_t sbo_a = p.hz * 16;
+      const int kzh = (p.kz + 1) >> 1;
+      int a_st = 0, a_ph = 0, b_st = 0, b_ph = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++it) {
+        const int acc = it % p.acc_stages;
+        const int aph = (it / p.acc_stages) & 1;
+        mbar_wait(&t_empty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_base = tmem_base + acc * acc_cols;
+        uint32_t accumulate = 0;
+        if (p.resident) b_st = 0;
+        for (int g = 0; g < p.n_groups; ++g) {
+          GroupInfo gi = group_info(p, g);
+          mbar_wait(&a_full[a_st], a_ph);
+          tc_fence_after();
+          const uint32_t a_base = a_base0 + a_st * p.a_stage_bytes;
+          const uint32_t lbo_a = gi.nch == 2 ? static_cast<uint32_t>(p.chunk_stride) : 16u;
+          for (int s0 = 0; s0 < gi.steps; s0 += p.bsteps) {
+            int n = min(p.bsteps, gi.steps - s0);
+            if (p.resident) {
+              if (it == 0) mbar_wait(&b_full[b_st], 0);
+            } else {
+              mbar_wait(&b_full[b_st], b_ph);
+            }
+            tc_fence_after();
+            const uint32_t b_base = b_base0 + b_st * p.b_stage_bytes;
+            for (int i = 0; i < n; ++i) {
+              int t = s0 + i, dx, dy, dz;
+              if (gi.nch == 2) {
+                dz = t % p.kz;
+                dy = (t / p.kz) % p.ky;
+                dx = t / (p.kz * p.ky);
+              } else {
+                dz = 2 * (t % kzh);
+                dy = (t / kzh) % p.ky;
+                dx = t / (kzh * p.ky);
+              }
+              const uint64_t bdesc = smem_desc(b_base + i * p.nt * SLAB_ROW_BYTES, 128u, 256u);
+              const uint32_t tap_off = ((dx * p.hy + dy) * p.hz + dz) * 16;
+              for (int s = 0; s < p.bx; ++s) {
+                const uint32_t a_addr = a_base + tap_off + s * p.hy * p.hz * 16;
+                umma_bf16(d_base + s * p.nt, smem_desc(a_addr, lbo_a, sbo_a), bdesc, idesc,
+                          accumulate);
+              }
+              accumulate = 1;
+            }
+            if (!p.resident) umma_commit(&b_empty[b_st]);
+            if (++b_st == p.nb_stages) {
+              b_st = 0;
+              b_ph ^= 1;
+            }
+          }
+          umma_commit(&a_empty[a_st]);
+          if (++a_st == p.na) {
+            a_st = 0;
+            a_ph ^= 1;
+          }
+        }
+        umma_commit(&t_full[acc]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== epilogue =====================
+    const int q = warp & 3;              // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;       // MMA row == TMEM lane
+    const int yy = row >> 3, zz = row & 7;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++it) {
+      TileCoord tc = decode_tile(p, tile);
+      const int acc = it % p.acc_stages;
+      mbar_wait(&t_full[acc], (it / p.acc_stages) & 1);
+      tc_fence_after();
+      const int y = tc.y0 + yy, z = tc.z0 + zz;
+      const long long orep = p.out_rep_off[tc.rep];
+      const long long brep = p.base_rep_off[tc.rep];
+      for (int s = 0; s < p.bx; ++s) {
+        const int x = tc.x0 + s;
+        const bool valid = x < p.ox && y < p.oy && z < p.oz;
+        for (int cc = 0; cc < p.nt; cc += 16) {
+          float v[16];
+          tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * acc_cols +
+                        s * p.nt + cc,
+                    v);
+          if (!valid) continue;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c0 = tc.nt * p.nt + cc + h * 8;  // first fmap of this chunk
+            if (c0 >= p.cout) continue;
+            const int nvalid = min(8, p.cout - c0);
+            float r[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) r[i] = (i < nvalid) ? p.bias[c0 + i] : 0.f;
+            if (p.has_base) {
+              float bv[8];
+              const EpiView &bvw = p.base;
+              long long boff = brep + tc.b * bvw.s[0] + x * bvw.s[2] + y * bvw.s[3] +
+                               z * bvw.s[4] + (bvw.blocked ? (c0 >> 3) * bvw.s[1] : c0 * bvw.s[1]);
+              load8(bvw, boff, bvw.blocked, bv);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (i < nvalid) r[i] += (p.scale ? p.scale[c0 + i] : 1.f) * bv[i];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              r[i] = (i < nvalid) ? apply_act(r[i] + v[h * 8 + i], p.act, p.alpha) : 0.f;
+            const EpiView &ov = p.out;
+            long long ooff = orep + tc.b * ov.s[0] + x * ov.s[2] + y * ov.s[3] + z * ov.s[4] +
+                             (ov.blocked ? (c0 >> 3) * ov.s[1] : c0 * ov.s[1]);
+            store8(ov, ooff, ov.blocked, nvalid, r);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&t_empty[acc]);
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, tmem_cols);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+
+size_t tc_smem_bytes(const TcParams &p) {
+  return static_cast<size_t>(p.na) * p.a_stage_bytes +
+         static_cast<size_t>(p.nb_stages) * p.b_stage_bytes +
+         (2 * p.na + 2 * p.nb_stages + 4) * sizeof(uint64_t) + 16;
+}
+
+int launch_conv3d_tc(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t stream) {
+  size_t smem = tc_smem_bytes(p);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(conv3d_tc_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(conv3d_tc)");
+    configured = true;
+  }
+  conv3d_tc_kernel<<<grid, 192, smem, stream>>>(p, maps);
+  return check_cuda(cudaGetLastError(), "conv3d_tc_kernel launch");
+}
+
+}  // namespace vxb

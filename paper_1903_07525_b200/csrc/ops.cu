@@ -1,0 +1,552 @@
+// ops.cu — bandwidth kernels and the CUDA-core convolution paths.
+//
+//   direct conv      generic strides / kernel sizes (reference a1 semantics,
+//                    _kernels.pyx:44-179) on CUDA cores; also the subimage
+//                    debug primitive (_kernels.pyx:182-271)
+//   gather deconv    transposed conv for k != stride (kernels_py.py:162-196)
+//   pool             ops.pool (ops.py:63-86)
+//   eltwise          ops.eltwise (ops.py:50-60)
+//   affine_act       ops.linear_transform + ops.activation (ops.py:89-102)
+//   mergecrop        ops.mergecrop (ops.py:113-136)
+//   pad_copy         ops.pad_copy (ops.py:105-110)
+//   copy             to_blocked / from_blocked (blocked.py:209-231)
+//
+// All element-wise kernels work on one 8-fmap chunk per thread: for the
+// blocked bf16 layout that is one 16-byte load/store, z fastest across the
+// warp so a warp touches 512 contiguous bytes.
+#include <cuda_bf16.h>
+#include "vxb_internal.h"
+
+namespace vxb {
+
+
+
+__device__ __forceinline__ long long voff(const DView &v, int b, int c, int x, int y, int z) {
+  return b * v.s[0] + (v.blocked ? (c >> 3) * v.s[1] + (c & 7) : c * v.s[1]) + x * v.s[2] +
+         y * v.s[3] + z * v.s[4];
+}
+__device__ __forceinline__ float vld(const DView &v, long long i) {
+  return v.dtype == VXB_BF16 ? __bfloat162float(static_cast<const __nv_bfloat16 *>(v.data)[i])
+                             : static_cast<const float *>(v.data)[i];
+}
+__device__ __forceinline__ void vst(const DView &v, long long i, float f) {
+  if (v.dtype == VXB_BF16)
+    static_cast<__nv_bfloat16 *>(v.data)[i] = __float2bfloat16_rn(f);
+  else
+    static_cast<float *>(v.data)[i] = f;
+}
+
+// chunk-granular access: lanes [0, 8) of chunk `ch` at voxel (b,x,y,z)
+__device__ __forceinline__ void ld_chunk(const DView &v, int b, int ch, int x, int y, int z,
+                                         float (&r)[8]) {
+  if (v.blocked) {
+    long long o = b * v.s[0] + ch * v.s[1] + x * v.s[2] + y * v.s[3] + z * v.s[4];
+    if (v.dtype == VXB_BF16) {
+      uint4 u = *reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(v.data) + o);
+      const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float2 f = __bfloat1622float2(h[i]);
+        r[2 * i] = f.x;
+        r[2 * i + 1] = f.y;
+      }
+    } else {
+      const float *p = static_cast<const float *>(v.data) + o;
+      float4 a = *reinterpret_cast<const float4 *>(p), c = *reinterpret_cast<const float4 *>(p + 4);
+      r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w;
+      r[4] = c.x; r[5] = c.y; r[6] = c.z; r[7] = c.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int c = ch * 8 + i;
+      r[i] = c < v.c ? vld(v, voff(v, b, c, x, y, z)) : 0.f;
+    }
+  }
+}
+// writes all 8 lanes for blocked views (caller zeroes lanes >= c), valid
+// channels only for standard views
+__device__ __forceinline__ void st_chunk(const DView &v, int b, int ch, int x, int y, int z,
+                                         const float (&r)[8]) {
+  if (v.blocked) {
+    long long o = b * v.s[0] + ch * v.s[1] + x * v.s[2] + y * v.s[3] + z * v.s[4];
+    if (v.dtype == VXB_BF16) {
+      uint4 u;
+      __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&u);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(r[2 * i], r[2 * i + 1]);
+      *reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(v.data) + o) = u;
+    } else {
+      float *p = static_cast<float *>(v.data) + o;
+      *reinterpret_cast<float4 *>(p) = make_float4(r[0], r[1], r[2], r[3]);
+      *reinterpret_cast<float4 *>(p + 4) = make_float4(r[4], r[5], r[6], r[7]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int c = ch * 8 + i;
+      if (c < v.c) vst(v, voff(v, b, c, x, y, z), r[i]);
+    }
+  }
+}
+
+__device__ __forceinline__ float act_fn(float v, int act, float alpha) {
+  if (act == VXB_ACT_RELU) return v > 0.f ? v : 0.f;
+  if (act == VXB_ACT_ELU) return v > 0.f ? v : alpha * expm1f(v);
+  if (act == VXB_ACT_SIGMOID) return 1.f / (1.f + expf(-v));
+  return v;
+}
+
+// flat index -> (b, chunk, x, y, z) with z fastest
+struct ChunkIdx {
+  int b, ch, x, y, z;
+};
+__device__ __forceinline__ bool chunk_index(long long i, int n, int nch, int X, int Y, int Z,
+                                            ChunkIdx &o) {
+  long long total = static_cast<long long>(n) * nch * X * Y * Z;
+  if (i >= total) return false;
+  o.z = static_cast<int>(i % Z);
+  i /= Z;
+  o.y = static_cast<int>(i % Y);
+  i /= Y;
+  o.x = static_cast<int>(i % X);
+  i /= X;
+  o.ch = static_cast<int>(i % nch);
+  o.b = static_cast<int>(i / nch);
+  return true;
+}
+
+__device__ __forceinline__ void zero_tail_lanes(float (&r)[8], int ch, int c) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (ch * 8 + i >= c) r[i] = 0.f;
+}
+
+// ------------------------------------------------------------------ copy
+__global__ void copy_kernel(DView src, DView dst) {
+  ChunkIdx k;
+  int nch = (dst.c + 7) >> 3;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+       chunk_index(i, dst.n, nch, dst.x, dst.y, dst.z, k);
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float r[8];
+    ld_chunk(src, k.b, k.ch, k.x, k.y, k.z, r);
+    zero_tail_lanes(r, k.ch, dst.c);
+    st_chunk(dst, k.b, k.ch, k.x, k.y, k.z, r);
+  }
+}
+
+__global__ void zero_kernel(DView dst) {
+  ChunkIdx k;
+  int nch = (dst.c + 7) >> 3;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+       chunk_index(i, dst.n, nch, dst.x, dst.y, dst.z, k);
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (dst.blocked) {
+      st_chunk(dst, k.b, k.ch, k.x, k.y, k.z, r);
+    } else {
+      for (int l = 0; l < 8; ++l)
+        if (k.ch * 8 + l < dst.c) vst(dst, voff(dst, k.b, k.ch * 8 + l, k.x, k.y, k.z), 0.f);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ pool
+// max: seed with the first window element, then max in (dx,dy,dz) order with
+// np.maximum NaN propagation; avg: fp32 sum in the same order, / kvol.
+__global__ void pool_kernel(DView in, DView out, int kx, int ky, int kz, int sx, int sy, int sz,
+                            int mode) {
+  ChunkIdx k;
+  int nch = (out.c + 7) >> 3;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+       chunk_index(i, out.n, nch, out.x, out.y, out.z, k);
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float r[8], t[8];
+    bool first = true;
+    for (int dx = 0; dx < kx; ++dx)
+      for (int dy = 0; dy < ky; ++dy)
+        for (int dz = 0; dz < kz; ++dz) {
+          ld_chunk(in, k.b, k.ch, k.x * sx + dx, k.y * sy + dy, k.z * sz + dz, t);
+          if (first) {
+#pragma unroll
+            for (int l = 0; l < 8; ++l) r[l] = t[l];
+            first = false;
+          } else if (mode == VXB_POOL_MAX) {
+#pragma unroll
+            for (int l = 0; l < 8; ++l) r[l] = (t[l] > r[l] || t[l] != t[l]) ? t[l] : r[l];
+          } else {
+#pragma unroll
+            for (int l = 0; l < 8; ++l) r[l] += t[l];
+          }
+        }
+    if (mode == VXB_POOL_AVG) {
+      float kv = static_cast<float>(kx * ky * kz);
+#pragma unroll
+      for (int l = 0; l < 8; ++l) r[l] = r[l] / kv;
+    }
+    zero_tail_lanes(r, k.ch, out.c);
+    st_chunk(out, k.b, k.ch, k.x, k.y, k.z, r);
+  }
+}
+
+// ------------------------------------------------------------------ eltwise
+__global__ void eltwise_kernel(DView a, DView b, DView out, int op) {
+  ChunkIdx k;
+  int nch = (out.c + 7) >> 3;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+       chunk_index(i, out.n, nch, out.x, out.y, out.z, k);
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float ra[8], rb[8], r[8];
+    ld_chunk(a, k.b, k.ch, k.x, k.y, k.z, ra);
+    ld_chunk(b, k.b, k.ch, k.x, k.y, k.z, rb);
+#pragma unroll
+    for (int l = 0; l < 8; ++l)
+      r[l] = op == VXB_ELT_ADD ? ra[l] + rb[l] : (op == VXB_ELT_MUL ? ra[l] * rb[l] : ra[l] / rb[l]);
+    zero_tail_lanes(r, k.ch, out.c);
+    st_chunk(out, k.b, k.ch, k.x, k.y, k.z, r);
+  }
+}
+
+// ------------------------------------------------------------------ affine + act
+__global__ void affine_act_kernel(DView in, DView out, const float *mult, const float *add, int act,
+                                  float alpha) {
+  ChunkIdx k;
+  int nch = (out.c + 7) >> 3;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+       chunk_index(i, out.n, nch, out.x, out.y, out.z, k);
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float r[8];
+    ld_chunk(in, k.b, k.ch, k.x, k.y, k.z, r);
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+      int c = k.ch * 8 + l;
+      if (c < out.c) {
+        float v = r[l];
+        if (mult) v = v * mult[c];
+        if (add) v = v + add[c];
+        r[l] = act_fn(v, act, alpha);
+      }
+    }
+    zero_tail_lanes(r, k.ch, out.c);
+    st_chunk(out, k.b, k.ch, k.x, k.y, k.z, r);
+  }
+}
+
+// ------------------------------------------------------------------ mergecrop
+__global__ void mergecrop_kernel(DView a, DView b, DView out, int oax, int oay, int oaz, int obx,
+                                 int oby, int obz) {
+  ChunkIdx k;
+  int nch = (out.c + 7) >> 3;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+       chunk_index(i, out.n, nch, out.x, out.y, out.z, k);
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float r[8];
+    if ((a.c & 7) == 0 && a.blocked && b.blocked) {
+      int ach = a.c >> 3;
+      if (k.ch < ach)
+        ld_chunk(a, k.b, k.ch, k.x + oax, k.y + oay, k.z + oaz, r);
+      else
+        ld_chunk(b, k.b, k.ch - ach, k.x + obx, k.y + oby, k.z + obz, r);
+    } else {
+#pragma unroll
+      for (int l = 0; l < 8; ++l) {
+        int c = k.ch * 8 + l;
+        if (c < a.c)
+          r[l] = vld(a, voff(a, k.b, c, k.x + oax, k.y + oay, k.z + oaz));
+        else if (c < a.c + b.c)
+          r[l] = vld(b, voff(b, k.b, c - a.c, k.x + obx, k.y + oby, k.z + obz));
+        else
+          r[l] = 0.f;
+      }
+    }
+    zero_tail_lanes(r, k.ch, out.c);
+    st_chunk(out, k.b, k.ch, k.x, k.y, k.z, r);
+  }
+}
+
+// ------------------------------------------------------------------ pad copy
+__global__ void pad_copy_kernel(DView in, DView out, int px, int py, int pz) {
+  ChunkIdx k;
+  int nch = (out.c + 7) >> 3;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+       chunk_index(i, out.n, nch, out.x, out.y, out.z, k);
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int x = k.x - px, y = k.y - py, z = k.z - pz;
+    if (x >= 0 && y >= 0 && z >= 0 && x < in.x && y < in.y && z < in.z)
+      ld_chunk(in, k.b, k.ch, x, y, z, r);
+    zero_tail_lanes(r, k.ch, out.c);
+    st_chunk(out, k.b, k.ch, k.x, k.y, k.z, r);
+  }
+}
+
+// ------------------------------------------------------------------ direct conv
+// One CTA = 128 output voxels (2 x 8 x 8) x 16 output fmaps.  Input chunks
+// are staged through shared memory (fp32), weights too.  Packed weight
+// layout: [cout_group(16)][in_chunk][tap][8 in][16 out] fp32.
+
+
+constexpr int DT_X = 2, DT_Y = 8, DT_Z = 8, DCO = 16;
+
+__global__ void __launch_bounds__(128) conv_direct_kernel(DirectParams p) {
+  extern __shared__ float dsm[];
+  const int taps = p.kx * p.ky * p.kz;
+  float *patch = dsm;                                   // [hx][hy][hz][8]
+  float *wsm = dsm + p.hx * p.hy * p.hz * 8;            // [tap][8][16]
+  int t = blockIdx.x;
+  int tz = t % p.tiles_z;
+  t /= p.tiles_z;
+  int ty = t % p.tiles_y;
+  int tx = t / p.tiles_y;
+  const int cg = blockIdx.y, b = blockIdx.z;
+  const int lx = threadIdx.x / (DT_Y * DT_Z), ly = (threadIdx.x / DT_Z) % DT_Y,
+            lz = threadIdx.x % DT_Z;
+  const int x0 = tx * DT_X, y0 = ty * DT_Y, z0 = tz * DT_Z;
+  const int ox = x0 + lx, oy = y0 + ly, oz = z0 + lz;
+  float acc[DCO];
+#pragma unroll
+  for (int i = 0; i < DCO; ++i) acc[i] = 0.f;
+  const int in_chunks = (p.cin + 7) >> 3;
+  const int npatch = p.hx * p.hy * p.hz;
+  for (int ch = 0; ch < in_chunks; ++ch) {
+    const int lanes = min(8, p.cin - ch * 8);
+    __syncthreads();
+    for (int i = threadIdx.x; i < npatch; i += blockDim.x) {
+      int iz = i % p.hz, iy = (i / p.hz) % p.hy, ix = i / (p.hz * p.hy);
+      int gx = x0 * p.sx - p.px + ix, gy = y0 * p.sy - p.py + iy, gz = z0 * p.sz - p.pz + iz;
+      float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (gx >= 0 && gy >= 0 && gz >= 0 && gx < p.in.x && gy < p.in.y && gz < p.in.z)
+        ld_chunk(p.in, b, ch, gx, gy, gz, r);
+#pragma unroll
+      for (int l = 0; l < 8; ++l) patch[i * 8 + l] = r[l];
+    }
+    const float *wsrc = p.w + (static_cast<long long>(cg) * in_chunks + ch) * taps * 8 * DCO;
+    for (int i = threadIdx.x; i < taps * 8 * DCO; i += blockDim.x) wsm[i] = wsrc[i];
+    __syncthreads();
+    for (int dx = 0; dx < p.kx; ++dx)
+      for (int dy = 0; dy < p.ky; ++dy)
+        for (int dz = 0; dz < p.kz; ++dz) {
+          const int tap = (dx * p.ky + dy) * p.kz + dz;
+          const float *src =
+              patch + (((lx * p.sx + dx) * p.hy + ly * p.sy + dy) * p.hz + lz * p.sz + dz) * 8;
+          const float *wt = wsm + tap * 8 * DCO;
+          for (int l = 0; l < lanes; ++l) {
+            const float v = src[l];
+#pragma unroll
+            for (int o = 0; o < DCO; ++o) acc[o] = fmaf(v, wt[l * DCO + o], acc[o]);
+          }
+        }
+  }
+  if (ox >= p.out.x || oy >= p.out.y || oz >= p.out.z) return;
+#pragma unroll
+  for (int h = 0; h < DCO / 8; ++h) {
+    const int ch = cg * (DCO / 8) + h;
+    if (ch * 8 >= p.cout) continue;
+    float r[8], bv[8];
+    if (p.has_base) ld_chunk(p.base, b, ch, ox, oy, oz, bv);
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+      int c = ch * 8 + l;
+      if (c < p.cout) {
+        float init = p.bias[c];
+        if (p.has_base) init += (p.scale ? p.scale[c] : 1.f) * bv[l];
+        r[l] = act_fn(init + acc[h * 8 + l], p.act, p.alpha);
+      } else {
+        r[l] = 0.f;
+      }
+    }
+    st_chunk(p.out, b, ch, ox, oy, oz, r);
+  }
+}
+
+// ------------------------------------------------------------------ subimage
+// one input chunk -> one output patch, through memory (test primitive)
+
+
+__global__ void subimage_kernel(SubParams p) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int nb = p.out.n;
+  int total = nb * p.ex * p.ey * p.ez * 8;
+  if (i >= total) return;
+  int o = i % 8;
+  int v = i / 8;
+  int zz = v % p.ez;
+  v /= p.ez;
+  int yy = v % p.ey;
+  v /= p.ey;
+  int xx = v % p.ex;
+  int b = v / p.ex;
+  int x = p.x0 + xx, y = p.y0 + yy, z = p.z0 + zz;
+  int co = p.ob * 8 + o;
+  long long oo = b * p.out.s[0] + p.ob * p.out.s[1] + o + x * p.out.s[2] + y * p.out.s[3] +
+                 z * p.out.s[4];
+  float acc;
+  if (p.first) {
+    acc = co < p.cout ? p.bias[co] : 0.f;
+    if (p.has_base && co < p.cout)
+      acc += (p.scale ? p.scale[co] : 1.f) *
+             vld(p.base, b * p.base.s[0] + p.ob * p.base.s[1] + o + x * p.base.s[2] +
+                             y * p.base.s[3] + z * p.base.s[4]);
+  } else {
+    acc = vld(p.out, oo);
+  }
+  for (int dx = 0; dx < p.kx; ++dx)
+    for (int dy = 0; dy < p.ky; ++dy)
+      for (int dz = 0; dz < p.kz; ++dz)
+        for (int l = 0; l < 8; ++l) {
+          int ci = p.ib * 8 + l;
+          if (ci >= p.cin || co >= p.cout) continue;
+          float xv = vld(p.in, b * p.in.s[0] + p.ib * p.in.s[1] + l +
+                                   (x * p.sx + dx) * p.in.s[2] + (y * p.sy + dy) * p.in.s[3] +
+                                   (z * p.sz + dz) * p.in.s[4]);
+          float wv = p.w[(((static_cast<long long>(co) * p.cin + ci) * p.kx + dx) * p.ky + dy) *
+                             p.kz + dz];
+          acc = fmaf(xv, wv, acc);
+        }
+  if (p.last) acc = co < p.cout ? act_fn(acc, p.act, p.alpha) : 0.f;
+  vst(p.out, oo, acc);
+}
+
+// ------------------------------------------------------------------ gather deconv
+// out[o] = act(bias + [base] + sum_{ci,d: (o-d)%s==0} in[(o-d)/s] W[co][ci][d])
+
+
+__global__ void deconv_gather_kernel(GatherDeconvParams p) {
+  ChunkIdx k;
+  int nch = (p.out.c + 7) >> 3;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+       chunk_index(i, p.out.n, nch, p.out.x, p.out.y, p.out.z, k);
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int dx = 0; dx < p.kx; ++dx) {
+      int ix = k.x - dx;
+      if (ix < 0 || ix % p.sx) continue;
+      ix /= p.sx;
+      if (ix >= p.in.x) continue;
+      for (int dy = 0; dy < p.ky; ++dy) {
+        int iy = k.y - dy;
+        if (iy < 0 || iy % p.sy) continue;
+        iy /= p.sy;
+        if (iy >= p.in.y) continue;
+        for (int dz = 0; dz < p.kz; ++dz) {
+          int iz = k.z - dz;
+          if (iz < 0 || iz % p.sz) continue;
+          iz /= p.sz;
+          if (iz >= p.in.z) continue;
+          for (int ci = 0; ci < p.cin; ++ci) {
+            float xv = vld(p.in, voff(p.in, k.b, ci, ix, iy, iz));
+#pragma unroll
+            for (int l = 0; l < 8; ++l) {
+              int co = k.ch * 8 + l;
+              if (co < p.cout)
+                acc[l] = fmaf(xv,
+                              p.w[(((static_cast<long long>(co) * p.cin + ci) * p.kx + dx) * p.ky +
+                                   dy) * p.kz + dz],
+                              acc[l]);
+            }
+          }
+        }
+      }
+    }
+    float r[8], bv[8];
+    if (p.has_base) ld_chunk(p.base, k.b, k.ch, k.x, k.y, k.z, bv);
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+      int co = k.ch * 8 + l;
+      if (co < p.cout) {
+        float init = p.bias[co];
+        if (p.has_base) init += (p.scale ? p.scale[co] : 1.f) * bv[l];
+        r[l] = act_fn(init + acc[l], p.act, p.alpha);
+      } else {
+        r[l] = 0.f;
+      }
+    }
+    st_chunk(p.out, k.b, k.ch, k.x, k.y, k.z, r);
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+static int grid_for(long long work, int threads) {
+  long long g = (work + threads - 1) / threads;
+  long long cap = 148LL * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+static long long chunk_work(const DView &v) {
+  return static_cast<long long>(v.n) * ((v.c + 7) / 8) * v.x * v.y * v.z;
+}
+
+int launch_copy(const DView &src, const DView &dst, cudaStream_t s) {
+  copy_kernel<<<grid_for(chunk_work(dst), 256), 256, 0, s>>>(src, dst);
+  return check_cuda(cudaGetLastError(), "copy_kernel");
+}
+int launch_zero(const DView &dst, cudaStream_t s) {
+  zero_kernel<<<grid_for(chunk_work(dst), 256), 256, 0, s>>>(dst);
+  return check_cuda(cudaGetLastError(), "zero_kernel");
+}
+int launch_pool(const DView &in, const DView &out, const int *w, const int *st, int mode,
+                cudaStream_t s) {
+  pool_kernel<<<grid_for(chunk_work(out), 256), 256, 0, s>>>(in, out, w[0], w[1], w[2], st[0],
+                                                              st[1], st[2], mode);
+  return check_cuda(cudaGetLastError(), "pool_kernel");
+}
+int launch_eltwise(const DView &a, const DView &b, const DView &out, int op, cudaStream_t s) {
+  eltwise_kernel<<<grid_for(chunk_work(out), 256), 256, 0, s>>>(a, b, out, op);
+  return check_cuda(cudaGetLastError(), "eltwise_kernel");
+}
+int launch_affine_act(const DView &in, const DView &out, const float *m, const float *a, int act,
+                      float alpha, cudaStream_t s) {
+  affine_act_kernel<<<grid_for(chunk_work(out), 256), 256, 0, s>>>(in, out, m, a, act, alpha);
+  return check_cuda(cudaGetLastError(), "affine_act_kernel");
+}
+int launch_mergecrop(const DView &a, const DView &b, const DView &out, const int *oa,
+                     const int *ob, cudaStream_t s) {
+  mergecrop_kernel<<<grid_for(chunk_work(out), 256), 256, 0, s>>>(a, b, out, oa[0], oa[1], oa[2],
+                                                                   ob[0], ob[1], ob[2]);
+  return check_cuda(cudaGetLastError(), "mergecrop_kernel");
+}
+int launch_pad_copy(const DView &in, const DView &out, const int *pads, cudaStream_t s) {
+  pad_copy_kernel<<<grid_for(chunk_work(out), 256), 256, 0, s>>>(in, out, pads[0], pads[1],
+                                                                  pads[2]);
+  return check_cuda(cudaGetLastError(), "pad_copy_kernel");
+}
+
+int launch_conv_direct(DirectParams p, cudaStream_t s) {
+  p.tiles_x = (p.out.x + DT_X - 1) / DT_X;
+  p.tiles_y = (p.out.y + DT_Y - 1) / DT_Y;
+  p.tiles_z = (p.out.z + DT_Z - 1) / DT_Z;
+  p.hx = (DT_X - 1) * p.sx + p.kx;
+  p.hy = (DT_Y - 1) * p.sy + p.ky;
+  p.hz = (DT_Z - 1) * p.sz + p.kz;
+  size_t smem = (static_cast<size_t>(p.hx) * p.hy * p.hz * 8 +
+                 static_cast<size_t>(p.kx) * p.ky * p.kz * 8 * DCO) *
+                sizeof(float);
+  if (smem > 227 * 1024)
+    return set_error(VXB_EUNSUPPORTED, "direct conv: staged patch of %zu bytes exceeds smem", smem);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(conv_direct_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(conv_direct)");
+    configured = true;
+  }
+  dim3 grid(p.tiles_x * p.tiles_y * p.tiles_z, (p.cout + DCO - 1) / DCO, p.out.n);
+  conv_direct_kernel<<<grid, 128, smem, s>>>(p);
+  return check_cuda(cudaGetLastError(), "conv_direct_kernel");
+}
+
+int launch_subimage(const SubParams &p, cudaStream_t s) {
+  int total = p.out.n * p.ex * p.ey * p.ez * 8;
+  subimage_kernel<<<(total + 127) / 128, 128, 0, s>>>(p);
+  return check_cuda(cudaGetLastError(), "subimage_kernel");
+}
+
+int launch_deconv_gather(const GatherDeconvParams &p, cudaStream_t s) {
+  deconv_gather_kernel<<<grid_for(chunk_work(p.out), 128), 128, 0, s>>>(p);
+  return check_cuda(cudaGetLastError(), "deconv_gather_kernel");
+}
+
+}  // namespace vxb

@@ -1,0 +1,794 @@
+// vxb_abi.cu — the extern "C" boundary (include/vxb.h): validation, path
+// selection, host-side weight packing, TMA descriptor encoding, launches.
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+#include "vxb_internal.h"
+
+namespace vxb {
+
+static thread_local std::string g_last_error;
+
+int set_error(int code, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int check_cuda(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return VXB_OK;
+  return set_error(VXB_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+static inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+static inline int round_up(int a, int b) { return ceil_div(a, b) * b; }
+
+static int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
+static DView to_dview(const vxb_tensor &t) {
+  DView v;
+  v.data = t.data;
+  for (int i = 0; i < 5; ++i) v.s[i] = t.s[i];
+  v.dtype = t.dtype;
+  v.blocked = t.blocked;
+  v.n = t.n;
+  v.c = t.c;
+  v.x = t.x;
+  v.y = t.y;
+  v.z = t.z;
+  return v;
+}
+
+static EpiView to_epi(const vxb_tensor &t) {
+  EpiView v;
+  v.data = t.data;
+  for (int i = 0; i < 5; ++i) v.s[i] = t.s[i];
+  v.dtype = t.dtype;
+  v.blocked = t.blocked;
+  return v;
+}
+
+static int check_view(const vxb_tensor *t, const char *what) {
+  if (!t || !t->data) return set_error(VXB_EINVAL, "%s: null tensor", what);
+  if (t->dtype != VXB_BF16 && t->dtype != VXB_F32)
+    return set_error(VXB_EINVAL, "%s: bad dtype %d", what, t->dtype);
+  if (t->n < 1 || t->c < 1 || t->x < 1 || t->y < 1 || t->z < 1)
+    return set_error(VXB_EINVAL, "%s: non-positive extent (%d,%d,%d,%d,%d)", what, t->n, t->c,
+                     t->x, t->y, t->z);
+  if (t->blocked) {
+    size_t esz = t->dtype == VXB_BF16 ? 2 : 4;
+    uintptr_t a = reinterpret_cast<uintptr_t>(t->data);
+    if (a % (8 * esz) != 0)
+      return set_error(VXB_EINVAL, "%s: blocked view base must be %zu-byte aligned", what, 8 * esz);
+    for (int i = 0; i < 5; ++i)
+      if (t->s[i] % 8 != 0)
+        return set_error(VXB_EINVAL, "%s: blocked view strides must be multiples of 8", what);
+  }
+  return VXB_OK;
+}
+
+static cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ------------------------------------------------------------------ TC geometry
+
+struct TcGroup {
+  int seg, chunk0, nch, steps;
+};
+
+struct TcLayout {
+  int npad, n_tiles, nt;
+  int seg_chunks[2];
+  std::vector<TcGroup> groups;
+  long long steps;  // per (rep, ntile)
+};
+
+static TcLayout tc_layout(int cin0, int cin1, int cout, const int k[3]) {
+  TcLayout L;
+  L.npad = round_up(cout, 16);
+  L.n_tiles = ceil_div(L.npad, 256);
+  L.nt = round_up(ceil_div(L.npad, L.n_tiles), 16);
+  L.seg_chunks[0] = ceil_div(cin0, 8);
+  L.seg_chunks[1] = cin1 > 0 ? ceil_div(cin1, 8) : 0;
+  L.steps = 0;
+  for (int seg = 0; seg < 2; ++seg) {
+    int c = L.seg_chunks[seg];
+    for (int j = 0; 2 * j < c; ++j) {
+      TcGroup g;
+      g.seg = seg;
+      g.chunk0 = 2 * j;
+      g.nch = std::min(2, c - 2 * j);
+      g.steps = g.nch == 2 ? k[0] * k[1] * k[2] : k[0] * k[1] * ceil_div(k[2], 2);
+      L.groups.push_back(g);
+      L.steps += g.steps;
+    }
+  }
+  return L;
+}
+
+static size_t tc_bytes_per_rep(const TcLayout &L) {
+  return static_cast<size_t>(L.n_tiles) * L.steps * L.nt * SLAB_ROW_BYTES;
+}
+
+static inline uint16_t f32_to_bf16_bits(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) {  // inf / nan
+    uint16_t h = static_cast<uint16_t>(u >> 16);
+    if (u & 0x007fffffu) h |= 0x40;
+    return h;
+  }
+  uint32_t lsb = (u >> 16) & 1u;
+  u += 0x7fffu + lsb;
+  return static_cast<uint16_t>(u >> 16);
+}
+
+// Pack w (cout, cin, kx, ky, kz) fp32 into per-step UMMA B slabs, bf16.
+// wtap(co, ci, dx, dy, dz) gives the weight; deconv reuses this with k=1.
+template <class WFn>
+static void tc_pack(const TcLayout &L, int cin0, int cin1, int cout, const int k[3], WFn wtap,
+                    uint8_t *dst) {
+  const int slab = L.nt * SLAB_ROW_BYTES;
+  const int kzh = ceil_div(k[2], 2);
+  long long step_idx = 0;
+  for (int nti = 0; nti < L.n_tiles; ++nti) {
+    step_idx = static_cast<long long>(nti) * L.steps;
+    for (const TcGroup &g : L.groups) {
+      const int cin_seg = g.seg == 0 ? cin0 : cin1;
+      const int cbase = g.seg == 0 ? 0 : cin0;
+      for (int t = 0; t < g.steps; ++t, ++step_idx) {
+        int dx, dy, dz;
+        if (g.nch == 2) {
+          dz = t % k[2];
+          dy = (t / k[2]) % k[1];
+          dx = t / (k[2] * k[1]);
+        } else {
+          dz = 2 * (t % kzh);
+          dy = (t / kzh) % k[1];
+          dx = t / (kzh * k[1]);
+        }
+        uint16_t *s = reinterpret_cast<uint16_t *>(dst + step_idx * slab);
+        for (int n = 0; n < L.nt; ++n) {
+          const int co = nti * L.nt + n;
+          for (int kk = 0; kk < 16; ++kk) {
+            const int h = kk >> 3, l = kk & 7;
+            int chunk = g.chunk0, tz = dz;
+            if (g.nch == 2)
+              chunk += h;
+            else
+              tz += h;
+            const int cl = chunk * 8 + l;
+            float v = 0.f;
+            if (co < cout && cl < cin_seg && tz < k[2]) v = wtap(co, cbase + cl, dx, dy, tz);
+            const size_t byte = static_cast<size_t>(n >> 3) * 256 + h * 128 + (n & 7) * 16 + l * 2;
+            s[byte / 2] = f32_to_bf16_bits(v);
+          }
+        }
+      }
+    }
+  }
+}
+
+struct TcConfig {
+  int bx, acc, na, nb, bsteps, resident, chunk_bytes, chunk_stride, chunk_slots, a_stage,
+      b_stage;
+  size_t smem;
+};
+
+static int tc_configure(const TcLayout &L, const int k[3], int ox, int reps, TcConfig &c) {
+  const int budget = 227 * 1024 - 512;
+  c.acc = env_int("VXB_TC_ACC", 2);
+  if (c.acc != 1 && c.acc != 2) c.acc = 2;
+  int bx_cap = env_int("VXB_TC_BX", 8);
+  c.bx = 1;
+  while (c.bx * 2 <= bx_cap && c.bx * 2 * L.nt * c.acc <= 512 && c.bx < ox) c.bx *= 2;
+  if (c.bx * L.nt * c.acc > 512) return set_error(VXB_EUNSUPPORTED, "TMEM overflow");
+  bool any_pair = false;
+  int max_steps = 1;
+  for (const TcGroup &g : L.groups) {
+    any_pair |= g.nch == 2;
+    max_steps = std::max(max_steps, g.steps);
+  }
+  const int slab = L.nt * SLAB_ROW_BYTES;
+  for (;;) {
+    const int hx = c.bx + k[0] - 1, hy = TILE_Y + k[1] - 1, hz = TILE_Z + k[2] - 1;
+    c.chunk_bytes = hx * hy * hz * 16;
+    c.chunk_stride = round_up(c.chunk_bytes + 128, 128);
+    c.chunk_slots = any_pair ? 2 : 1;
+    c.a_stage = c.chunk_slots * c.chunk_stride;
+    c.na = 2;
+    // resident weights: whole filter bank of the (single) N tile in smem
+    long long total_w = L.steps * slab;
+    c.resident = 0;
+    if (reps * L.n_tiles == 1 && c.na * c.a_stage + total_w <= budget) {
+      c.bsteps = max_steps;
+      int nbs = 0;
+      for (const TcGroup &g : L.groups) nbs += ceil_div(g.steps, c.bsteps);
+      c.b_stage = c.bsteps * slab;
+      if (c.na * c.a_stage + static_cast<long long>(nbs) * c.b_stage <= budget) {
+        c.resident = 1;
+        c.nb = nbs;
+      }
+    }
+    if (!c.resident) {
+      c.bsteps = std::max(1, std::min(max_steps, 32768 / slab));
+      c.b_stage = c.bsteps * slab;
+      int room = (budget - c.na * c.a_stage) / c.b_stage;
+      c.nb = std::min(4, room);
+      while (c.nb < 2 && c.bsteps > 1) {
+        c.bsteps = (c.bsteps + 1) / 2;
+        c.b_stage = c.bsteps * slab;
+        room = (budget - c.na * c.a_stage) / c.b_stage;
+        c.nb = std::min(4, room);
+      }
+    }
+    if (c.nb >= 1 && (c.resident || c.nb >= 2)) break;
+    if (c.bx == 1) return set_error(VXB_EUNSUPPORTED, "conv tile does not fit in shared memory");
+    c.bx /= 2;
+  }
+  c.smem = static_cast<size_t>(c.na) * c.a_stage + static_cast<size_t>(c.nb) * c.b_stage +
+           (2 * c.na + 2 * c.nb + 4) * sizeof(uint64_t) + 16;
+  return VXB_OK;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 4-D map over a blocked bf16 view: (lane*z, y, x, batch*chunk)
+static int make_input_map(const vxb_tensor &t, int hx, int hy, int hz, CUtensorMap *m,
+                          int *bstride) {
+  if (t.dtype != VXB_BF16 || !t.blocked)
+    return set_error(VXB_EINVAL, "tensor-core conv input must be a blocked bf16 view");
+  if (t.s[4] != 8)
+    return set_error(VXB_EINVAL, "tensor-core conv input: z stride must be 8 (got %lld)",
+                     static_cast<long long>(t.s[4]));
+  const int nch = ceil_div(t.c, 8);
+  long long total = nch;
+  *bstride = 0;
+  if (t.n > 1) {
+    if (t.s[0] % t.s[1] != 0)
+      return set_error(VXB_EINVAL, "tensor-core conv input: batch stride not a chunk multiple");
+    *bstride = static_cast<int>(t.s[0] / t.s[1]);
+    total = static_cast<long long>(t.n - 1) * *bstride + nch;
+  }
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return set_error(VXB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(8) * t.z, static_cast<cuuint64_t>(t.y),
+                        static_cast<cuuint64_t>(t.x), static_cast<cuuint64_t>(total)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(t.s[3]) * 2,
+                           static_cast<cuuint64_t>(t.s[2]) * 2,
+                           static_cast<cuuint64_t>(t.s[1]) * 2};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(8 * hz), static_cast<cuuint32_t>(hy),
+                       static_cast<cuuint32_t>(hx), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, t.data, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(VXB_ECUDA, "cuTensorMapEncodeTiled failed (%d): dims %llu %llu %llu %llu",
+                     static_cast<int>(r), (unsigned long long)dims[0],
+                     (unsigned long long)dims[1], (unsigned long long)dims[2],
+                     (unsigned long long)dims[3]);
+  return VXB_OK;
+}
+
+static int device_sms() {
+  static int sms = -1;
+  if (sms < 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = -1;
+  }
+  return sms;
+}
+
+struct TcLaunch {
+  const vxb_tensor *in[2];
+  int off[2][3];
+  int cin0, cin1, cout;
+  int k[3], pad[3];
+  int ox, oy, oz, nb;
+  int reps;
+  long long out_rep_off[MAX_REPS], base_rep_off[MAX_REPS];
+  EpiView out, base;
+  int has_base;
+  const void *w;
+  const float *bias, *scale;
+  int act;
+  float alpha;
+};
+
+static int run_tc(const TcLaunch &a, cudaStream_t stream) {
+  TcLayout L = tc_layout(a.cin0, a.cin1, a.cout, a.k);
+  TcConfig c;
+  int rc = tc_configure(L, a.k, a.ox, a.reps, c);
+  if (rc) return rc;
+  TcParams p;
+  memset(&p, 0, sizeof(p));
+  p.nb = a.nb;
+  p.ox = a.ox;
+  p.oy = a.oy;
+  p.oz = a.oz;
+  p.bx = c.bx;
+  p.nt = L.nt;
+  p.acc_stages = c.acc;
+  p.tiles_x = ceil_div(a.ox, c.bx);
+  p.tiles_y = ceil_div(a.oy, TILE_Y);
+  p.tiles_z = ceil_div(a.oz, TILE_Z);
+  p.n_tiles = L.n_tiles;
+  p.reps = a.reps;
+  long long total = static_cast<long long>(p.tiles_x) * p.tiles_y * p.tiles_z * p.nb *
+                    p.n_tiles * p.reps;
+  if (total > 0x7fffffffLL) return set_error(VXB_EUNSUPPORTED, "too many tiles");
+  p.total_tiles = static_cast<int>(total);
+  p.kx = a.k[0];
+  p.ky = a.k[1];
+  p.kz = a.k[2];
+  p.hx = c.bx + a.k[0] - 1;
+  p.hy = TILE_Y + a.k[1] - 1;
+  p.hz = TILE_Z + a.k[2] - 1;
+  for (int i = 0; i < 3; ++i) p.pad[i] = a.pad[i];
+  TcMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  for (int s = 0; s < 2; ++s) {
+    p.seg_chunks[s] = L.seg_chunks[s];
+    if (!p.seg_chunks[s]) continue;
+    for (int i = 0; i < 3; ++i) p.seg_off[s][i] = a.off[s][i];
+    rc = make_input_map(*a.in[s], p.hx, p.hy, p.hz, &maps.m[s], &p.seg_bstride[s]);
+    if (rc) return rc;
+  }
+  p.n_groups = static_cast<int>(L.groups.size());
+  p.chunk_bytes = c.chunk_bytes;
+  p.chunk_stride = c.chunk_stride;
+  p.chunk_slots = c.chunk_slots;
+  p.a_stage_bytes = c.a_stage;
+  p.b_stage_bytes = c.b_stage;
+  p.na = c.na;
+  p.nb_stages = c.nb;
+  p.bsteps = c.bsteps;
+  p.resident = c.resident;
+  p.w = static_cast<const uint8_t *>(a.w);
+  p.w_ntile_stride = L.steps * L.nt * SLAB_ROW_BYTES;
+  p.w_rep_stride = static_cast<long long>(tc_bytes_per_rep(L));
+  p.bias = a.bias;
+  p.scale = a.scale;
+  p.out = a.out;
+  p.base = a.base;
+  p.has_base = a.has_base;
+  for (int r = 0; r < MAX_REPS; ++r) {
+    p.out_rep_off[r] = a.out_rep_off[r];
+    p.base_rep_off[r] = a.base_rep_off[r];
+  }
+  p.cout = a.cout;
+  p.act = a.act;
+  p.alpha = a.alpha;
+  int sms = device_sms();
+  if (sms <= 0) return set_error(VXB_ECUDA, "no CUDA device");
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < static_cast<uint32_t>(c.bx * L.nt * c.acc)) tmem_cols <<= 1;
+  int per_sm = std::min<int>(static_cast<int>((228 * 1024) / (c.smem + 1024)),
+                             static_cast<int>(512 / tmem_cols));
+  per_sm = std::max(1, std::min(per_sm, env_int("VXB_TC_CTAS_PER_SM", 4)));
+  int grid = static_cast<int>(std::min<long long>(total, static_cast<long long>(sms) * per_sm));
+  return launch_conv3d_tc(p, maps, grid, stream);
+}
+
+}  // namespace vxb
+
+using namespace vxb;
+
+extern "C" {
+
+int vxb_abi_version(void) { return VXB_ABI_VERSION; }
+const char *vxb_last_error(void) { return g_last_error.c_str(); }
+int vxb_device_sms(void) { return device_sms(); }
+
+int vxb_conv_select(int cin, int cout, const int k[3], const int stride[3]) {
+  (void)cin;
+  (void)cout;
+  if (stride[0] == 1 && stride[1] == 1 && stride[2] == 1 && TILE_Z + k[2] - 1 <= 32 &&
+      TILE_Y + k[1] - 1 <= 256 && k[0] <= 64 && k[0] >= 1 && k[1] >= 1 && k[2] >= 1)
+    return VXB_PATH_TC;
+  return VXB_PATH_DIRECT;
+}
+
+static size_t direct_bytes(int cin, int cout, const int k[3]) {
+  return static_cast<size_t>(ceil_div(cout, DCO_DIRECT)) * ceil_div(cin, 8) * k[0] * k[1] * k[2] *
+         8 * DCO_DIRECT * sizeof(float);
+}
+
+size_t vxb_conv_weights_bytes2(int cin0, int cin1, int cout, const int k[3], const int stride[3],
+                               int path) {
+  if (path == 0) path = vxb_conv_select(cin0 + cin1, cout, k, stride);
+  if (path == VXB_PATH_TC) return tc_bytes_per_rep(tc_layout(cin0, cin1, cout, k));
+  return direct_bytes(cin0 + cin1, cout, k);
+}
+
+size_t vxb_conv_weights_bytes(int cin, int cout, const int k[3], const int stride[3], int path) {
+  return vxb_conv_weights_bytes2(cin, 0, cout, k, stride, path);
+}
+
+int vxb_conv_pack_weights2(const float *w, int cin0, int cin1, int cout, const int k[3],
+                           const int stride[3], int path, void *dst, size_t dst_bytes) {
+  const int cin = cin0 + cin1;
+  if (!w || !dst) return set_error(VXB_EINVAL, "pack: null pointer");
+  if (path == 0) path = vxb_conv_select(cin, cout, k, stride);
+  size_t need = vxb_conv_weights_bytes2(cin0, cin1, cout, k, stride, path);
+  if (dst_bytes < need) return set_error(VXB_EINVAL, "pack: need %zu bytes, got %zu", need, dst_bytes);
+  auto wtap = [&](int co, int ci, int dx, int dy, int dz) {
+    return w[((((static_cast<size_t>(co) * cin) + ci) * k[0] + dx) * k[1] + dy) * k[2] + dz];
+  };
+  if (path == VXB_PATH_TC) {
+    TcLayout L = tc_layout(cin0, cin1, cout, k);
+    tc_pack(L, cin0, cin1, cout, k, wtap, static_cast<uint8_t *>(dst));
+    return VXB_OK;
+  }
+  // direct: [cout_group][in_chunk][tap][8 in][16 out] fp32
+  float *o = static_cast<float *>(dst);
+  const int taps = k[0] * k[1] * k[2], ich = ceil_div(cin, 8), ncg = ceil_div(cout, DCO_DIRECT);
+  size_t idx = 0;
+  for (int cg = 0; cg < ncg; ++cg)
+    for (int ch = 0; ch < ich; ++ch)
+      for (int t = 0; t < taps; ++t) {
+        const int dz = t % k[2], dy = (t / k[2]) % k[1], dx = t / (k[2] * k[1]);
+        for (int l = 0; l < 8; ++l)
+          for (int oo = 0; oo < DCO_DIRECT; ++oo, ++idx) {
+            const int ci = ch * 8 + l, co = cg * DCO_DIRECT + oo;
+            o[idx] = (ci < cin && co < cout) ? wtap(co, ci, dx, dy, dz) : 0.f;
+          }
+      }
+  return VXB_OK;
+}
+
+int vxb_conv_pack_weights(const float *w, int cin, int cout, const int k[3], const int stride[3],
+                          int path, void *dst, size_t dst_bytes) {
+  return vxb_conv_pack_weights2(w, cin, 0, cout, k, stride, path, dst, dst_bytes);
+}
+
+int vxb_conv3d(const vxb_conv_desc *d, void *stream) {
+  if (!d) return set_error(VXB_EINVAL, "conv3d: null descriptor");
+  int rc;
+  if ((rc = check_view(&d->in0, "conv3d.in0"))) return rc;
+  if ((rc = check_view(&d->out, "conv3d.out"))) return rc;
+  const bool two = d->in1.data != nullptr;
+  if (two && (rc = check_view(&d->in1, "conv3d.in1"))) return rc;
+  const bool additive = d->base.data != nullptr;
+  if (additive && (rc = check_view(&d->base, "conv3d.base"))) return rc;
+  if (!d->w_packed || !d->bias) return set_error(VXB_EINVAL, "conv3d: null weights/bias");
+  const int cin0 = d->in0.c, cin1 = two ? d->in1.c : 0;
+  if (cin0 + cin1 != d->cin)
+    return set_error(VXB_EINVAL, "conv3d: cin %d != input fmaps %d", d->cin, cin0 + cin1);
+  if (d->out.c != d->cout)
+    return set_error(VXB_EINVAL, "conv3d: out view has %d fmaps, cout %d", d->out.c, d->cout);
+  for (int i = 0; i < 3; ++i)
+    if (d->k[i] < 1 || d->stride[i] < 1 || d->pad[i] < 0)
+      return set_error(VXB_EINVAL, "conv3d: bad kernel/stride/pad");
+  if (d->act < 0 || d->act > 3) return set_error(VXB_EINVAL, "conv3d: bad act %d", d->act);
+  const int path = d->path ? d->path : vxb_conv_select(d->cin, d->cout, d->k, d->stride);
+  cudaStream_t s = as_stream(stream);
+  if (path == VXB_PATH_TC) {
+    if (d->stride[0] != 1 || d->stride[1] != 1 || d->stride[2] != 1)
+      return set_error(VXB_EUNSUPPORTED, "tensor-core conv requires stride 1");
+    TcLaunch a;
+    memset(&a, 0, sizeof(a));
+    a.in[0] = &d->in0;
+    a.in[1] = two ? &d->in1 : nullptr;
+    for (int i = 0; i < 3; ++i) {
+      a.off[0][i] = d->off0[i];
+      a.off[1][i] = d->off1[i];
+      a.k[i] = d->k[i];
+      a.pad[i] = d->pad[i];
+    }
+    a.cin0 = cin0;
+    a.cin1 = cin1;
+    a.cout = d->cout;
+    a.ox = d->out.x;
+    a.oy = d->out.y;
+    a.oz = d->out.z;
+    a.nb = d->out.n;
+    a.reps = 1;
+    a.out = to_epi(d->out);
+    a.has_base = additive;
+    if (additive) a.base = to_epi(d->base);
+    a.w = d->w_packed;
+    a.bias = d->bias;
+    a.scale = additive ? d->base_scale : nullptr;
+    a.act = d->act;
+    a.alpha = d->alpha;
+    return run_tc(a, s);
+  }
+  if (two) return set_error(VXB_EUNSUPPORTED, "direct conv path takes a single input");
+  DirectParams p;
+  memset(&p, 0, sizeof(p));
+  p.in = to_dview(d->in0);
+  p.out = to_dview(d->out);
+  if (additive) p.base = to_dview(d->base);
+  p.w = static_cast<const float *>(d->w_packed);
+  p.bias = d->bias;
+  p.scale = additive ? d->base_scale : nullptr;
+  p.cin = d->cin;
+  p.cout = d->cout;
+  p.kx = d->k[0];
+  p.ky = d->k[1];
+  p.kz = d->k[2];
+  p.sx = d->stride[0];
+  p.sy = d->stride[1];
+  p.sz = d->stride[2];
+  // crop offsets fold into a negative pad
+  p.px = d->pad[0] - d->off0[0];
+  p.py = d->pad[1] - d->off0[1];
+  p.pz = d->pad[2] - d->off0[2];
+  p.act = d->act;
+  p.alpha = d->alpha;
+  p.has_base = additive;
+  return launch_conv_direct(p, s);
+}
+
+int vxb_conv3d_subimage(const vxb_conv_desc *d, const float *w_std, int in_chunk, int out_chunk,
+                        const int origin[3], const int extent[3], int first, int last,
+                        void *stream) {
+  int rc;
+  if (!d || !w_std) return set_error(VXB_EINVAL, "subimage: null argument");
+  if ((rc = check_view(&d->in0, "subimage.in"))) return rc;
+  if ((rc = check_view(&d->out, "subimage.out"))) return rc;
+  if (!d->in0.blocked || !d->out.blocked)
+    return set_error(VXB_EINVAL, "subimage: blocked views required");
+  SubParams p;
+  memset(&p, 0, sizeof(p));
+  p.in = to_dview(d->in0);
+  p.out = to_dview(d->out);
+  p.has_base = d->base.data != nullptr;
+  if (p.has_base) p.base = to_dview(d->base);
+  p.w = w_std;
+  p.bias = d->bias;
+  p.scale = d->base_scale;
+  p.cin = d->cin;
+  p.cout = d->cout;
+  p.kx = d->k[0];
+  p.ky = d->k[1];
+  p.kz = d->k[2];
+  p.sx = d->stride[0];
+  p.sy = d->stride[1];
+  p.sz = d->stride[2];
+  p.ib = in_chunk;
+  p.ob = out_chunk;
+  p.x0 = origin[0];
+  p.y0 = origin[1];
+  p.z0 = origin[2];
+  p.ex = extent[0];
+  p.ey = extent[1];
+  p.ez = extent[2];
+  p.first = first;
+  p.last = last;
+  p.act = d->act;
+  p.alpha = d->alpha;
+  return launch_subimage(p, as_stream(stream));
+}
+
+// ------------------------------------------------------------------ deconv
+
+static bool deconv_tc(const int k[3], const int stride[3]) {
+  return k[0] == stride[0] && k[1] == stride[1] && k[2] == stride[2] &&
+         k[0] * k[1] * k[2] <= MAX_REPS;
+}
+
+size_t vxb_deconv_weights_bytes(int cin, int cout, const int k[3], const int stride[3]) {
+  if (deconv_tc(k, stride)) {
+    int one[3] = {1, 1, 1};
+    return static_cast<size_t>(k[0] * k[1] * k[2]) * tc_bytes_per_rep(tc_layout(cin, 0, cout, one));
+  }
+  return static_cast<size_t>(cout) * cin * k[0] * k[1] * k[2] * sizeof(float);
+}
+
+int vxb_deconv_pack_weights(const float *w, int cin, int cout, const int k[3], const int stride[3],
+                            void *dst, size_t dst_bytes) {
+  if (!w || !dst) return set_error(VXB_EINVAL, "deconv pack: null pointer");
+  size_t need = vxb_deconv_weights_bytes(cin, cout, k, stride);
+  if (dst_bytes < need) return set_error(VXB_EINVAL, "deconv pack: need %zu bytes", need);
+  if (!deconv_tc(k, stride)) {
+    memcpy(dst, w, need);
+    return VXB_OK;
+  }
+  int one[3] = {1, 1, 1};
+  TcLayout L = tc_layout(cin, 0, cout, one);
+  size_t per = tc_bytes_per_rep(L);
+  int r = 0;
+  for (int dx = 0; dx < k[0]; ++dx)
+    for (int dy = 0; dy < k[1]; ++dy)
+      for (int dz = 0; dz < k[2]; ++dz, ++r) {
+        auto wtap = [&](int co, int ci, int, int, int) {
+          return w[((((static_cast<size_t>(co) * cin) + ci) * k[0] + dx) * k[1] + dy) * k[2] + dz];
+        };
+        tc_pack(L, cin, 0, cout, one, wtap, static_cast<uint8_t *>(dst) + r * per);
+      }
+  return VXB_OK;
+}
+
+int vxb_deconv3d(const vxb_deconv_desc *d, void *stream) {
+  if (!d) return set_error(VXB_EINVAL, "deconv3d: null descriptor");
+  int rc;
+  if ((rc = check_view(&d->in, "deconv3d.in"))) return rc;
+  if ((rc = check_view(&d->out, "deconv3d.out"))) return rc;
+  const bool additive = d->base.data != nullptr;
+  if (additive && (rc = check_view(&d->base, "deconv3d.base"))) return rc;
+  if (d->in.c != d->cin || d->out.c != d->cout)
+    return set_error(VXB_EINVAL, "deconv3d: fmap counts do not match the views");
+  for (int i = 0; i < 3; ++i) {
+    int ext = i == 0 ? d->in.x : (i == 1 ? d->in.y : d->in.z);
+    int oext = i == 0 ? d->out.x : (i == 1 ? d->out.y : d->out.z);
+    if ((ext - 1) * d->stride[i] + d->k[i] != oext)
+      return set_error(VXB_EINVAL, "deconv3d: output extent mismatch on axis %d", i);
+  }
+  cudaStream_t s = as_stream(stream);
+  if (deconv_tc(d->k, d->stride)) {
+    TcLaunch a;
+    memset(&a, 0, sizeof(a));
+    a.in[0] = &d->in;
+    a.in[1] = nullptr;
+    for (int i = 0; i < 3; ++i) a.k[i] = 1;
+    a.cin0 = d->cin;
+    a.cout = d->cout;
+    a.ox = d->in.x;
+    a.oy = d->in.y;
+    a.oz = d->in.z;
+    a.nb = d->in.n;
+    a.reps = d->k[0] * d->k[1] * d->k[2];
+    a.out = to_epi(d->out);
+    for (int i = 0; i < 3; ++i) a.out.s[2 + i] = d->out.s[2 + i] * d->stride[i];
+    a.has_base = additive;
+    if (additive) {
+      a.base = to_epi(d->base);
+      for (int i = 0; i < 3; ++i) a.base.s[2 + i] = d->base.s[2 + i] * d->stride[i];
+    }
+    int r = 0;
+    for (int dx = 0; dx < d->k[0]; ++dx)
+      for (int dy = 0; dy < d->k[1]; ++dy)
+        for (int dz = 0; dz < d->k[2]; ++dz, ++r) {
+          a.out_rep_off[r] = dx * d->out.s[2] + dy * d->out.s[3] + dz * d->out.s[4];
+          if (additive)
+            a.base_rep_off[r] = dx * d->base.s[2] + dy * d->base.s[3] + dz * d->base.s[4];
+        }
+    a.w = d->w_packed;
+    a.bias = d->bias;
+    a.scale = additive ? d->base_scale : nullptr;
+    a.act = d->act;
+    a.alpha = d->alpha;
+    return run_tc(a, s);
+  }
+  GatherDeconvParams p;
+  memset(&p, 0, sizeof(p));
+  p.in = to_dview(d->in);
+  p.out = to_dview(d->out);
+  p.has_base = additive;
+  if (additive) p.base = to_dview(d->base);
+  p.w = static_cast<const float *>(d->w_packed);
+  p.bias = d->bias;
+  p.scale = additive ? d->base_scale : nullptr;
+  p.cin = d->cin;
+  p.cout = d->cout;
+  p.kx = d->k[0];
+  p.ky = d->k[1];
+  p.kz = d->k[2];
+  p.sx = d->stride[0];
+  p.sy = d->stride[1];
+  p.sz = d->stride[2];
+  p.act = d->act;
+  p.alpha = d->alpha;
+  return launch_deconv_gather(p, s);
+}
+
+// ------------------------------------------------------------------ ops
+
+static int same_shape(const vxb_tensor *a, const vxb_tensor *b, const char *what) {
+  if (a->n != b->n || a->c != b->c || a->x != b->x || a->y != b->y || a->z != b->z)
+    return set_error(VXB_EINVAL, "%s: shape mismatch", what);
+  return VXB_OK;
+}
+
+int vxb_pool3d(const vxb_tensor *in, const vxb_tensor *out, const int window[3],
+               const int stride[3], int mode, void *stream) {
+  int rc;
+  if ((rc = check_view(in, "pool.in")) || (rc = check_view(out, "pool.out"))) return rc;
+  if (mode != VXB_POOL_MAX && mode != VXB_POOL_AVG) return set_error(VXB_EINVAL, "pool: mode");
+  const int ie[3] = {in->x, in->y, in->z}, oe[3] = {out->x, out->y, out->z};
+  for (int i = 0; i < 3; ++i) {
+    if (window[i] < 1 || stride[i] < 1 || window[i] > ie[i])
+      return set_error(VXB_EINVAL, "pool: bad window/stride on axis %d", i);
+    if ((ie[i] - window[i]) / stride[i] + 1 != oe[i])
+      return set_error(VXB_EINVAL, "pool: output extent mismatch on axis %d", i);
+  }
+  if (in->n != out->n || in->c != out->c) return set_error(VXB_EINVAL, "pool: n/c mismatch");
+  return launch_pool(to_dview(*in), to_dview(*out), window, stride, mode, as_stream(stream));
+}
+
+int vxb_eltwise(const vxb_tensor *a, const vxb_tensor *b, const vxb_tensor *out, int op,
+                void *stream) {
+  int rc;
+  if ((rc = check_view(a, "eltwise.a")) || (rc = check_view(b, "eltwise.b")) ||
+      (rc = check_view(out, "eltwise.out")))
+    return rc;
+  if ((rc = same_shape(a, b, "eltwise")) || (rc = same_shape(a, out, "eltwise"))) return rc;
+  if (op < 0 || op > 2) return set_error(VXB_EINVAL, "eltwise: op %d", op);
+  return launch_eltwise(to_dview(*a), to_dview(*b), to_dview(*out), op, as_stream(stream));
+}
+
+int vxb_affine_act(const vxb_tensor *in, const vxb_tensor *out, const float *mult,
+                   const float *add, int act, float alpha, void *stream) {
+  int rc;
+  if ((rc = check_view(in, "affine.in")) || (rc = check_view(out, "affine.out"))) return rc;
+  if ((rc = same_shape(in, out, "affine_act"))) return rc;
+  if (act < 0 || act > 3) return set_error(VXB_EINVAL, "affine_act: act %d", act);
+  return launch_affine_act(to_dview(*in), to_dview(*out), mult, add, act, alpha,
+                           as_stream(stream));
+}
+
+int vxb_mergecrop(const vxb_tensor *a, const vxb_tensor *b, const vxb_tensor *out, void *stream) {
+  int rc;
+  if ((rc = check_view(a, "mergecrop.a")) || (rc = check_view(b, "mergecrop.b")) ||
+      (rc = check_view(out, "mergecrop.out")))
+    return rc;
+  const int ea[3] = {a->x, a->y, a->z}, eb[3] = {b->x, b->y, b->z};
+  const int eo[3] = {out->x, out->y, out->z};
+  int oa[3], ob[3];
+  for (int i = 0; i < 3; ++i) {
+    int common = std::min(ea[i], eb[i]);
+    if (eo[i] != common) return set_error(VXB_EINVAL, "mergecrop: output extent mismatch");
+    oa[i] = (ea[i] - common) / 2;  // shapes.crop_offsets: floor
+    ob[i] = (eb[i] - common) / 2;
+  }
+  if (out->c != a->c + b->c || a->n != b->n || out->n != a->n)
+    return set_error(VXB_EINVAL, "mergecrop: fmap/batch mismatch");
+  return launch_mergecrop(to_dview(*a), to_dview(*b), to_dview(*out), oa, ob, as_stream(stream));
+}
+
+int vxb_pad_copy(const vxb_tensor *in, const vxb_tensor *out, const int pads[3], void *stream) {
+  int rc;
+  if ((rc = check_view(in, "pad.in")) || (rc = check_view(out, "pad.out"))) return rc;
+  if (out->x != in->x + 2 * pads[0] || out->y != in->y + 2 * pads[1] ||
+      out->z != in->z + 2 * pads[2] || in->c != out->c || in->n != out->n)
+    return set_error(VXB_EINVAL, "pad_copy: shape mismatch");
+  return launch_pad_copy(to_dview(*in), to_dview(*out), pads, as_stream(stream));
+}
+
+int vxb_copy(const vxb_tensor *src, const vxb_tensor *dst, void *stream) {
+  int rc;
+  if ((rc = check_view(src, "copy.src")) || (rc = check_view(dst, "copy.dst"))) return rc;
+  if ((rc = same_shape(src, dst, "copy"))) return rc;
+  return launch_copy(to_dview(*src), to_dview(*dst), as_stream(stream));
+}
+
+int vxb_zero(const vxb_tensor *t, void *stream) {
+  int rc;
+  if ((rc = check_view(t, "zero"))) return rc;
+  return launch_zero(to_dview(*t), as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+// vxb_internal.h — host/device shared parameter blocks and helpers.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include "../../include/vxb.h"
+
+namespace vxb {
+
+constexpr int LANES = 8;          // fmaps per chunk (blocked.py DEFAULT_SIMD_WIDTH)
+constexpr int TILE_Y = 16;        // output tile rows along y per 128-row MMA
+constexpr int TILE_Z = 8;         // output tile along z (one 8-row core-matrix group)
+constexpr int SLAB_ROW_BYTES = 32;  // one B row: 16 bf16 of K
+constexpr int MAX_REPS = 8;
+
+// Epilogue view of an output / base tensor, element strides.
+struct EpiView {
+  void *data;
+  long long s[5];   // batch, chunk (or channel when !blocked), x, y, z
+  int dtype;        // VXB_BF16 / VXB_F32
+  int blocked;
+};
+
+// Parameters of the tcgen05 implicit-GEMM convolution kernel.
+struct TcParams {
+  int nb;                      // batch
+  int ox, oy, oz;              // output extents
+  int tiles_x, tiles_y, tiles_z;
+  int n_tiles, reps, total_tiles;
+  int bx;                      // x-slices per CTA tile (each slice = 128 MMA rows)
+  int nt;                      // N per tile (multiple of 16)
+  int acc_stages;              // TMEM accumulator stages
+  int kx, ky, kz;
+  int hx, hy, hz;              // halo tile extents
+  int pad[3];
+  // input segments (fused concat): chunk counts, crop offsets, batch chunk stride
+  int seg_chunks[2];
+  int seg_off[2][3];
+  int seg_bstride[2];          // chunk-index stride between batches in the TMA map
+  int n_groups;
+  int chunk_bytes;             // bytes of one TMA'd chunk array (hx*hy*hz*16)
+  int chunk_stride;            // smem distance between the two chunk arrays of a stage
+  int chunk_slots;             // chunk arrays per A stage (1 or 2)
+  int a_stage_bytes, b_stage_bytes;
+  int na, nb_stages;           // ring depths
+  int bsteps;                  // K steps per B stage
+  int resident;                // weights loaded once, kept in smem
+  const uint8_t *w;
+  long long w_ntile_stride, w_rep_stride;   // bytes
+  const float *bias, *scale;
+  EpiView out, base;
+  long long out_rep_off[MAX_REPS], base_rep_off[MAX_REPS];
+  int cout, act;
+  float alpha;
+  int has_base;
+};
+
+struct TcMaps {
+  CUtensorMap m[2];
+};
+
+
+// ---- CUDA-core kernels (ops.cu)
+struct DView {
+  void *data;
+  long long s[5];
+  int dtype, blocked;
+  int n, c, x, y, z;
+};
+
+struct DirectParams {
+  DView in, out, base;
+  const float *w, *bias, *scale;
+  int cin, cout, kx, ky, kz, sx, sy, sz, px, py, pz;
+  int act, has_base;
+  float alpha;
+  int tiles_x, tiles_y, tiles_z;
+  int hx, hy, hz;  // staged input patch extents
+};
+
+struct SubParams {
+  DView in, out, base;
+  const float *w, *bias, *scale;  // w: standard (cout, cin, kx, ky, kz)
+  int cin, cout, kx, ky, kz, sx, sy, sz;
+  int ib, ob, x0, y0, z0, ex, ey, ez, first, last, act, has_base;
+  float alpha;
+};
+
+struct GatherDeconvParams {
+  DView in, out, base;
+  const float *w, *bias, *scale;  // standard (cout, cin, kx, ky, kz)
+  int cin, cout, kx, ky, kz, sx, sy, sz, act, has_base;
+  float alpha;
+};
+
+int launch_copy(const DView &src, const DView &dst, cudaStream_t s);
+int launch_zero(const DView &dst, cudaStream_t s);
+int launch_pool(const DView &in, const DView &out, const int *w, const int *st, int mode,
+                cudaStream_t s);
+int launch_eltwise(const DView &a, const DView &b, const DView &out, int op, cudaStream_t s);
+int launch_affine_act(const DView &in, const DView &out, const float *m, const float *a, int act,
+                      float alpha, cudaStream_t s);
+int launch_mergecrop(const DView &a, const DView &b, const DView &out, const int *oa,
+                     const int *ob, cudaStream_t s);
+int launch_pad_copy(const DView &in, const DView &out, const int *pads, cudaStream_t s);
+int launch_conv_direct(DirectParams p, cudaStream_t s);
+int launch_subimage(const SubParams &p, cudaStream_t s);
+int launch_deconv_gather(const GatherDeconvParams &p, cudaStream_t s);
+
+// ---- tensor-core conv (conv3d_tc.cu)
+size_t tc_smem_bytes(const TcParams &p);
+int launch_conv3d_tc(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t stream);
+constexpr int DCO_DIRECT = 16;  // output fmaps per direct-conv CTA
+
+// status helpers (vxb_abi.cu)
+int set_error(int code, const char *fmt, ...);
+int check_cuda(cudaError_t e, const char *what);
+
+}  // namespace vxb
