@@ -128,7 +128,8 @@ typedef struct vxb_deconv_desc {
   int32_t stride[3];
   int32_t act;
   float alpha;
-  int32_t reserved[8];
+  int32_t path;            /* 0 = auto, VXB_PATH_TC (k == stride), VXB_PATH_DIRECT (gather) */
+  int32_t reserved[7];
 } vxb_deconv_desc;
 
 /* ---- library ---- */
@@ -165,9 +166,10 @@ int vxb_conv3d_subimage(const vxb_conv_desc *d, const float *w_std, int in_chunk
                         int first, int last, void *stream);
 
 /* ---- deconvolution ---- */
-size_t vxb_deconv_weights_bytes(int cin, int cout, const int k[3], const int stride[3]);
+size_t vxb_deconv_weights_bytes(int cin, int cout, const int k[3], const int stride[3],
+                                int path);
 int vxb_deconv_pack_weights(const float *w, int cin, int cout, const int k[3],
-                            const int stride[3], void *dst, size_t dst_bytes);
+                            const int stride[3], int path, void *dst, size_t dst_bytes);
 int vxb_deconv3d(const vxb_deconv_desc *d, void *stream);
 
 /* ---- bandwidth kernels (ops.py) ---- */

@@ -71,7 +71,8 @@ class VxbDeconvDesc(ctypes.Structure):
         ("stride", c_int32 * 3),
         ("act", c_int32),
         ("alpha", c_float),
-        ("reserved", c_int32 * 8),
+        ("path", c_int32),
+        ("reserved", c_int32 * 7),
     ]
 
 
@@ -92,8 +93,9 @@ SIGNATURES = [
     ("vxb_conv3d", c_int, [POINTER(VxbConvDesc), c_void_p]),
     ("vxb_conv3d_subimage", c_int,
      [POINTER(VxbConvDesc), c_void_p, c_int, c_int, I3, I3, c_int, c_int, c_void_p]),
-    ("vxb_deconv_weights_bytes", c_size_t, [c_int, c_int, I3, I3]),
-    ("vxb_deconv_pack_weights", c_int, [c_void_p, c_int, c_int, I3, I3, c_void_p, c_size_t]),
+    ("vxb_deconv_weights_bytes", c_size_t, [c_int, c_int, I3, I3, c_int]),
+    ("vxb_deconv_pack_weights", c_int,
+     [c_void_p, c_int, c_int, I3, I3, c_int, c_void_p, c_size_t]),
     ("vxb_deconv3d", c_int, [POINTER(VxbDeconvDesc), c_void_p]),
     ("vxb_pool3d", c_int, [TP, TP, I3, I3, c_int, c_void_p]),
     ("vxb_eltwise", c_int, [TP, TP, TP, c_int, c_void_p]),

@@ -595,13 +595,17 @@ int vxb_conv3d_subimage(const vxb_conv_desc *d, const float *w_std, int in_chunk
 
 // ------------------------------------------------------------------ deconv
 
-static bool deconv_tc(const int k[3], const int stride[3]) {
+static bool deconv_tc_ok(const int k[3], const int stride[3]) {
   return k[0] == stride[0] && k[1] == stride[1] && k[2] == stride[2] &&
          k[0] * k[1] * k[2] <= MAX_REPS;
 }
+static bool deconv_tc(const int k[3], const int stride[3], int path) {
+  return path != VXB_PATH_DIRECT && deconv_tc_ok(k, stride);
+}
 
-size_t vxb_deconv_weights_bytes(int cin, int cout, const int k[3], const int stride[3]) {
-  if (deconv_tc(k, stride)) {
+size_t vxb_deconv_weights_bytes(int cin, int cout, const int k[3], const int stride[3],
+                                int path) {
+  if (deconv_tc(k, stride, path)) {
     int one[3] = {1, 1, 1};
     return static_cast<size_t>(k[0] * k[1] * k[2]) * tc_bytes_per_rep(tc_layout(cin, 0, cout, one));
   }
@@ -609,11 +613,13 @@ size_t vxb_deconv_weights_bytes(int cin, int cout, const int k[3], const int str
 }
 
 int vxb_deconv_pack_weights(const float *w, int cin, int cout, const int k[3], const int stride[3],
-                            void *dst, size_t dst_bytes) {
+                            int path, void *dst, size_t dst_bytes) {
   if (!w || !dst) return set_error(VXB_EINVAL, "deconv pack: null pointer");
-  size_t need = vxb_deconv_weights_bytes(cin, cout, k, stride);
+  if (path == VXB_PATH_TC && !deconv_tc_ok(k, stride))
+    return set_error(VXB_EUNSUPPORTED, "tensor-core deconv needs k == stride, <= 8 taps");
+  size_t need = vxb_deconv_weights_bytes(cin, cout, k, stride, path);
   if (dst_bytes < need) return set_error(VXB_EINVAL, "deconv pack: need %zu bytes", need);
-  if (!deconv_tc(k, stride)) {
+  if (!deconv_tc(k, stride, path)) {
     memcpy(dst, w, need);
     return VXB_OK;
   }
@@ -648,7 +654,9 @@ int vxb_deconv3d(const vxb_deconv_desc *d, void *stream) {
       return set_error(VXB_EINVAL, "deconv3d: output extent mismatch on axis %d", i);
   }
   cudaStream_t s = as_stream(stream);
-  if (deconv_tc(d->k, d->stride)) {
+  if (d->path == VXB_PATH_TC && !deconv_tc_ok(d->k, d->stride))
+    return set_error(VXB_EUNSUPPORTED, "tensor-core deconv needs k == stride, <= 8 taps");
+  if (deconv_tc(d->k, d->stride, d->path)) {
     TcLaunch a;
     memset(&a, 0, sizeof(a));
     a.in[0] = &d->in;

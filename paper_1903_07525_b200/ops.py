@@ -137,9 +137,11 @@ class PackedDeconv:
     cout: int
     k: tuple
     stride: tuple
+    path: int = 0
 
 
-def pack_deconv(kernel, bias, *, stride, base_scale=None, device=None) -> PackedDeconv:
+def pack_deconv(kernel, bias, *, stride, base_scale=None, force_gather=False,
+                device=None) -> PackedDeconv:
     """Pack a (cout, cin, kx, ky, kz) deconv bank (oracle.py:67-93 orientation)."""
     import torch
     L = _lib.lib()
@@ -147,14 +149,16 @@ def pack_deconv(kernel, bias, *, stride, base_scale=None, device=None) -> Packed
     cout, cin = int(w.shape[0]), int(w.shape[1])
     k = tuple(int(v) for v in w.shape[2:])
     stride = tuple(int(s) for s in stride)
-    nbytes = L.vxb_deconv_weights_bytes(cin, cout, _lib.i3(k), _lib.i3(stride))
+    path = _lib.PATH_DIRECT if force_gather else 0
+    nbytes = L.vxb_deconv_weights_bytes(cin, cout, _lib.i3(k), _lib.i3(stride), path)
     host = np.zeros(nbytes, dtype=np.uint8)
     _lib.check(L.vxb_deconv_pack_weights(w.ctypes.data, cin, cout, _lib.i3(k), _lib.i3(stride),
-                                         host.ctypes.data, nbytes), "vxb_deconv_pack_weights")
+                                         path, host.ctypes.data, nbytes),
+               "vxb_deconv_pack_weights")
     dev = device or torch.device("cuda", torch.cuda.current_device())
     scale = None if base_scale is None else device_vector(base_scale, cout, dev)
     return PackedDeconv(torch.from_numpy(host).to(dev), device_vector(bias, cout, dev), scale,
-                        cin, cout, k, stride)
+                        cin, cout, k, stride, path)
 
 
 def deconv3d(x: DTensor, pk: PackedDeconv, out: DTensor, *, base: DTensor = None,
@@ -172,6 +176,7 @@ def deconv3d(x: DTensor, pk: PackedDeconv, out: DTensor, *, base: DTensor = None
     d.k = _lib.i3(pk.k)
     d.stride = _lib.i3(pk.stride)
     d.act, d.alpha = _act(fused_act)
+    d.path = pk.path
     _lib.check(L.vxb_deconv3d(ctypes.byref(d), stream or current_stream_handle()), "vxb_deconv3d")
 
 

@@ -1,0 +1,413 @@
+"""B200 plan execution (reference: executor.py:51-203).
+
+``PlanRunner(plan).run(inputs)`` keeps the reference's contract: inputs are a
+dict name -> standard (batch, fmap, x, y, z) array (or a bare array for a
+single-input plan), the result is a dict name -> standard float32 array, and
+bad inputs raise ``ExecutionError`` with the reference's messages.
+
+Binding (once):
+  * every step is lowered to one device op over ``DTensor`` views in HBM
+    (bf16, channel-blocked, S = 8): convolutions get their weights packed
+    for the tensor-core or CUDA-core path, BN/Scale coefficients are computed
+    in float64 exactly like executor._bn_coefficients (executor.py:44-49);
+  * Pad steps and zero-halo buffers (ir.eliminate_padding) become *virtual*
+    padding of the consuming convolution (TMA zero fill), so no pad copies
+    and no halo storage exist on the device;
+  * storage is assigned by liveness from a pool (like the reference arena,
+    plan.py:92-127) and allocated once;
+  * the whole forward pass (input pack, all steps, output unpack) is captured
+    into one CUDA graph.
+Running: H2D of the inputs into pinned/static buffers, one graph replay,
+D2H of the outputs.  ``run_device`` skips the host copies.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from . import ops as K
+from .device import DTensor, LANES, chunks, standard
+from .errors import ExecutionError, PlanError
+from .formats import (ROLE_BIAS, ROLE_BN_MEAN, ROLE_BN_VAR, ROLE_KERNEL, ROLE_SCALE_BETA,
+                      ROLE_SCALE_GAMMA)
+from .netspec import DEFAULT_ELU_ALPHA, LayerKind
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def bn_coefficients(mean, var, eps):
+    """executor._bn_coefficients (executor.py:44-49): fp64 then fp32."""
+    f = 1.0 / np.sqrt(np.asarray(var, np.float64) + eps)
+    return f.astype(np.float32), (-np.asarray(mean, np.float64) * f).astype(np.float32)
+
+
+class _Value:
+    """A logical tensor produced by one step (interior dims, no halo)."""
+
+    __slots__ = ("dims", "slot", "readers", "dt", "dtype")
+
+    def __init__(self, dims, dtype="bf16"):
+        self.dims = tuple(int(d) for d in dims)
+        self.slot = None
+        self.readers = 0
+        self.dt = None
+        self.dtype = dtype
+
+    @property
+    def nbytes(self):
+        n, c, x, y, z = self.dims
+        esz = 2 if self.dtype == "bf16" else 4
+        return n * chunks(c) * x * y * z * LANES * esz
+
+
+class PlanRunner:
+    """Executes one ExecutionPlan on one B200; reusable, deterministic."""
+
+    def __init__(self, plan, backend=None, *, device=None, use_graph=True, fuse_concat=True):
+        torch = _torch()
+        from .backend import resolve_device_backend
+        self.backend = resolve_device_backend(backend)
+        if not torch.cuda.is_available():
+            raise ExecutionError("the B200 backend needs a CUDA device; none is visible")
+        self.plan = plan
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self.use_graph = use_graph
+        self.precision = self.backend.precision
+        self.fuse_concat = fuse_concat and self.precision == "bf16"
+        self._conv_path = _lib.PATH_DIRECT if self.precision == "fp32" else 0
+        self.stream = torch.cuda.Stream(device=self.device)
+        with torch.cuda.device(self.device):
+            self._lower()
+            self._allocate()
+            self._bind()
+        self._graph = None
+        self.launches = len(self._calls)
+
+    # ------------------------------------------------------------ lowering
+    def _lower(self):
+        plan = self.plan
+        self._input_dims = {name: tuple(dims) for name, _, dims in plan.inputs}
+        cur: dict = {}       # buffer id -> value currently held
+        self._values = []
+        self._ops = []       # (kind, step, info dict)
+
+        def new_value(dims):
+            v = _Value(dims, self.precision)
+            self._values.append(v)
+            return v
+
+        self._in_values = {}
+        for name, bid, dims in plan.inputs:
+            v = new_value(dims)
+            cur[bid] = v
+            self._in_values[name] = v
+
+        def read(si, allow_halo=False):
+            v = cur.get(si.buffer)
+            if v is None:
+                raise PlanError("step reads buffer %d before it is written" % si.buffer)
+            halo = tuple((a - b) // 2 for a, b in zip(si.dims[2:], v.dims[2:]))
+            if min(halo) < 0 or tuple(si.dims[:2]) != v.dims[:2]:
+                raise PlanError("buffer %d read with dims %s, holds %s"
+                                % (si.buffer, si.dims, v.dims))
+            if any(halo) and not allow_halo:
+                raise PlanError("a %s step cannot read a zero-halo view" % "non-conv")
+            v.readers += 1
+            return v, halo
+
+        for st in plan.steps:
+            kind = st.kind
+            if kind is LayerKind.PAD:
+                v, halo = read(st.inputs[0], allow_halo=True)
+                v.readers -= 1  # an alias is not a read; its readers are counted later
+                cur[st.output.buffer] = v
+                continue
+            info = {}
+            if kind is LayerKind.CONVOLUTION:
+                v, halo = read(st.inputs[0], allow_halo=True)
+                info["x"], info["pad"] = v, halo
+            elif kind is LayerKind.MERGE_CROP:
+                info["a"], _ = read(st.inputs[0])
+                info["b"], _ = read(st.inputs[1])
+            else:
+                info["ins"] = [read(si)[0] for si in st.inputs]
+            if st.additive:
+                info["base"], _ = read(st.base)
+            out = new_value(st.output.dims)
+            info["out"] = out
+            cur[st.output.buffer] = out
+            self._ops.append((kind, st, info))
+        self._out_values = {}
+        for name, bid, dims in plan.outputs:
+            v = cur[bid]
+            if v.dims != tuple(dims):
+                raise PlanError("output %r dims %s, buffer holds %s" % (name, dims, v.dims))
+            v.readers += 1
+            self._out_values[name] = v
+        if self.fuse_concat:
+            self._fuse_mergecrop()
+
+    def _fuse_mergecrop(self):
+        """Zero-copy MergeCrop: a conv whose only input is a MergeCrop of two
+        chunk-aligned tensors reads both directly as two K segments (fused
+        concat).  The MergeCrop output is never stored."""
+        producers = {id(info["out"]): i for i, (_, _, info) in enumerate(self._ops)}
+        drop = set()
+        for kind, st, info in self._ops:
+            if kind is not LayerKind.CONVOLUTION:
+                continue
+            src = producers.get(id(info["x"]))
+            if src is None:
+                continue
+            mkind, mst, minfo = self._ops[src]
+            if mkind is not LayerKind.MERGE_CROP or minfo["out"].readers != 1:
+                continue
+            if any(info["pad"]) or minfo["a"].dims[1] % LANES:
+                continue
+            stride = tuple(st.params.get("stride", (1, 1, 1)))
+            if stride != (1, 1, 1):
+                continue
+            a, b, m = minfo["a"], minfo["b"], minfo["out"]
+            info["segments"] = (a, b,
+                                tuple((sa - sm) // 2 for sa, sm in zip(a.dims[2:], m.dims[2:])),
+                                tuple((sb - sm) // 2 for sb, sm in zip(b.dims[2:], m.dims[2:])))
+            m.readers = 0
+            info["x"] = None
+            drop.add(src)
+        if drop:
+            self._ops = [op for i, op in enumerate(self._ops) if i not in drop]
+
+    # ------------------------------------------------------------ storage
+    def _reads(self, info):
+        if "segments" in info:
+            rs = [info["segments"][0], info["segments"][1]]
+        elif "x" in info:
+            rs = [info["x"]]
+        else:
+            rs = []
+        rs += [info[k] for k in ("a", "b", "base") if k in info]
+        return rs + list(info.get("ins", []))
+
+    def _allocate(self):
+        """Liveness-based slot assignment (best fit by bytes, like the
+        reference arena plan.py:92-127), then one allocation per slot."""
+        torch = _torch()
+        last = {}
+        for v in self._in_values.values():
+            last[id(v)] = -1
+        for i, (_, _, info) in enumerate(self._ops):
+            for r in self._reads(info):
+                last[id(r)] = i
+            last.setdefault(id(info["out"]), i)
+        for v in self._out_values.values():
+            last[id(v)] = len(self._ops)
+        slots, free = [], []
+
+        def grab(v):
+            need = v.nbytes
+            fits = [q for q in free if slots[q] >= need]
+            if fits:
+                q = min(fits, key=lambda k: (slots[k], k))
+            elif free:
+                q = max(free, key=lambda k: slots[k])
+                slots[q] = need
+            else:
+                slots.append(need)
+                return len(slots) - 1
+            free.remove(q)
+            return q
+
+        for v in self._in_values.values():
+            v.slot = grab(v)
+        live = list(self._in_values.values())
+        for i, (_, _, info) in enumerate(self._ops):
+            info["out"].slot = grab(info["out"])
+            live.append(info["out"])
+            keep = []
+            for v in live:
+                if last.get(id(v), -1) <= i:
+                    free.append(v.slot)
+                else:
+                    keep.append(v)
+            live = keep
+        self._storage = [torch.empty(max(b, 16), dtype=torch.uint8, device=self.device)
+                         for b in slots]
+        self.device_bytes = sum(slots)
+        for v in self._values:
+            if v.slot is None:
+                continue
+            n, c, x, y, z = v.dims
+            td = torch.bfloat16 if v.dtype == "bf16" else torch.float32
+            numel = n * chunks(c) * x * y * z * LANES
+            t = self._storage[v.slot].view(td)[:numel].view(n, chunks(c), x, y, z, LANES)
+            v.dt = DTensor(t, c, True)
+        # network boundary: fp32 standard staging tensors (device + pinned host)
+        self._in_std = {name: torch.empty(self._input_dims[name], dtype=torch.float32,
+                                          device=self.device)
+                        for name in self._in_values}
+        self._out_std = {name: torch.empty(v.dims, dtype=torch.float32, device=self.device)
+                         for name, v in self._out_values.items()}
+        self._in_pinned = {name: torch.empty(t.shape, dtype=torch.float32, pin_memory=True)
+                           for name, t in self._in_std.items()}
+        self._out_pinned = {name: torch.empty(t.shape, dtype=torch.float32, pin_memory=True)
+                            for name, t in self._out_std.items()}
+
+    # ------------------------------------------------------------ binding
+    def _bind(self):
+        w = self.plan.weights
+        dev = self.device
+        calls = []
+        for name, v in self._in_values.items():
+            src = standard(self._in_std[name])
+            calls.append(lambda s=src, d=v.dt: _copy(s, d))
+        for kind, st, info in self._ops:
+            out = info["out"].dt
+            if kind is LayerKind.CONVOLUTION:
+                base = info["base"].dt if "base" in info else None
+                scale = st.base_scale if st.additive else None
+                kern = w.tensor(st.name, ROLE_KERNEL)
+                stride = tuple(st.params.get("stride", (1, 1, 1)))
+                if "segments" in info:
+                    a, b, oa, ob = info["segments"]
+                    pk = K.pack_conv(kern, w.tensor(st.name, ROLE_BIAS), stride=stride,
+                                     base_scale=scale, cin_split=a.dims[1], device=dev)
+                    calls.append(lambda a=a.dt, b=b.dt, pk=pk, out=out, base=base, oa=oa, ob=ob,
+                                 act=st.fused_act: K.conv3d(a, pk, out, base=base, fused_act=act,
+                                                            x2=b, off=oa, off2=ob))
+                else:
+                    pk = K.pack_conv(kern, w.tensor(st.name, ROLE_BIAS), stride=stride,
+                                     base_scale=scale, path=self._conv_path, device=dev)
+                    calls.append(lambda x=info["x"].dt, pk=pk, out=out, base=base,
+                                 pad=info["pad"], act=st.fused_act:
+                                 K.conv3d(x, pk, out, pad=pad, base=base, fused_act=act))
+            elif kind is LayerKind.DECONVOLUTION:
+                base = info["base"].dt if "base" in info else None
+                scale = st.base_scale if st.additive else None
+                pk = K.pack_deconv(w.tensor(st.name, ROLE_KERNEL), w.tensor(st.name, ROLE_BIAS),
+                                   stride=tuple(st.params["stride"]), base_scale=scale,
+                                   force_gather=self.precision == "fp32", device=dev)
+                calls.append(lambda x=info["ins"][0].dt, pk=pk, out=out, base=base,
+                             act=st.fused_act: K.deconv3d(x, pk, out, base=base, fused_act=act))
+            elif kind is LayerKind.POOLING:
+                calls.append(lambda x=info["ins"][0].dt, out=out, p=st.params:
+                             K.pool3d(x, out, p["window"], p["stride"], p["mode"]))
+            elif kind is LayerKind.ELTWISE:
+                a, b = info["ins"]
+                calls.append(lambda a=a.dt, b=b.dt, out=out, op=st.params["op"]:
+                             K.eltwise(a, b, out, op))
+            elif kind is LayerKind.MERGE_CROP:
+                calls.append(lambda a=info["a"].dt, b=info["b"].dt, out=out:
+                             K.mergecrop(a, b, out))
+            elif kind in (LayerKind.BATCH_NORM, LayerKind.SCALE):
+                if kind is LayerKind.BATCH_NORM:
+                    m, a = bn_coefficients(w.tensor(st.name, ROLE_BN_MEAN),
+                                           w.tensor(st.name, ROLE_BN_VAR), w.bn_eps(st.name))
+                else:
+                    m = w.tensor(st.name, ROLE_SCALE_GAMMA)
+                    a = w.tensor(st.name, ROLE_SCALE_BETA)
+                from .device import device_vector
+                md, ad = device_vector(m, device=dev), device_vector(a, device=dev)
+                calls.append(lambda x=info["ins"][0].dt, out=out, md=md, ad=ad:
+                             K.affine_act(x, out, md, ad))
+            elif kind in (LayerKind.RELU, LayerKind.ELU, LayerKind.SIGMOID):
+                act = kind.value.lower()
+                alpha = float(st.params.get("alpha", DEFAULT_ELU_ALPHA))
+                calls.append(lambda x=info["ins"][0].dt, out=out, act=act, alpha=alpha:
+                             K.affine_act(x, out, None, None, act, alpha))
+            else:
+                raise ExecutionError("plan step %r has unrunnable kind %s" % (st.name, kind))
+        for name, v in self._out_values.items():
+            dst = standard(self._out_std[name])
+            calls.append(lambda s=v.dt, d=dst: _copy(s, d))
+        self._calls = calls
+
+    # ------------------------------------------------------------ running
+    def _launch_all(self):
+        for c in self._calls:
+            c()
+
+    def _replay(self):
+        torch = _torch()
+        if not self.use_graph:
+            with torch.cuda.stream(self.stream):
+                self._launch_all()
+            return
+        if self._graph is None:
+            with torch.cuda.stream(self.stream):
+                self._launch_all()          # warm-up (first launches configure kernels)
+            self.stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.stream):
+                self._launch_all()
+            self._graph = g
+        with torch.cuda.stream(self.stream):
+            self._graph.replay()
+
+    def _normalize(self, inputs):
+        if not isinstance(inputs, dict):
+            if len(self._input_dims) != 1:
+                raise ExecutionError("plan has %d inputs, pass a dict" % len(self._input_dims))
+            inputs = {next(iter(self._input_dims)): inputs}
+        for name, want in self._input_dims.items():
+            if name not in inputs:
+                raise ExecutionError("missing value for input %r" % name)
+            got = tuple(inputs[name].shape)
+            if got != tuple(want):
+                raise ExecutionError("input %r has shape %s, plan wants %s"
+                                     % (name, got, tuple(want)))
+        return inputs
+
+    def run_device(self, inputs):
+        """Device-resident forward: inputs/outputs are CUDA fp32 NCDHW tensors.
+        Work is enqueued on ``self.stream``; the returned tensors are the
+        runner's static output buffers (valid until the next call)."""
+        torch = _torch()
+        inputs = self._normalize(inputs)
+        cs = torch.cuda.current_stream(self.device)
+        self.stream.wait_stream(cs)
+        with torch.cuda.stream(self.stream):
+            for name, t in inputs.items():
+                self._in_std[name].copy_(t, non_blocking=True)
+        self._replay()
+        cs.wait_stream(self.stream)
+        return dict(self._out_std)
+
+    def run(self, inputs) -> dict:
+        """Reference-compatible forward (executor.py:168-198): host in, host out.
+        Inputs go host -> pinned staging -> HBM, outputs the reverse."""
+        torch = _torch()
+        inputs = self._normalize(inputs)
+        for name, arr in inputs.items():
+            self._in_pinned[name].numpy()[...] = np.asarray(arr, dtype=np.float32)
+        with torch.cuda.stream(self.stream):
+            for name, t in self._in_pinned.items():
+                self._in_std[name].copy_(t, non_blocking=True)
+        self._replay()
+        with torch.cuda.stream(self.stream):
+            for name, t in self._out_std.items():
+                self._out_pinned[name].copy_(t, non_blocking=True)
+        self.stream.synchronize()
+        return {name: t.numpy().copy() for name, t in self._out_pinned.items()}
+
+    @property
+    def h2d_bytes(self) -> int:
+        return sum(t.numel() * 4 for t in self._in_std.values())
+
+    @property
+    def d2h_bytes(self) -> int:
+        return sum(t.numel() * 4 for t in self._out_std.values())
+
+
+def _copy(src: DTensor, dst: DTensor):
+    from .device import copy
+    copy(src, dst)
+
+
+def execute(plan, inputs, backend=None) -> dict:
+    """One-shot convenience (executor.py:201-203)."""
+    return PlanRunner(plan, backend=backend).run(inputs)

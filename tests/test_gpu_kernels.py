@@ -1,0 +1,288 @@
+"""Device kernels vs the CPU oracle, through the C ABI (libvxb.so).
+
+Tolerances (stated per precision):
+  * bf16 tensor-core path: compared with the fp32 oracle run on the same
+    bf16-rounded operands, so the only differences are fp32 accumulation
+    order and the final bf16 store: max-normalised error <= 8e-3.
+  * fp32 CUDA-core path (backend b200-fp32): <= 2e-5 absolute on O(1) data,
+    the reference's own 1e-5-class gate (test_kernels.py:140-156).
+  * pool / crop / concat / layout copies: bit-exact.
+"""
+
+import numpy as np
+import pytest
+
+from vxb_testutil import cuda_ready
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not cuda_ready(), reason="needs CUDA + libvxb.so")]
+
+from oracle import ref_numpy as R  # noqa: E402
+
+BF16_TOL = 8e-3
+
+
+def _dev():
+    from paper_1903_07525_b200 import device as D, ops as K
+    return D, K
+
+
+def _conv_bf16(x, w, b, pad, act=None, base=None, scale=None, out_dtype="bf16"):
+    import torch
+    D, K = _dev()
+    xd = D.to_device_blocked(x)
+    osp = tuple(s + 2 * p - k + 1 for s, p, k in zip(x.shape[2:], pad, w.shape[2:]))
+    out = D.empty_blocked(x.shape[0], w.shape[0], osp, out_dtype)
+    bd = D.to_device_blocked(base) if base is not None else None
+    pk = K.pack_conv(w, b, base_scale=scale)
+    K.conv3d(xd, pk, out, pad=pad, base=bd, fused_act=(act, 1.0) if act else None)
+    torch.cuda.synchronize()
+    return D.to_host_standard(out), pk.path
+
+
+def _ref_bf16(x, w, b, pad, act=None, base=None, scale=None):
+    q = R.bf16_round
+    y = R.conv3d(q(x), q(w), np.zeros_like(b), 1, pad)
+    init = b.reshape(1, -1, 1, 1, 1).astype(np.float32)
+    if base is not None:
+        s = np.ones_like(b) if scale is None else scale
+        init = init + s.reshape(1, -1, 1, 1, 1) * q(base)
+    y = init + y
+    return R.activation(y, act) if act else y
+
+
+CASES = [
+    # cin, cout, spatial, k, pad, act, base
+    (16, 16, (4, 16, 8), (3, 3, 3), (1, 1, 1), "relu", False),
+    (8, 8, (6, 20, 12), (3, 3, 3), (1, 1, 1), None, False),
+    (8, 16, (5, 17, 9), (1, 3, 3), (0, 1, 1), "elu", False),
+    (32, 32, (9, 33, 17), (3, 3, 3), (1, 1, 1), "elu", True),
+    (64, 64, (5, 19, 23), (3, 3, 3), (1, 1, 1), "elu", False),
+    (128, 128, (3, 16, 16), (3, 3, 3), (1, 1, 1), "relu", False),
+    (1, 32, (10, 20, 12), (3, 3, 3), (0, 0, 0), "relu", False),
+    (36, 28, (6, 20, 19), (3, 3, 3), (1, 1, 1), "elu", True),
+    (28, 3, (6, 20, 19), (1, 1, 1), (0, 0, 0), "sigmoid", False),
+    (80, 80, (6, 24, 24), (1, 3, 3), (0, 1, 1), "elu", True),
+    (256, 512, (3, 11, 11), (3, 3, 3), (0, 0, 0), "relu", False),
+    (5, 7, (8, 8, 8), (3, 3, 3), (0, 0, 0), None, False),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "c%d-%d_k%s" % (c[0], c[1], c[3]))
+def test_tc_conv_matches_oracle(case):
+    cin, cout, sp, k, pad, act, use_base = case
+    rng = np.random.default_rng(cin * 1000 + cout)
+    x = rng.uniform(-1, 1, (1, cin) + sp).astype(np.float32)
+    w = (rng.standard_normal((cout, cin) + k) * np.sqrt(2.0 / (cin * np.prod(k)))).astype(np.float32)
+    b = (rng.standard_normal(cout) * 0.1).astype(np.float32)
+    osp = tuple(s + 2 * p - kk + 1 for s, p, kk in zip(sp, pad, k))
+    base = rng.uniform(-1, 1, (1, cout) + osp).astype(np.float32) if use_base else None
+    scale = rng.uniform(0.5, 1.5, cout).astype(np.float32) if use_base else None
+    got, path = _conv_bf16(x, w, b, pad, act, base, scale)
+    assert path == 1  # tensor-core path
+    want = _ref_bf16(x, w, b, pad, act, base, scale)
+    mx, l2 = R.normalized_error(got, want)
+    assert mx < BF16_TOL and l2 < 3e-3, (mx, l2)
+
+
+def test_tc_conv_fp32_output_and_batch2():
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-1, 1, (2, 16, 4, 18, 10)).astype(np.float32)
+    w = (rng.standard_normal((24, 16, 3, 3, 3)) * 0.1).astype(np.float32)
+    b = rng.standard_normal(24).astype(np.float32)
+    got, _ = _conv_bf16(x, w, b, (1, 1, 1), None, out_dtype="fp32")
+    want = _ref_bf16(x, w, b, (1, 1, 1))
+    mx, _ = R.normalized_error(got, want)
+    assert mx < 1e-5
+
+
+def test_fused_concat_conv_matches_mergecrop_then_conv():
+    import torch
+    D, K = _dev()
+    rng = np.random.default_rng(3)
+    a = rng.uniform(-1, 1, (1, 16, 12, 22, 14)).astype(np.float32)   # skip (larger)
+    bb = rng.uniform(-1, 1, (1, 24, 8, 18, 10)).astype(np.float32)   # up
+    w = (rng.standard_normal((8, 40, 3, 3, 3)) * 0.1).astype(np.float32)
+    bias = rng.standard_normal(8).astype(np.float32)
+    m = R.mergecrop(R.bf16_round(a), R.bf16_round(bb))
+    want = R.activation(R.conv3d(m, R.bf16_round(w), bias), "relu")
+    ad, bd = D.to_device_blocked(a), D.to_device_blocked(bb)
+    out = D.empty_blocked(1, 8, (6, 16, 8))
+    pk = K.pack_conv(w, bias, cin_split=16)
+    K.conv3d(ad, pk, out, x2=bd, off=(2, 2, 2), off2=(0, 0, 0), fused_act=("relu", 1.0))
+    torch.cuda.synchronize()
+    mx, _ = R.normalized_error(D.to_host_standard(out), want)
+    assert mx < BF16_TOL
+
+
+@pytest.mark.parametrize("stride,pad", [((1, 1, 1), (1, 1, 1)), ((2, 2, 2), (0, 0, 0)),
+                                        ((1, 2, 3), (1, 0, 1))])
+def test_direct_fp32_path_matches_oracle_1e5(stride, pad):
+    """reference gate (test_kernels.py:149-156): strided convs, fp32, 1e-5."""
+    import torch
+    D, K = _dev()
+    from paper_1903_07525_b200 import _lib
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((2, 8, 7, 8, 9)).astype(np.float32)
+    w = (rng.standard_normal((8, 8, 3, 3, 3)) * 0.2).astype(np.float32)
+    b = rng.standard_normal(8).astype(np.float32)
+    want = R.conv3d(x, w, b, stride, pad)
+    xd = D.to_device_blocked(x, dtype="fp32")
+    out = D.empty_blocked(2, 8, want.shape[2:], "fp32")
+    pk = K.pack_conv(w, b, stride=stride, path=_lib.PATH_DIRECT)
+    K.conv3d(xd, pk, out, pad=pad)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(D.to_host_standard(out), want, atol=2e-5, rtol=0)
+
+
+def test_known_answers_through_backend_api():
+    """test_kernels.py:80-136 known answers via Backend.conv3d / subimage."""
+    from paper_1903_07525_b200 import get_backend
+    from paper_1903_07525_b200.kernels_b200 import ConvInvocation, SubImageTask
+    from oracle.ref_engine import to_blocked, from_blocked
+    for name in ("b200", "b200-fp32"):
+        be = get_backend(name)
+        one = np.ones((1, 1, 3, 3, 3), np.float32)
+        out = np.zeros((1, 1, 1, 1, 1, 8), np.float32)
+        inv = ConvInvocation(to_blocked(one), 1, one, np.zeros(8, np.float32), out, 1)
+        be.conv3d(inv)
+        assert out[0, 0, 0, 0, 0, 0] == 27.0 and not out[..., 1:].any()
+        # bias + base: 10.5 (test_kernels.py:91-99)
+        z = np.zeros((1, 1, 3, 3, 3), np.float32)
+        base = to_blocked(np.full((1, 1, 1, 1, 1), 10.0, np.float32))
+        out = np.zeros((1, 1, 1, 1, 1, 8), np.float32)
+        inv = ConvInvocation(to_blocked(z), 1, z, np.array([0.5] + [0] * 7, np.float32), out, 1,
+                             additive=True, base_view=base)
+        be.conv3d(inv)
+        assert out[0, 0, 0, 0, 0, 0] == 10.5
+        # epilogue order relu(bias + scale*base) (test_kernels.py:170-181)
+        base = to_blocked(np.full((1, 1, 1, 1, 1), -4.0, np.float32))
+        for bias, want in ((1.0, 0.0), (3.0, 1.0)):
+            out = np.zeros((1, 1, 1, 1, 1, 8), np.float32)
+            inv = ConvInvocation(to_blocked(z), 1, z, np.array([bias] + [0] * 7, np.float32), out,
+                                 1, additive=True, base_view=base,
+                                 base_scale=np.array([0.5] + [0] * 7, np.float32),
+                                 fused_act=("relu", 0.0))
+            be.conv3d(inv)
+            assert out[0, 0, 0, 0, 0, 0] == want
+    # sub-image chaining == full conv (test_kernels.py:103-115), fp32 primitive
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((1, 16, 5, 5, 5)).astype(np.float32)
+    k = (rng.standard_normal((8, 16, 3, 3, 3)) * 0.2).astype(np.float32)
+    bias = rng.standard_normal(8).astype(np.float32)
+    out = np.zeros((1, 1, 3, 3, 3, 8), np.float32)
+    inv = ConvInvocation(to_blocked(x), 16, k, bias, out, 8)
+    be = get_backend("b200")
+    for ib, (first, last) in enumerate([(True, False), (False, True)]):
+        be.subimage(SubImageTask(ib, 0, (0, 0, 0), (3, 3, 3), first, last), inv)
+    np.testing.assert_allclose(from_blocked(out, 8), R.conv3d(x, k, bias), atol=1e-5, rtol=0)
+
+
+def test_tail_lanes_zero_and_halo_clean():
+    """test_kernels.py:198-222: sigmoid tails stay 0; writing into a halo
+    interior leaves the halo untouched."""
+    from paper_1903_07525_b200 import get_backend
+    from paper_1903_07525_b200.kernels_b200 import ConvInvocation
+    from oracle.ref_engine import to_blocked
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((1, 5, 6, 6, 6)).astype(np.float32)
+    k = (rng.standard_normal((5, 5, 3, 3, 3)) * 0.2).astype(np.float32)
+    b = rng.standard_normal(5).astype(np.float32)
+    alloc = np.full((1, 1, 6, 6, 6, 8), 7.0, np.float32)
+    interior = alloc[:, :, 1:5, 1:5, 1:5, :]
+    inv = ConvInvocation(to_blocked(x), 5, k, np.pad(b, (0, 3)), interior, 5,
+                         fused_act=("sigmoid", 0.0))
+    get_backend("b200").conv3d(inv)
+    assert not interior[..., 5:].any()
+    ring = alloc.copy()
+    ring[:, :, 1:5, 1:5, 1:5, :] = 7.0
+    assert (ring == 7.0).all()
+    want = R.activation(R.conv3d(R.bf16_round(x), R.bf16_round(k), b), "sigmoid")
+    got = interior.transpose(0, 1, 5, 2, 3, 4).reshape(1, 8, 4, 4, 4)[:, :5]
+    assert R.normalized_error(got, want)[0] < BF16_TOL
+
+
+def test_conv_deterministic():
+    rng = np.random.default_rng(2)
+    x = rng.uniform(-1, 1, (1, 32, 6, 20, 20)).astype(np.float32)
+    w = (rng.standard_normal((32, 32, 3, 3, 3)) * 0.1).astype(np.float32)
+    b = np.zeros(32, np.float32)
+    a1, _ = _conv_bf16(x, w, b, (1, 1, 1))
+    a2, _ = _conv_bf16(x, w, b, (1, 1, 1))
+    np.testing.assert_array_equal(a1, a2)
+
+
+def test_pool_bit_exact_and_avg():
+    import torch
+    D, K = _dev()
+    rng = np.random.default_rng(4)
+    x = R.bf16_round(rng.standard_normal((2, 13, 6, 7, 9)).astype(np.float32))
+    for win in ((2, 2, 2), (1, 2, 2)):
+        want = R.pool3d(x, win, win, "max")
+        xd = D.to_device_blocked(x)
+        out = D.empty_blocked(2, 13, want.shape[2:])
+        K.pool3d(xd, out, win, win, "max")
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(D.to_host_standard(out), want)
+    want = R.pool3d(x, 2, 2, "avg")
+    out = D.empty_blocked(2, 13, want.shape[2:], "fp32")
+    K.pool3d(D.to_device_blocked(x, dtype="fp32"), out, (2, 2, 2), (2, 2, 2), "avg")
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(D.to_host_standard(out), want)
+
+
+def test_mergecrop_eltwise_affine_exact(golden_ops):
+    import torch
+    D, K = _dev()
+    g = golden_ops
+    a = D.to_device_blocked(g["mc_a"], dtype="fp32")
+    b = D.to_device_blocked(g["mc_b"], dtype="fp32")
+    out = D.empty_blocked(1, 9, (7, 7, 7), "fp32")
+    K.mergecrop(a, b, out)
+    for op in ("add", "mul", "div"):
+        o = D.empty_blocked(1, 5, (3, 3, 3), "fp32")
+        K.eltwise(D.to_device_blocked(g["elt_a"], dtype="fp32"),
+                  D.to_device_blocked(g["elt_b"], dtype="fp32"), o, op)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(D.to_host_standard(o), g["elt_" + op])
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(D.to_host_standard(out), g["mc_y"])
+    x = D.to_device_blocked(g["bn_x"], dtype="fp32")
+    o = D.empty_blocked(1, 5, (4, 4, 4), "fp32")
+    K.affine_act(x, o, D.device_vector(g["bn_gamma"]), D.device_vector(g["bn_beta"]))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(D.to_host_standard(o), g["sc_y"])
+    K.affine_act(x, o, None, None, "elu", 0.7)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(D.to_host_standard(o), g["elu_y"], atol=1e-6, rtol=0)
+
+
+def test_layout_round_trip_exact(rng):
+    D, _ = _dev()
+    x = R.bf16_round(rng.standard_normal((2, 11, 3, 5, 7)).astype(np.float32))
+    np.testing.assert_array_equal(D.to_host_standard(D.to_device_blocked(x)), x)
+    t = D.to_device_blocked(x)
+    assert not t.t[:, 1, ..., 3:].float().abs().sum().item()   # tail lanes are zero
+
+
+@pytest.mark.parametrize("i", [0, 1, 2])
+def test_deconv_golden(golden_ops, i):
+    import torch
+    D, K = _dev()
+    g = golden_ops
+    x, w, b, s = g["deconv%d_x" % i], g["deconv%d_w" % i], g["deconv%d_b" % i], g["deconv%d_s" % i]
+    want_fp32 = g["deconv%d_y" % i]
+    # fp32 gather path: reference gate
+    pk = K.pack_deconv(w, b, stride=tuple(s), force_gather=True)
+    out = D.empty_blocked(1, w.shape[0], want_fp32.shape[2:], "fp32")
+    K.deconv3d(D.to_device_blocked(x, dtype="fp32"), pk, out)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(D.to_host_standard(out), want_fp32, atol=2e-5, rtol=0)
+    # bf16 tensor-core path when k == stride
+    if tuple(s) == tuple(w.shape[2:]):
+        pk = K.pack_deconv(w, b, stride=tuple(s))
+        out = D.empty_blocked(1, w.shape[0], want_fp32.shape[2:])
+        K.deconv3d(D.to_device_blocked(x), pk, out)
+        torch.cuda.synchronize()
+        want = R.deconv3d(R.bf16_round(x), R.bf16_round(w), b, tuple(s))
+        assert R.normalized_error(D.to_host_standard(out), want)[0] < BF16_TOL

@@ -1,0 +1,112 @@
+"""Whole-network parity on the GPU: PlanRunner (CUDA graph) and run_tiled.
+
+Oracles: the reference's own outputs for three zoo nets (golden, produced by
+voxplan.oracle.ref_run / voxplan.PlanRunner), and oracle/ref_numpy for the
+BASELINE config networks at reduced sizes.  Tolerances:
+  * backend b200-fp32 (fp32 CUDA cores): max-normalised <= 1e-5 vs ref_run;
+  * backend b200 (bf16 storage, tcgen05): vs the bf16-storage plan oracle
+    (same roundings) <= 2e-2 max-normalised / 1e-2 L2 (rounding flips of
+    intermediate bf16 values propagate); vs the fp32 oracle the per-config
+    bound is stated in DESIGN.md and checked here on the small configs.
+"""
+
+import numpy as np
+import pytest
+
+from vxb_testutil import cuda_ready
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not cuda_ready(), reason="needs CUDA + libvxb.so")]
+
+import paper_1903_07525_b200 as P  # noqa: E402
+from paper_1903_07525_b200 import configs as C, formats, plan as vplan, prototxt  # noqa: E402
+from oracle import ref_numpy as R  # noqa: E402
+
+
+def _net(g, i):
+    spec = prototxt.parse_network(bytes(g["net%d_prototxt" % i]).decode())
+    store = formats.parse_weights(bytes(g["net%d_pznw" % i]))
+    return spec, store
+
+
+@pytest.mark.parametrize("i", [0, 1, 2])
+def test_reference_plan_fp32_matches_reference(golden_nets, i):
+    """The reference's own compiled plan (halo buffers, Pad steps, fused
+    flags) executed by the B200 runner in fp32 equals the reference output."""
+    plan = vplan.parse_plan(bytes(golden_nets["net%d_plan" % i]))
+    runner = P.PlanRunner(plan, backend="b200-fp32")
+    (name, got), = runner.run(golden_nets["net%d_x" % i]).items()
+    mx, l2 = R.normalized_error(got, golden_nets["net%d_ref" % i])
+    assert mx < 1e-5, mx
+
+
+@pytest.mark.parametrize("i", [0, 1, 2])
+def test_reference_plan_bf16(golden_nets, i):
+    plan = vplan.parse_plan(bytes(golden_nets["net%d_plan" % i]))
+    runner = P.PlanRunner(plan, backend="b200")
+    x = golden_nets["net%d_x" % i]
+    (name, got), = runner.run(x).items()
+    emu = R.run_plan(plan, x, storage="bf16")[name]
+    mx, l2 = R.normalized_error(got, emu)
+    assert mx < 2e-2 and l2 < 1e-2, (mx, l2)
+    mx, l2 = R.normalized_error(got, golden_nets["net%d_ref" % i])
+    assert l2 < 3e-2, l2
+
+
+def _small(cfg):
+    return {1: lambda: C.config1(),
+            3: lambda: C.config3(spatial=(8, 32, 32)),
+            4: lambda: C.config4(spatial=(68, 68, 68), base=8, levels=3),
+            5: lambda: C.config5(patch=(6, 48, 48), feats=(8, 12, 16, 20))}[cfg]()
+
+
+@pytest.mark.parametrize("cfg", [1, 3, 4, 5])
+@pytest.mark.parametrize("backend", ["b200", "b200-fp32"])
+def test_config_networks(cfg, backend):
+    spec, store = _small(cfg)
+    plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
+    lo, hi = C.input_range(cfg)
+    x = C.make_input(spec, 0, lo, hi)
+    runner = P.PlanRunner(plan, backend=backend)
+    (name, got), = runner.run(x).items()
+    ref = R.ref_run(spec, store, x)[name]
+    mx, l2 = R.normalized_error(got, ref)
+    if backend == "b200-fp32":
+        assert mx < 2e-5, mx
+    else:
+        emu = R.run_plan(plan, x, storage="bf16")[name]
+        emx, el2 = R.normalized_error(got, emu)
+        assert emx < 2e-2 and el2 < 1e-2, (emx, el2)
+        assert l2 < 3e-2, l2
+
+
+def test_runner_graph_replay_deterministic_and_validates():
+    spec, store = _small(3)
+    plan, _ = P.compile_network(spec, store, fixpoint=True)
+    runner = P.PlanRunner(plan)
+    x = C.make_input(spec, 1)
+    a = runner.run(x)["out_elu"]
+    b = runner.run({"data": x})["out_elu"]
+    np.testing.assert_array_equal(a, b)
+    with pytest.raises(P.ExecutionError):
+        runner.run({"nope": x})
+    with pytest.raises(P.ExecutionError):
+        runner.run(x[:, :, :4])
+
+
+def test_run_tiled_equals_manual_assembly():
+    """test_acceptance.py:343-362 / test_tiling.py:111-142: tiled output equals
+    the manual assembly of per-patch runs, exactly (each tile is a
+    deterministic function of its input window)."""
+    spec, store = C.config5(patch=(4, 32, 32), feats=(8, 12, 16))
+    plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
+    vol = np.random.default_rng(0).uniform(0, 1, (1, 1, 7, 80, 70)).astype(np.float32)
+    grid = P.grid_for(plan, vol.shape[2:], overlap=0)
+    got = P.run_tiled(plan, vol, grid=grid)
+    runner = P.PlanRunner(plan)
+    want = np.empty_like(got)
+    for t in grid.tiles:
+        res = runner.run(vol[(slice(None), slice(None)) + t.input_window(grid.patch_in)])["prob"]
+        want[(slice(None), slice(None)) + t.out_window] = res[(slice(None), slice(None))
+                                                              + t.local_window]
+    np.testing.assert_array_equal(got, want)

@@ -1,0 +1,156 @@
+"""CPU-only checks: the C-ABI library loads and exports every declared symbol,
+host-side packing, backend registry rules, tiling geometry vs the reference,
+and the multi-rank tile partition over a gloo process group."""
+
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+from vxb_testutil import GOLDEN, ROOT
+
+from paper_1903_07525_b200 import _lib, backend, tiling
+from paper_1903_07525_b200.errors import ExecutionError, TileError
+
+
+def _declared_symbols():
+    hdr = open(os.path.join(ROOT, "include", "vxb.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(vxb_[a-z_0-9]+)\s*\(",
+                                 hdr, re.M)))
+
+
+def test_header_symbols_all_bound_and_exported():
+    syms = _declared_symbols()
+    assert len(syms) >= 20
+    bound = {name for name, _, _ in _lib.SIGNATURES}
+    assert set(syms) == bound, set(syms) ^ bound
+    if not _lib.library_available():
+        pytest.skip("libvxb.so not built")
+    L = _lib.lib()
+    for s in syms:
+        assert hasattr(L, s)
+    assert L.vxb_abi_version() == 1
+
+
+def test_host_packing_sizes_and_selection():
+    if not _lib.library_available():
+        pytest.skip("libvxb.so not built")
+    L = _lib.lib()
+    k3, s1 = _lib.i3((3, 3, 3)), _lib.i3((1, 1, 1))
+    assert L.vxb_conv_select(16, 16, k3, s1) == _lib.PATH_TC
+    assert L.vxb_conv_select(16, 16, k3, _lib.i3((2, 2, 2))) == _lib.PATH_DIRECT
+    # C16 -> N tile 16, one channel-pair group of 27 steps, 32 B rows
+    assert L.vxb_conv_weights_bytes(16, 16, k3, s1, 0) == 27 * 16 * 32
+    # odd chunk (Cin=8): z-pair steps 3*3*2
+    assert L.vxb_conv_weights_bytes(8, 16, k3, s1, 0) == 18 * 16 * 32
+    # Cout 512 -> two N tiles of 256
+    assert L.vxb_conv_weights_bytes(256, 512, k3, s1, 0) == 2 * 16 * 27 * 256 * 32
+    w = np.random.default_rng(0).standard_normal((16, 16, 3, 3, 3)).astype(np.float32)
+    n = L.vxb_conv_weights_bytes(16, 16, k3, s1, 0)
+    dst = np.zeros(n, np.uint8)
+    assert L.vxb_conv_pack_weights(w.ctypes.data, 16, 16, k3, s1, 0, dst.ctypes.data, n) == 0
+    # slab for step 0 (tap 0,0,0): row n, k-half h, lane l at (n/8)*256 + h*128 + (n%8)*16 + 2l
+    bf = dst.view(np.uint16)
+    from oracle.ref_numpy import bf16_round
+    for (co, ci) in [(0, 0), (5, 3), (9, 12), (15, 15)]:
+        h, l = ci // 8, ci % 8
+        off = ((co // 8) * 256 + h * 128 + (co % 8) * 16 + 2 * l) // 2
+        val = np.array([bf[off]], np.uint16).astype(np.uint32) << 16
+        assert val.view(np.float32)[0] == bf16_round(w[co, ci, 0, 0, 0])
+    assert L.vxb_conv_pack_weights(w.ctypes.data, 16, 16, k3, s1, 0, dst.ctypes.data, 10) != 0
+    assert b"need" in L.vxb_last_error()
+
+
+def test_backend_registry_rules(monkeypatch):
+    with pytest.raises(ExecutionError):
+        backend.get_backend("nope")
+    monkeypatch.setattr(_lib, "LIB_PATH", "/nonexistent/libvxb.so")
+    monkeypatch.setattr(_lib, "_LIB", None)
+    with pytest.raises(ExecutionError):
+        backend.get_backend("b200")
+    with pytest.raises(ExecutionError):
+        _lib.lib()
+    assert backend.available_backends() == ()
+    monkeypatch.setenv(backend.BACKEND_ENV, "bogus")
+    with pytest.raises(ExecutionError):
+        backend.get_backend()
+
+
+def test_tiles_match_reference_geometry():
+    for case in json.load(open(os.path.join(GOLDEN, "tiles.json"))):
+        g = tiling.plan_tiles(case["volume"], case["patch_in"], case["patch_out"], case["overlap"])
+        assert list(g.counts) == case["counts"]
+        assert list(g.volume_out) == case["volume_out"]
+        got = [[list(t.index), list(t.in_lo), list(t.keep_lo), list(t.keep_hi), list(t.out_lo)]
+               for t in g.tiles]
+        assert got == case["tiles"]
+
+
+@pytest.mark.parametrize("vol,pin,pout,ov", [
+    ((40, 40, 40), (16, 16, 16), (16, 16, 16), None),
+    ((37, 50, 29), (12, 20, 9), (8, 16, 5), None),
+    ((31, 33, 35), (10, 12, 14), (6, 8, 10), 8),
+    ((18, 1024, 1024), (18, 192, 192), (18, 192, 192), 0),
+])
+def test_exactly_once_coverage(vol, pin, pout, ov):
+    g = tiling.plan_tiles(vol, pin, pout, ov)
+    cover = np.zeros(g.volume_out, np.int32)
+    for t in g.tiles:
+        cover[t.out_window] += 1
+        assert all(0 <= a < b <= p for a, b, p in zip(t.keep_lo, t.keep_hi, pout))
+    assert (cover == 1).all()
+
+
+def test_tile_errors():
+    with pytest.raises(TileError):
+        tiling.plan_tiles((10, 10, 10), (12, 8, 8), (12, 8, 8))
+    with pytest.raises(TileError):
+        tiling.plan_tiles((20, 20, 20), (8, 8, 8), (6, 6, 6), 3)   # odd surplus
+    with pytest.raises(TileError):
+        tiling.plan_tiles((20, 20, 20), (8, 8, 8), (4, 4, 4), 2)   # below shrinkage
+
+
+def test_partition_blocks():
+    for n, parts in [(288, 1), (288, 2), (288, 8), (7, 3), (5, 8)]:
+        seen = []
+        for r in range(parts):
+            seen += list(tiling.partition(n, parts, r))
+        assert seen == list(range(n))
+
+
+def _rank_main(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = tiling.plan_tiles((128, 1024, 1024), (18, 192, 192), (18, 192, 192), 0)
+    mine = [g.tiles[i] for i in tiling.partition(len(g.tiles), world, rank)]
+    vox = sum(int(np.prod(np.array(t.keep_hi) - np.array(t.keep_lo))) for t in mine)
+    t = torch.tensor([float(vox), float(rank + 1)])
+    tot = t.clone()
+    dist.all_reduce(tot[:1], op=dist.ReduceOp.SUM)
+    mx = t[1:].clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)    # bench.py: max-over-ranks timing
+    if rank == 0:
+        q.put((tot[0].item(), mx.item()))
+    dist.destroy_process_group()
+
+
+def test_two_rank_tile_partition_gloo():
+    import multiprocessing as mp
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    total, mx = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+    assert total == 128 * 1024 * 1024
+    assert mx == 2.0
