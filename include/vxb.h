@@ -137,6 +137,9 @@ int vxb_abi_version(void);
 const char *vxb_last_error(void);
 /* number of SMs of the current device, or -1 */
 int vxb_device_sms(void);
+/* debug: with VXB_TC_DEBUG=1 the tensor-core conv records per-tile phase
+ * timestamps (ns, [cta][tile<64][8]) of its last launch; copies up to count */
+size_t vxb_debug_read(unsigned long long *host, size_t count);
 
 /* ---- convolution (kernels_cy.conv3d / _kernels.conv3d) ---- */
 int vxb_conv_select(int cin, int cout, const int k[3], const int stride[3]);

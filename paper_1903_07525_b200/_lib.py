@@ -84,6 +84,7 @@ SIGNATURES = [
     ("vxb_abi_version", c_int, []),
     ("vxb_last_error", c_char_p, []),
     ("vxb_device_sms", c_int, []),
+    ("vxb_debug_read", c_size_t, [c_void_p, c_size_t]),
     ("vxb_conv_select", c_int, [c_int, c_int, I3, I3]),
     ("vxb_conv_weights_bytes", c_size_t, [c_int, c_int, I3, I3, c_int]),
     ("vxb_conv_pack_weights", c_int, [c_void_p, c_int, c_int, I3, I3, c_int, c_void_p, c_size_t]),

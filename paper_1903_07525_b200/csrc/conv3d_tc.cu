@@ -72,6 +72,17 @@ __device__ __forceinline__ TileCoord decode_tile(const TcParams &p, int t) {
   return c;
 }
 
+// Fast activations for bf16 outputs: relative error < 3e-5, far below the
+// bf16 store rounding (3.9e-3); fp32 outputs use the libm forms below.
+__device__ __forceinline__ float fast_expm1(float v) {
+  return fabsf(v) < 1e-2f ? fmaf(0.5f * v, v, v) : __expf(v) - 1.f;
+}
+__device__ __forceinline__ float apply_act_fast(float v, int act, float alpha) {
+  if (act == VXB_ACT_RELU) return fmaxf(v, 0.f);
+  if (act == VXB_ACT_ELU) return v > 0.f ? v : alpha * fast_expm1(v);
+  if (act == VXB_ACT_SIGMOID) return __fdividef(1.f, 1.f + __expf(-v));
+  return v;
+}
 __device__ __forceinline__ float apply_act(float v, int act, float alpha) {
   if (act == VXB_ACT_RELU) return v > 0.f ? v : 0.f;
   if (act == VXB_ACT_ELU) return v > 0.f ? v : alpha * expm1f(v);
@@ -140,16 +151,49 @@ __device__ __forceinline__ void store8(const EpiView &v, long long off, bool blo
   }
 }
 
-__global__ void __launch_bounds__(192, 1)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void dbg_mark(const TcParams &p, int it, int slot) {
+  if (p.dbg && it < 64) p.dbg[(static_cast<size_t>(blockIdx.x) * 64 + it) * 8 + slot] = gtimer();
+}
+
+constexpr int EPI_WARPS = 12;
+constexpr int TC_THREADS = 64 + 32 * EPI_WARPS;
+
+// Byte offsets inside the dynamic smem block (all derivable from p).
+struct SmemMap {
+  uint32_t a, b, bias, scale, tab_pair, tab_odd, bars;
+};
+__host__ __device__ inline SmemMap smem_map(const TcParams &p) {
+  SmemMap m;
+  m.a = 0;
+  m.b = p.na * p.a_stage_bytes;
+  m.bias = m.b + p.nb_stages * p.b_stage_bytes;
+  const uint32_t cpad = p.n_tiles * p.nt;
+  m.scale = m.bias + cpad * 4;
+  m.tab_pair = m.scale + cpad * 4;
+  m.tab_odd = m.tab_pair + p.kx * p.ky * p.kz * 4;
+  m.bars = (m.tab_odd + p.kx * p.ky * ((p.kz + 1) / 2) * 4 + 15) & ~15u;
+  return m;
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
     conv3d_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const SmemMap sm = smem_map(p);
 
-  // smem carve-up: [A stages][B stages][barriers][tmem ptr]
-  uint8_t *a_buf = smem;
-  uint8_t *b_buf = smem + p.na * p.a_stage_bytes;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(b_buf + p.nb_stages * p.b_stage_bytes);
+  uint8_t *a_buf = smem + sm.a;
+  uint8_t *b_buf = smem + sm.b;
+  float *s_bias = reinterpret_cast<float *>(smem + sm.bias);
+  float *s_scale = reinterpret_cast<float *>(smem + sm.scale);
+  uint32_t *tab_pair = reinterpret_cast<uint32_t *>(smem + sm.tab_pair);
+  uint32_t *tab_odd = reinterpret_cast<uint32_t *>(smem + sm.tab_odd);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + sm.bars);
   uint64_t *a_full = bars;
   uint64_t *a_empty = a_full + p.na;
   uint64_t *b_full = a_empty + p.na;
@@ -162,13 +206,30 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t tmem_cols = 32;
   while (tmem_cols < static_cast<uint32_t>(acc_cols * p.acc_stages)) tmem_cols <<= 1;
 
-  // zero the guard bytes behind every chunk array (read, with zero weight,
-  // by the odd-chunk z-pair steps)
+  // one-time setup by all threads: guard bytes behind every chunk array
+  // (read with zero weight by odd-chunk z-pair steps), per-fmap epilogue
+  // vectors, and the per-step A-operand byte offsets (no divisions later)
   for (int s = 0; s < p.na; ++s)
     for (int c = 0; c < p.chunk_slots; ++c) {
       uint8_t *g = a_buf + s * p.a_stage_bytes + c * p.chunk_stride + p.chunk_bytes;
       for (int i = threadIdx.x; i < 32; i += blockDim.x) reinterpret_cast<uint32_t *>(g)[i] = 0u;
     }
+  const int cpad = p.n_tiles * p.nt;
+  for (int c = threadIdx.x; c < cpad; c += blockDim.x) {
+    s_bias[c] = c < p.cout ? p.bias[c] : 0.f;
+    s_scale[c] = (c < p.cout && p.scale) ? p.scale[c] : 1.f;
+  }
+  {
+    const int kzh = (p.kz + 1) >> 1;
+    for (int t = threadIdx.x; t < p.kx * p.ky * p.kz; t += blockDim.x) {
+      int dz = t % p.kz, dy = (t / p.kz) % p.ky, dx = t / (p.kz * p.ky);
+      tab_pair[t] = ((dx * p.hy + dy) * p.hz + dz) * 16;
+    }
+    for (int t = threadIdx.x; t < p.kx * p.ky * kzh; t += blockDim.x) {
+      int dz = 2 * (t % kzh), dy = (t / kzh) % p.ky, dx = t / (kzh * p.ky);
+      tab_odd[t] = ((dx * p.hy + dy) * p.hz + dz) * 16;
+    }
+  }
   fence_proxy_async_smem();
 
   if (warp == 0 && lane == 0) {
@@ -184,7 +245,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&t_full[i], 1);
-      mbar_init(&t_empty[i], 4);
+      mbar_init(&t_empty[i], EPI_WARPS);
     }
     fence_mbar_init();
   }
@@ -202,7 +263,9 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       int a_st = 0, a_ph = 0, b_st = 0, b_ph = 0;
       bool first = true;
-      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+      int pit = 0;
+      const uint32_t slab = static_cast<uint32_t>(p.nt * SLAB_ROW_BYTES);
+      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++pit) {
         TileCoord tc = decode_tile(p, tile);
         const uint8_t *wbase = p.w + tc.rep * p.w_rep_stride + tc.nt * p.w_ntile_stride;
         long long step_base = 0;
@@ -210,13 +273,14 @@ __global__ void __launch_bounds__(192, 1)
         for (int g = 0; g < p.n_groups; ++g) {
           GroupInfo gi = group_info(p, g);
           mbar_wait(&a_empty[a_st], a_ph ^ 1);
+          if (g == 0) dbg_mark(p, pit, 0);
           mbar_expect_tx(&a_full[a_st], gi.nch * p.chunk_bytes);
           const int *off = p.seg_off[gi.seg];
-          int cx = tc.x0 - p.pad[0] + off[0];
-          int cy = tc.y0 - p.pad[1] + off[1];
-          int cz = (tc.z0 - p.pad[2] + off[2]) * LANES;
+          const int cx = tc.x0 - p.pad[0] + off[0];
+          const int cy = tc.y0 - p.pad[1] + off[1];
+          const int cz = (tc.z0 - p.pad[2] + off[2]) * LANES;
           for (int ci = 0; ci < gi.nch; ++ci) {
-            int chunk = tc.b * p.seg_bstride[gi.seg] + gi.chunk0 + ci;
+            const int chunk = tc.b * p.seg_bstride[gi.seg] + gi.chunk0 + ci;
             tma_load_4d(a_buf + a_st * p.a_stage_bytes + ci * p.chunk_stride, &maps.m[gi.seg],
                         &a_full[a_st], cz, cy, cx, chunk);
           }
@@ -226,12 +290,12 @@ __global__ void __launch_bounds__(192, 1)
           }
           if (!p.resident || first) {
             for (int s0 = 0; s0 < gi.steps; s0 += p.bsteps) {
-              int n = min(p.bsteps, gi.steps - s0);
-              uint32_t bytes = static_cast<uint32_t>(n * p.nt * SLAB_ROW_BYTES);
+              const int n = min(p.bsteps, gi.steps - s0);
+              const uint32_t bytes = n * slab;
               mbar_wait(&b_empty[b_st], b_ph ^ 1);
               mbar_expect_tx(&b_full[b_st], bytes);
-              bulk_load(b_buf + b_st * p.b_stage_bytes,
-                        wbase + (step_base + s0) * p.nt * SLAB_ROW_BYTES, bytes, &b_full[b_st]);
+              bulk_load(b_buf + b_st * p.b_stage_bytes, wbase + (step_base + s0) * slab, bytes,
+                        &b_full[b_st]);
               if (++b_st == p.nb_stages) {
                 b_st = 0;
                 b_ph ^= 1;
@@ -246,127 +310,170 @@ __global__ void __launch_bounds__(192, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    if (lane == 0) {
-      const uint32_t idesc = idesc_bf16(128, p.nt);
-      const uint32_t a_base0 = smem_u32(a_buf);
-      const uint32_t b_base0 = smem_u32(b_buf);
-      const uint32_t sbo_a = p.hz * 16;
-      const int kzh = (p.kz + 1) >> 1;
-      int a_st = 0, a_ph = 0, b_st = 0, b_ph = 0;
-      int it = 0;
-      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++it) {
-        const int acc = it % p.acc_stages;
-        const int aph = (it / p.acc_stages) & 1;
-        mbar_wait(&t_empty[acc], aph ^ 1);
+    // The whole warp walks the schedule (so descriptor arithmetic stays
+    // warp-uniform); one elected lane issues each tcgen05 instruction.
+    const uint32_t idesc = idesc_bf16(128, p.nt);
+    const uint32_t a_base0 = smem_u32(a_buf);
+    const uint32_t b_base0 = smem_u32(b_buf);
+    const uint32_t sbo_a = p.hz * 16;
+    const uint64_t slice_inc = static_cast<uint64_t>((p.hy * p.hz * 16) >> 4);
+    const uint64_t slab_inc = static_cast<uint64_t>((p.nt * SLAB_ROW_BYTES) >> 4);
+    int a_st = 0, a_ph = 0, b_st = 0, b_ph = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++it) {
+      const int acc = it % p.acc_stages;
+      mbar_wait(&t_empty[acc], ((it / p.acc_stages) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d_base = tmem_base + acc * acc_cols;
+      uint32_t accumulate = 0;
+      if (p.resident) b_st = 0;
+      for (int g = 0; g < p.n_groups; ++g) {
+        GroupInfo gi = group_info(p, g);
+        mbar_wait(&a_full[a_st], a_ph);
+        if (g == 0 && lane == 0) dbg_mark(p, it, 1);
         tc_fence_after();
-        const uint32_t d_base = tmem_base + acc * acc_cols;
-        uint32_t accumulate = 0;
-        if (p.resident) b_st = 0;
-        for (int g = 0; g < p.n_groups; ++g) {
-          GroupInfo gi = group_info(p, g);
-          mbar_wait(&a_full[a_st], a_ph);
-          tc_fence_after();
-          const uint32_t a_base = a_base0 + a_st * p.a_stage_bytes;
-          const uint32_t lbo_a = gi.nch == 2 ? static_cast<uint32_t>(p.chunk_stride) : 16u;
-          for (int s0 = 0; s0 < gi.steps; s0 += p.bsteps) {
-            int n = min(p.bsteps, gi.steps - s0);
-            if (p.resident) {
-              if (it == 0) mbar_wait(&b_full[b_st], 0);
-            } else {
-              mbar_wait(&b_full[b_st], b_ph);
-            }
-            tc_fence_after();
-            const uint32_t b_base = b_base0 + b_st * p.b_stage_bytes;
-            for (int i = 0; i < n; ++i) {
-              int t = s0 + i, dx, dy, dz;
-              if (gi.nch == 2) {
-                dz = t % p.kz;
-                dy = (t / p.kz) % p.ky;
-                dx = t / (p.kz * p.ky);
-              } else {
-                dz = 2 * (t % kzh);
-                dy = (t / kzh) % p.ky;
-                dx = t / (kzh * p.ky);
-              }
-              const uint64_t bdesc = smem_desc(b_base + i * p.nt * SLAB_ROW_BYTES, 128u, 256u);
-              const uint32_t tap_off = ((dx * p.hy + dy) * p.hz + dz) * 16;
-              for (int s = 0; s < p.bx; ++s) {
-                const uint32_t a_addr = a_base + tap_off + s * p.hy * p.hz * 16;
-                umma_bf16(d_base + s * p.nt, smem_desc(a_addr, lbo_a, sbo_a), bdesc, idesc,
-                          accumulate);
-              }
-              accumulate = 1;
-            }
-            if (!p.resident) umma_commit(&b_empty[b_st]);
-            if (++b_st == p.nb_stages) {
-              b_st = 0;
-              b_ph ^= 1;
-            }
+        const bool pair = gi.nch == 2;
+        const uint32_t *tab = pair ? tab_pair : tab_odd;
+        const uint64_t adesc0 =
+            smem_desc(a_base0 + a_st * p.a_stage_bytes, pair ? p.chunk_stride : 16u, sbo_a);
+        for (int s0 = 0; s0 < gi.steps; s0 += p.bsteps) {
+          const int n = min(p.bsteps, gi.steps - s0);
+          if (p.resident) {
+            if (it == 0) mbar_wait(&b_full[b_st], 0);
+          } else {
+            mbar_wait(&b_full[b_st], b_ph);
           }
-          umma_commit(&a_empty[a_st]);
-          if (++a_st == p.na) {
-            a_st = 0;
-            a_ph ^= 1;
+          tc_fence_after();
+          uint64_t bdesc = smem_desc(b_base0 + b_st * p.b_stage_bytes, 128u, 256u);
+          for (int i = 0; i < n; ++i, bdesc += slab_inc) {
+            uint64_t adesc = adesc0 + (tab[s0 + i] >> 4);
+            uint32_t d = d_base;
+            for (int s = 0; s < p.bx; ++s, adesc += slice_inc, d += p.nt)
+              umma_bf16_elect(d, adesc, bdesc, idesc, accumulate);
+            accumulate = 1;
+          }
+          if (!p.resident) umma_commit_elect(&b_empty[b_st]);
+          if (++b_st == p.nb_stages) {
+            b_st = 0;
+            b_ph ^= 1;
           }
         }
-        umma_commit(&t_full[acc]);
+        umma_commit_elect(&a_empty[a_st]);
+        if (++a_st == p.na) {
+          a_st = 0;
+          a_ph ^= 1;
+        }
       }
+      umma_commit_elect(&t_full[acc]);
+      if (lane == 0) dbg_mark(p, it, 2);
     }
     __syncwarp();
   } else {
-    // ===================== epilogue =====================
-    const int q = warp & 3;              // TMEM lane quarter this warp may access
-    const int row = q * 32 + lane;       // MMA row == TMEM lane
+    // ===================== epilogue (EPI_WARPS warps, EPI_WARPS/4 per quarter) ==
+    const int q = warp & 3;                   // TMEM lane quarter this warp may access
+    const int sub = (warp - 2) >> 2;          // which share of the work items
+    constexpr int NSUB = EPI_WARPS / 4;
+    const int row = q * 32 + lane;            // MMA row == TMEM lane
     const int yy = row >> 3, zz = row & 7;
+    const int cw = (p.nt % 32 == 0) ? 32 : 16;
+    const int col_items = p.nt / cw;
+    const int items = p.bx * col_items;
+    const EpiView &ov = p.out;
+    const EpiView &bvw = p.base;
+    const bool fast = ov.dtype == VXB_BF16 && ov.blocked;
     int it = 0;
     for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++it) {
       TileCoord tc = decode_tile(p, tile);
       const int acc = it % p.acc_stages;
-      mbar_wait(&t_full[acc], (it / p.acc_stages) & 1);
-      tc_fence_after();
       const int y = tc.y0 + yy, z = tc.z0 + zz;
-      const long long orep = p.out_rep_off[tc.rep];
-      const long long brep = p.base_rep_off[tc.rep];
-      for (int s = 0; s < p.bx; ++s) {
+      const bool yz_ok = y < p.oy && z < p.oz;
+      const long long orow = p.out_rep_off[tc.rep] + tc.b * ov.s[0] + y * ov.s[3] + z * ov.s[4];
+      const long long brow =
+          p.base_rep_off[tc.rep] + tc.b * bvw.s[0] + y * bvw.s[3] + z * bvw.s[4];
+      mbar_wait(&t_full[acc], (it / p.acc_stages) & 1);
+      if (warp == 2 && lane == 0) dbg_mark(p, it, 3);
+      tc_fence_after();
+      for (int item = sub; item < items; item += NSUB) {
+        const int s = item / col_items;
+        const int cc = (item % col_items) * cw;
         const int x = tc.x0 + s;
-        const bool valid = x < p.ox && y < p.oy && z < p.oz;
-        for (int cc = 0; cc < p.nt; cc += 16) {
-          float v[16];
-          tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * acc_cols +
-                        s * p.nt + cc,
-                    v);
-          if (!valid) continue;
+        const bool valid = yz_ok && x < p.ox;
+        const int cbase = tc.nt * p.nt + cc;   // first fmap of this item
+        const int nch = cw >> 3;
+        // residual operand, fetched before the TMEM load so the two overlap
+        float bv[32];
+        if (p.has_base) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c0 = tc.nt * p.nt + cc + h * 8;  // first fmap of this chunk
-            if (c0 >= p.cout) continue;
-            const int nvalid = min(8, p.cout - c0);
-            float r[8];
+          for (int h = 0; h < 4; ++h) {
+            float t8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            const int c0 = cbase + h * 8;
+            if (h < nch && valid && c0 < p.cout)
+              load8(bvw, brow + x * bvw.s[2] + (bvw.blocked ? (c0 >> 3) * bvw.s[1] : c0 * bvw.s[1]),
+                    bvw.blocked, t8);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) r[i] = (i < nvalid) ? p.bias[c0 + i] : 0.f;
-            if (p.has_base) {
-              float bv[8];
-              const EpiView &bvw = p.base;
-              long long boff = brep + tc.b * bvw.s[0] + x * bvw.s[2] + y * bvw.s[3] +
-                               z * bvw.s[4] + (bvw.blocked ? (c0 >> 3) * bvw.s[1] : c0 * bvw.s[1]);
-              load8(bvw, boff, bvw.blocked, bv);
+            for (int i = 0; i < 8; ++i) bv[h * 8 + i] = t8[i];
+          }
+        }
+        float v[32];
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                               acc * acc_cols + s * p.nt + cc;
+        if (cw == 32)
+          tmem_ld32(taddr, v);
+        else
+          tmem_ld16(taddr, *reinterpret_cast<float(*)[16]>(v));
+        if (!valid) continue;
+        const long long obase = orow + x * ov.s[2];
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                if (i < nvalid) r[i] += (p.scale ? p.scale[c0 + i] : 1.f) * bv[i];
+        for (int h = 0; h < 4; ++h) {
+          const int c0 = cbase + h * 8;
+          if (h >= nch || c0 >= p.cout) break;
+          const int nvalid = min(8, p.cout - c0);
+          const float4 b0 = *reinterpret_cast<const float4 *>(s_bias + c0);
+          const float4 b1 = *reinterpret_cast<const float4 *>(s_bias + c0 + 4);
+          float r[8] = {v[h * 8 + 0] + b0.x, v[h * 8 + 1] + b0.y, v[h * 8 + 2] + b0.z,
+                        v[h * 8 + 3] + b0.w, v[h * 8 + 4] + b1.x, v[h * 8 + 5] + b1.y,
+                        v[h * 8 + 6] + b1.z, v[h * 8 + 7] + b1.w};
+          if (p.has_base) {
+            const float4 s0 = *reinterpret_cast<const float4 *>(s_scale + c0);
+            const float4 s1 = *reinterpret_cast<const float4 *>(s_scale + c0 + 4);
+            const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) r[i] = fmaf(sc[i], bv[h * 8 + i], r[i]);
+          }
+          if (fast) {
+            switch (p.act) {
+              case VXB_ACT_RELU:
+#pragma unroll
+                for (int i = 0; i < 8; ++i) r[i] = fmaxf(r[i], 0.f);
+                break;
+              case VXB_ACT_ELU:
+#pragma unroll
+                for (int i = 0; i < 8; ++i) r[i] = r[i] > 0.f ? r[i] : p.alpha * fast_expm1(r[i]);
+                break;
+              case VXB_ACT_SIGMOID:
+#pragma unroll
+                for (int i = 0; i < 8; ++i) r[i] = __fdividef(1.f, 1.f + __expf(-r[i]));
+                break;
+              default:
+                break;
             }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) r[i] = apply_act(r[i], p.act, p.alpha);
+          }
+          if (nvalid < 8) {
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-              r[i] = (i < nvalid) ? apply_act(r[i] + v[h * 8 + i], p.act, p.alpha) : 0.f;
-            const EpiView &ov = p.out;
-            long long ooff = orep + tc.b * ov.s[0] + x * ov.s[2] + y * ov.s[3] + z * ov.s[4] +
-                             (ov.blocked ? (c0 >> 3) * ov.s[1] : c0 * ov.s[1]);
-            store8(ov, ooff, ov.blocked, nvalid, r);
+              if (i >= nvalid) r[i] = 0.f;
           }
+          store8(ov, obase + (ov.blocked ? (c0 >> 3) * ov.s[1] : c0 * ov.s[1]), ov.blocked,
+                 nvalid, r);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&t_empty[acc]);
+      if (warp == 2 && lane == 0) dbg_mark(p, it, 4);
     }
   }
 
@@ -380,9 +487,7 @@ __global__ void __launch_bounds__(192, 1)
 // ---------------------------------------------------------------- host side
 
 size_t tc_smem_bytes(const TcParams &p) {
-  return static_cast<size_t>(p.na) * p.a_stage_bytes +
-         static_cast<size_t>(p.nb_stages) * p.b_stage_bytes +
-         (2 * p.na + 2 * p.nb_stages + 4) * sizeof(uint64_t) + 16;
+  return smem_map(p).bars + (2 * p.na + 2 * p.nb_stages + 4) * sizeof(uint64_t) + 16;
 }
 
 int launch_conv3d_tc(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t stream) {
@@ -394,7 +499,7 @@ int launch_conv3d_tc(const TcParams &p, const TcMaps &maps, int grid, cudaStream
     if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(conv3d_tc)");
     configured = true;
   }
-  conv3d_tc_kernel<<<grid, 192, smem, stream>>>(p, maps);
+  conv3d_tc_kernel<<<grid, TC_THREADS, smem, stream>>>(p, maps);
   return check_cuda(cudaGetLastError(), "conv3d_tc_kernel launch");
 }
 

@@ -188,7 +188,7 @@ struct TcConfig {
 };
 
 static int tc_configure(const TcLayout &L, const int k[3], int ox, int reps, TcConfig &c) {
-  const int budget = 227 * 1024 - 512;
+  const int budget = 227 * 1024 - 6144;  // room for bias/scale/tap tables/barriers
   c.acc = env_int("VXB_TC_ACC", 2);
   if (c.acc != 1 && c.acc != 2) c.acc = 2;
   int bx_cap = env_int("VXB_TC_BX", 8);
@@ -208,7 +208,7 @@ static int tc_configure(const TcLayout &L, const int k[3], int ox, int reps, TcC
     c.chunk_stride = round_up(c.chunk_bytes + 128, 128);
     c.chunk_slots = any_pair ? 2 : 1;
     c.a_stage = c.chunk_slots * c.chunk_stride;
-    c.na = 2;
+    c.na = std::max(2, std::min(6, env_int("VXB_TC_NA", 2)));
     // resident weights: whole filter bank of the (single) N tile in smem
     long long total_w = L.steps * slab;
     c.resident = 0;
@@ -298,6 +298,9 @@ static int make_input_map(const vxb_tensor &t, int hx, int hy, int hz, CUtensorM
                      (unsigned long long)dims[3]);
   return VXB_OK;
 }
+
+static void *g_dbg = nullptr;
+static const size_t kDbgBytes = 1024 * 64 * 8 * sizeof(unsigned long long);
 
 static int device_sms() {
   static int sms = -1;
@@ -392,8 +395,18 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   p.alpha = a.alpha;
   int sms = device_sms();
   if (sms <= 0) return set_error(VXB_ECUDA, "no CUDA device");
+  if (env_int("VXB_TC_DEBUG", 0)) {
+    if (!g_dbg) {
+      cudaError_t e = cudaMalloc(&g_dbg, kDbgBytes);
+      if (e != cudaSuccess) return check_cuda(e, "debug buffer");
+    }
+    cudaMemsetAsync(g_dbg, 0, kDbgBytes, stream);
+    p.dbg = static_cast<unsigned long long *>(g_dbg);
+  }
   uint32_t tmem_cols = 32;
   while (tmem_cols < static_cast<uint32_t>(c.bx * L.nt * c.acc)) tmem_cols <<= 1;
+  c.smem = tc_smem_bytes(p);
+  if (c.smem > 227 * 1024) return set_error(VXB_EUNSUPPORTED, "conv needs %zu B smem", c.smem);
   int per_sm = std::min<int>(static_cast<int>((228 * 1024) / (c.smem + 1024)),
                              static_cast<int>(512 / tmem_cols));
   per_sm = std::max(1, std::min(per_sm, env_int("VXB_TC_CTAS_PER_SM", 4)));
@@ -410,6 +423,14 @@ extern "C" {
 int vxb_abi_version(void) { return VXB_ABI_VERSION; }
 const char *vxb_last_error(void) { return g_last_error.c_str(); }
 int vxb_device_sms(void) { return device_sms(); }
+
+size_t vxb_debug_read(unsigned long long *host, size_t count) {
+  if (!g_dbg || !host) return 0;
+  size_t n = std::min(count, kDbgBytes / sizeof(unsigned long long));
+  if (cudaMemcpy(host, g_dbg, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 0;
+  return n;
+}
 
 int vxb_conv_select(int cin, int cout, const int k[3], const int stride[3]) {
   (void)cin;

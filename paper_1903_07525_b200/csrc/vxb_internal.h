@@ -53,6 +53,7 @@ struct TcParams {
   int cout, act;
   float alpha;
   int has_base;
+  unsigned long long *dbg;     // optional per-tile phase timestamps (VXB_TC_DEBUG)
 };
 
 struct TcMaps {
