@@ -52,10 +52,16 @@ __device__ __forceinline__ GroupInfo group_info(const TcParams &p, int g) {
 
 struct TileCoord {
   int rep, nt, b, x0, y0, z0;
+  bool dummy;   // padding tile of a CTA pair: loads as tile 0, stores nothing
 };
 
 __device__ __forceinline__ TileCoord decode_tile(const TcParams &p, int t) {
   TileCoord c;
+  int sp = t % p.spatial_pad;
+  const int rn = t / p.spatial_pad;
+  c.dummy = sp >= p.spatial_real;
+  if (c.dummy) sp = 0;
+  t = sp + rn * p.spatial_real;
   int tz = t % p.tiles_z;
   t /= p.tiles_z;
   int ty = t % p.tiles_y;
@@ -180,6 +186,20 @@ __host__ __device__ inline SmemMap smem_map(const TcParams &p) {
   return m;
 }
 
+// Epilogue variants are compile-time so every instantiation carries only its
+// own code (a kernel with all variants inlined thrashes the instruction cache).
+//   ACT: VXB_ACT_* or -1 (runtime); FASTOUT: blocked bf16 output with fast
+//   activations; BASE: fused residual operand.
+__device__ __forceinline__ void store8_bf16_blocked(const EpiView &v, long long off,
+                                                    const float (&x)[8]) {
+  uint4 u;
+  __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
+  *reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(v.data) + off) = u;
+}
+
+template <int ACT, bool FASTOUT, bool BASE>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     conv3d_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -202,6 +222,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t *t_empty = t_full + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(t_empty + 2);
 
+  // CTA pairs (cluster 2) walk pairs of tiles in lockstep so they can share
+  // one B (weight) stream through TMA multicast
+  const int crank = p.cluster == 2 ? static_cast<int>(cluster_rank()) : 0;
+  const int first_tile = (blockIdx.x / p.cluster) * p.cluster + crank;
+  const int tile_step = gridDim.x;
+  const uint16_t pair_mask = 0x3;
   const int acc_cols = p.bx * p.nt;
   uint32_t tmem_cols = 32;
   while (tmem_cols < static_cast<uint32_t>(acc_cols * p.acc_stages)) tmem_cols <<= 1;
@@ -241,7 +267,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int i = 0; i < p.nb_stages; ++i) {
       mbar_init(&b_full[i], 1);
-      mbar_init(&b_empty[i], 1);
+      mbar_init(&b_empty[i], p.cluster);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&t_full[i], 1);
@@ -255,6 +281,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (p.cluster == 2) cluster_sync_all();   // peer barriers initialised before multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -265,7 +292,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       bool first = true;
       int pit = 0;
       const uint32_t slab = static_cast<uint32_t>(p.nt * SLAB_ROW_BYTES);
-      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++pit) {
+      for (int tile = first_tile; tile < p.total_tiles; tile += tile_step, ++pit) {
         TileCoord tc = decode_tile(p, tile);
         const uint8_t *wbase = p.w + tc.rep * p.w_rep_stride + tc.nt * p.w_ntile_stride;
         long long step_base = 0;
@@ -294,8 +321,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               const uint32_t bytes = n * slab;
               mbar_wait(&b_empty[b_st], b_ph ^ 1);
               mbar_expect_tx(&b_full[b_st], bytes);
-              bulk_load(b_buf + b_st * p.b_stage_bytes, wbase + (step_base + s0) * slab, bytes,
-                        &b_full[b_st]);
+              if (p.cluster == 2) {
+                // each CTA of the pair fetches one half and multicasts it to both
+                const uint32_t hb = bytes >> 1;
+                bulk_load_mc(b_buf + b_st * p.b_stage_bytes + crank * hb,
+                             wbase + (step_base + s0) * slab + crank * hb, hb, &b_full[b_st],
+                             pair_mask);
+              } else {
+                bulk_load(b_buf + b_st * p.b_stage_bytes, wbase + (step_base + s0) * slab, bytes,
+                          &b_full[b_st]);
+              }
               if (++b_st == p.nb_stages) {
                 b_st = 0;
                 b_ph ^= 1;
@@ -320,7 +355,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint64_t slab_inc = static_cast<uint64_t>((p.nt * SLAB_ROW_BYTES) >> 4);
     int a_st = 0, a_ph = 0, b_st = 0, b_ph = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++it) {
+    for (int tile = first_tile; tile < p.total_tiles; tile += tile_step, ++it) {
       const int acc = it % p.acc_stages;
       mbar_wait(&t_empty[acc], ((it / p.acc_stages) & 1) ^ 1);
       tc_fence_after();
@@ -352,7 +387,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               umma_bf16_elect(d, adesc, bdesc, idesc, accumulate);
             accumulate = 1;
           }
-          if (!p.resident) umma_commit_elect(&b_empty[b_st]);
+          if (!p.resident) {
+            if (p.cluster == 2)
+              umma_commit_mc_elect(&b_empty[b_st], pair_mask);   // frees the slot in both CTAs
+            else
+              umma_commit_elect(&b_empty[b_st]);
+          }
           if (++b_st == p.nb_stages) {
             b_st = 0;
             b_ph ^= 1;
@@ -370,105 +410,127 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncwarp();
   } else {
     // ===================== epilogue (EPI_WARPS warps, EPI_WARPS/4 per quarter) ==
+    // Work item = (x-slice, 16 accumulator columns).  TMEM loads and residual
+    // loads of item k+1 are in flight while item k is finished (software
+    // pipeline, two register sets).
     const int q = warp & 3;                   // TMEM lane quarter this warp may access
     const int sub = (warp - 2) >> 2;          // which share of the work items
     constexpr int NSUB = EPI_WARPS / 4;
     const int row = q * 32 + lane;            // MMA row == TMEM lane
     const int yy = row >> 3, zz = row & 7;
-    const int cw = (p.nt % 32 == 0) ? 32 : 16;
-    const int col_items = p.nt / cw;
+    const int col_items = p.nt >> 4;
     const int items = p.bx * col_items;
     const EpiView &ov = p.out;
     const EpiView &bvw = p.base;
-    const bool fast = ov.dtype == VXB_BF16 && ov.blocked;
+    const int act = ACT >= 0 ? ACT : p.act;
     int it = 0;
-    for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++it) {
+    for (int tile = first_tile; tile < p.total_tiles; tile += tile_step, ++it) {
       TileCoord tc = decode_tile(p, tile);
       const int acc = it % p.acc_stages;
       const int y = tc.y0 + yy, z = tc.z0 + zz;
-      const bool yz_ok = y < p.oy && z < p.oz;
+      const bool yz_ok = y < p.oy && z < p.oz && !tc.dummy;
       const long long orow = p.out_rep_off[tc.rep] + tc.b * ov.s[0] + y * ov.s[3] + z * ov.s[4];
       const long long brow =
           p.base_rep_off[tc.rep] + tc.b * bvw.s[0] + y * bvw.s[3] + z * bvw.s[4];
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * acc_cols;
       mbar_wait(&t_full[acc], (it / p.acc_stages) & 1);
       if (warp == 2 && lane == 0) dbg_mark(p, it, 3);
       tc_fence_after();
-      for (int item = sub; item < items; item += NSUB) {
-        const int s = item / col_items;
-        const int cc = (item % col_items) * cw;
+
+      auto taddr_of = [&](int item) {
+        const int s = item / col_items, cc = (item % col_items) << 4;
+        return tbase + s * p.nt + cc;
+      };
+      auto load_base = [&](int item, float (&bv)[16]) {
+        const int s = item / col_items, cc = (item % col_items) << 4;
         const int x = tc.x0 + s;
-        const bool valid = yz_ok && x < p.ox;
-        const int cbase = tc.nt * p.nt + cc;   // first fmap of this item
-        const int nch = cw >> 3;
-        // residual operand, fetched before the TMEM load so the two overlap
-        float bv[32];
-        if (p.has_base) {
+        const bool ok = yz_ok && x < p.ox;
 #pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            float t8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            const int c0 = cbase + h * 8;
-            if (h < nch && valid && c0 < p.cout)
-              load8(bvw, brow + x * bvw.s[2] + (bvw.blocked ? (c0 >> 3) * bvw.s[1] : c0 * bvw.s[1]),
-                    bvw.blocked, t8);
+        for (int h = 0; h < 2; ++h) {
+          float t8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          const int c0 = tc.nt * p.nt + cc + h * 8;
+          if (ok && c0 < p.cout)
+            load8(bvw, brow + x * bvw.s[2] + (bvw.blocked ? (c0 >> 3) * bvw.s[1] : c0 * bvw.s[1]),
+                  bvw.blocked, t8);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) bv[h * 8 + i] = t8[i];
-          }
+          for (int i = 0; i < 8; ++i) bv[h * 8 + i] = t8[i];
         }
-        float v[32];
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                               acc * acc_cols + s * p.nt + cc;
-        if (cw == 32)
-          tmem_ld32(taddr, v);
-        else
-          tmem_ld16(taddr, *reinterpret_cast<float(*)[16]>(v));
-        if (!valid) continue;
+      };
+      auto finish = [&](int item, const uint32_t (&rv)[16], const float (&bv)[16]) {
+        const int s = item / col_items, cc = (item % col_items) << 4;
+        const int x = tc.x0 + s;
+        if (!(yz_ok && x < p.ox)) return;
         const long long obase = orow + x * ov.s[2];
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const int c0 = cbase + h * 8;
-          if (h >= nch || c0 >= p.cout) break;
+        for (int h = 0; h < 2; ++h) {
+          const int c0 = tc.nt * p.nt + cc + h * 8;
+          if (c0 >= p.cout) break;
           const int nvalid = min(8, p.cout - c0);
           const float4 b0 = *reinterpret_cast<const float4 *>(s_bias + c0);
           const float4 b1 = *reinterpret_cast<const float4 *>(s_bias + c0 + 4);
-          float r[8] = {v[h * 8 + 0] + b0.x, v[h * 8 + 1] + b0.y, v[h * 8 + 2] + b0.z,
-                        v[h * 8 + 3] + b0.w, v[h * 8 + 4] + b1.x, v[h * 8 + 5] + b1.y,
-                        v[h * 8 + 6] + b1.z, v[h * 8 + 7] + b1.w};
-          if (p.has_base) {
+          const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+          float r[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) r[i] = __uint_as_float(rv[h * 8 + i]) + bb[i];
+          if (BASE) {
             const float4 s0 = *reinterpret_cast<const float4 *>(s_scale + c0);
             const float4 s1 = *reinterpret_cast<const float4 *>(s_scale + c0 + 4);
             const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
             for (int i = 0; i < 8; ++i) r[i] = fmaf(sc[i], bv[h * 8 + i], r[i]);
           }
-          if (fast) {
-            switch (p.act) {
-              case VXB_ACT_RELU:
+          if (FASTOUT) {
+            if (act == VXB_ACT_RELU) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) r[i] = fmaxf(r[i], 0.f);
-                break;
-              case VXB_ACT_ELU:
+              for (int i = 0; i < 8; ++i) r[i] = fmaxf(r[i], 0.f);
+            } else if (act == VXB_ACT_ELU) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) r[i] = r[i] > 0.f ? r[i] : p.alpha * fast_expm1(r[i]);
-                break;
-              case VXB_ACT_SIGMOID:
+              for (int i = 0; i < 8; ++i) r[i] = r[i] > 0.f ? r[i] : p.alpha * fast_expm1(r[i]);
+            } else if (act == VXB_ACT_SIGMOID) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) r[i] = __fdividef(1.f, 1.f + __expf(-r[i]));
-                break;
-              default:
-                break;
+              for (int i = 0; i < 8; ++i) r[i] = __fdividef(1.f, 1.f + __expf(-r[i]));
             }
           } else {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) r[i] = apply_act(r[i], p.act, p.alpha);
+            for (int i = 0; i < 8; ++i) r[i] = apply_act(r[i], act, p.alpha);
           }
           if (nvalid < 8) {
 #pragma unroll
             for (int i = 0; i < 8; ++i)
               if (i >= nvalid) r[i] = 0.f;
           }
-          store8(ov, obase + (ov.blocked ? (c0 >> 3) * ov.s[1] : c0 * ov.s[1]), ov.blocked,
-                 nvalid, r);
+          if (FASTOUT)
+            store8_bf16_blocked(ov, obase + (c0 >> 3) * ov.s[1], r);
+          else
+            store8(ov, obase + (ov.blocked ? (c0 >> 3) * ov.s[1] : c0 * ov.s[1]), ov.blocked,
+                   nvalid, r);
         }
+      };
+
+      uint32_t ra[16], rb[16];
+      float ba[16], bb2[16];
+      int item = sub;
+      if (item < items) {
+        tmem_ld16_issue(taddr_of(item), ra);
+        if (BASE) load_base(item, ba);
+      }
+      while (item < items) {
+        const int nxt = item + NSUB;
+        tmem_wait_ld16(ra);
+        if (nxt < items) {
+          tmem_ld16_issue(taddr_of(nxt), rb);
+          if (BASE) load_base(nxt, bb2);
+        }
+        finish(item, ra, ba);
+        if (nxt >= items) break;
+        const int nn = nxt + NSUB;
+        tmem_wait_ld16(rb);
+        if (nn < items) {
+          tmem_ld16_issue(taddr_of(nn), ra);
+          if (BASE) load_base(nn, ba);
+        }
+        finish(nxt, rb, bb2);
+        item = nn;
       }
       tc_fence_before();
       __syncwarp();
@@ -478,6 +540,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 
   __syncthreads();
+  if (p.cluster == 2) cluster_sync_all();   // no CTA leaves while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, tmem_cols);
@@ -490,17 +553,50 @@ size_t tc_smem_bytes(const TcParams &p) {
   return smem_map(p).bars + (2 * p.na + 2 * p.nb_stages + 4) * sizeof(uint64_t) + 16;
 }
 
-int launch_conv3d_tc(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t stream) {
-  size_t smem = tc_smem_bytes(p);
+template <int ACT, bool FASTOUT, bool BASE>
+static int launch_variant(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t stream,
+                          size_t smem) {
+  auto kern = conv3d_tc_kernel<ACT, FASTOUT, BASE>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv3d_tc_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(conv3d_tc)");
     configured = true;
   }
-  conv3d_tc_kernel<<<grid, TC_THREADS, smem, stream>>>(p, maps);
-  return check_cuda(cudaGetLastError(), "conv3d_tc_kernel launch");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = p.cluster > 1 ? 1 : 0;
+  return check_cuda(cudaLaunchKernelEx(&cfg, kern, p, maps), "conv3d_tc_kernel launch");
+}
+
+template <bool BASE>
+static int launch_act(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t s,
+                      size_t smem) {
+  const bool fast = p.out.dtype == VXB_BF16 && p.out.blocked;
+  if (!fast) return launch_variant<-1, false, BASE>(p, maps, grid, s, smem);
+  switch (p.act) {
+    case VXB_ACT_RELU: return launch_variant<VXB_ACT_RELU, true, BASE>(p, maps, grid, s, smem);
+    case VXB_ACT_ELU: return launch_variant<VXB_ACT_ELU, true, BASE>(p, maps, grid, s, smem);
+    case VXB_ACT_SIGMOID:
+      return launch_variant<VXB_ACT_SIGMOID, true, BASE>(p, maps, grid, s, smem);
+    default: return launch_variant<VXB_ACT_NONE, true, BASE>(p, maps, grid, s, smem);
+  }
+}
+
+int launch_conv3d_tc(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t stream) {
+  const size_t smem = tc_smem_bytes(p);
+  return p.has_base ? launch_act<true>(p, maps, grid, stream, smem)
+                    : launch_act<false>(p, maps, grid, stream, smem);
 }
 
 }  // namespace vxb

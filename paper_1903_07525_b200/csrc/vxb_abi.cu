@@ -202,13 +202,14 @@ static int tc_configure(const TcLayout &L, const int k[3], int ox, int reps, TcC
     max_steps = std::max(max_steps, g.steps);
   }
   const int slab = L.nt * SLAB_ROW_BYTES;
+  int na_cap = std::max(2, std::min(6, env_int("VXB_TC_NA", 3)));
   for (;;) {
     const int hx = c.bx + k[0] - 1, hy = TILE_Y + k[1] - 1, hz = TILE_Z + k[2] - 1;
     c.chunk_bytes = hx * hy * hz * 16;
     c.chunk_stride = round_up(c.chunk_bytes + 128, 128);
     c.chunk_slots = any_pair ? 2 : 1;
     c.a_stage = c.chunk_slots * c.chunk_stride;
-    c.na = std::max(2, std::min(6, env_int("VXB_TC_NA", 2)));
+    c.na = na_cap;
     // resident weights: whole filter bank of the (single) N tile in smem
     long long total_w = L.steps * slab;
     c.resident = 0;
@@ -235,6 +236,10 @@ static int tc_configure(const TcLayout &L, const int k[3], int ox, int reps, TcC
       }
     }
     if (c.nb >= 1 && (c.resident || c.nb >= 2)) break;
+    if (na_cap > 2) {
+      --na_cap;
+      continue;
+    }
     if (c.bx == 1) return set_error(VXB_EUNSUPPORTED, "conv tile does not fit in shared memory");
     c.bx /= 2;
   }
@@ -348,9 +353,14 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   p.tiles_z = ceil_div(a.oz, TILE_Z);
   p.n_tiles = L.n_tiles;
   p.reps = a.reps;
-  long long total = static_cast<long long>(p.tiles_x) * p.tiles_y * p.tiles_z * p.nb *
-                    p.n_tiles * p.reps;
+  const long long spatial = static_cast<long long>(p.tiles_x) * p.tiles_y * p.tiles_z * p.nb;
+  // weight-streaming convs run as CTA pairs sharing one multicast B stream
+  p.cluster = (!c.resident && env_int("VXB_TC_CLUSTER", 2) == 2 && spatial >= 2) ? 2 : 1;
+  const long long spatial_pad = (spatial + p.cluster - 1) / p.cluster * p.cluster;
+  long long total = spatial_pad * p.n_tiles * p.reps;
   if (total > 0x7fffffffLL) return set_error(VXB_EUNSUPPORTED, "too many tiles");
+  p.spatial_real = static_cast<int>(spatial);
+  p.spatial_pad = static_cast<int>(spatial_pad);
   p.total_tiles = static_cast<int>(total);
   p.kx = a.k[0];
   p.ky = a.k[1];
@@ -411,6 +421,7 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
                              static_cast<int>(512 / tmem_cols));
   per_sm = std::max(1, std::min(per_sm, env_int("VXB_TC_CTAS_PER_SM", 4)));
   int grid = static_cast<int>(std::min<long long>(total, static_cast<long long>(sms) * per_sm));
+  grid = std::max(p.cluster, grid / p.cluster * p.cluster);
   return launch_conv3d_tc(p, maps, grid, stream);
 }
 

@@ -27,6 +27,8 @@ struct TcParams {
   int ox, oy, oz;              // output extents
   int tiles_x, tiles_y, tiles_z;
   int n_tiles, reps, total_tiles;
+  int spatial_real, spatial_pad;  // tiles per (rep, ntile); padded to the cluster size
+  int cluster;                    // 1, or 2 = CTA pair sharing B via TMA multicast
   int bx;                      // x-slices per CTA tile (each slice = 128 MMA rows)
   int nt;                      // N per tile (multiple of 16)
   int acc_stages;              // TMEM accumulator stages
