@@ -167,7 +167,7 @@ __device__ __forceinline__ void dbg_mark(const TcParams &p, int it, int slot) {
 }
 
 constexpr int EPI_WARPS = 12;
-constexpr int TC_THREADS = 64 + 32 * EPI_WARPS;
+constexpr int TC_THREADS = 96 + 32 * EPI_WARPS;   // A-TMA, MMA, B-TMA + epilogue
 
 // Byte offsets inside the dynamic smem block (all derivable from p).
 struct SmemMap {
@@ -199,7 +199,73 @@ __device__ __forceinline__ void store8_bf16_blocked(const EpiView &v, long long 
   *reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(v.data) + off) = u;
 }
 
-template <int ACT, bool FASTOUT, bool BASE>
+
+// ---------------------------------------------------------------- MMA issue
+// One group (<= 2 input chunks x all taps) of MMAs.  Everything is passed by
+// value and kept in scalar locals so that, executed by a convergent warp,
+// ptxas holds the descriptors in uniform registers.
+struct MmaCtx {
+  uint64_t *b_full, *b_empty;
+  int nb_stages, bsteps, resident, first_tile_iter, cluster;
+};
+
+template <int BX, bool PAIRM>
+__device__ __forceinline__ void mma_group(
+    const uint32_t a_lo0, const uint32_t a_hi, const uint32_t b_base0, const uint32_t b_stage_bytes,
+    const uint32_t b_hi, const uint32_t b_inc, const uint32_t slice_inc, const uint32_t d_base,
+    const uint32_t nt, const uint32_t idesc, const int steps, const int tz_n, const uint32_t dz_step,
+    const uint32_t dy_wrap, const uint32_t dx_wrap, const int ky, const MmaCtx &cx, int &b_st,
+    int &b_ph, uint32_t &acc) {
+  int tz = 0, ty = 0;
+  uint32_t off = 0;
+  for (int s0 = 0; s0 < steps; s0 += cx.bsteps) {
+    const int n = min(cx.bsteps, steps - s0);
+    if (cx.resident) {
+      if (cx.first_tile_iter) mbar_wait(&cx.b_full[b_st], 0);
+    } else {
+      mbar_wait(&cx.b_full[b_st], b_ph);
+    }
+    tc_fence_after();
+    uint32_t b_lo = desc_lo(b_base0 + b_st * b_stage_bytes, 128u);
+    for (int i = 0; i < n; ++i) {
+      const uint32_t a_lo = a_lo0 + off;
+#pragma unroll
+      for (int s = 0; s < BX; ++s) {
+        if (PAIRM)
+          umma_bf16_pair_lohi_elect(d_base + s * nt, a_lo + s * slice_inc, a_hi, b_lo, b_hi,
+                                    idesc, acc);
+        else
+          umma_bf16_lohi_elect(d_base + s * nt, a_lo + s * slice_inc, a_hi, b_lo, b_hi, idesc,
+                               acc);
+      }
+      acc = 1;
+      b_lo += b_inc;
+      off += dz_step;
+      if (++tz == tz_n) {
+        tz = 0;
+        off += dy_wrap;
+        if (++ty == ky) {
+          ty = 0;
+          off += dx_wrap;
+        }
+      }
+    }
+    if (!cx.resident) {
+      if (PAIRM)
+        umma_commit_pair_elect(&cx.b_empty[b_st], 0x3);
+      else if (cx.cluster == 2)
+        umma_commit_mc_elect(&cx.b_empty[b_st], 0x3);   // frees the slot in both CTAs
+      else
+        umma_commit_elect(&cx.b_empty[b_st]);
+    }
+    if (++b_st == cx.nb_stages) {
+      b_st = 0;
+      b_ph ^= 1;
+    }
+  }
+}
+
+template <int ACT, bool FASTOUT, bool BASE, bool PAIR>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     conv3d_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -267,17 +333,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int i = 0; i < p.nb_stages; ++i) {
       mbar_init(&b_full[i], 1);
-      mbar_init(&b_empty[i], p.cluster);
+      mbar_init(&b_empty[i], PAIR ? 1 : p.cluster);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&t_full[i], 1);
-      mbar_init(&t_empty[i], EPI_WARPS);
+      mbar_init(&t_empty[i], PAIR ? 2 * EPI_WARPS : EPI_WARPS);
     }
     fence_mbar_init();
   }
   if (warp == 1) {
-    tmem_alloc(tmem_slot, tmem_cols);
-    tmem_relinquish();
+    if (PAIR) {
+      tmem_alloc_pair(tmem_slot, tmem_cols);
+      tmem_relinquish_pair();
+    } else {
+      tmem_alloc(tmem_slot, tmem_cols);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -286,126 +357,165 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== A producer: halo tiles (TMA 4-D boxes) ==========
     if (lane == 0) {
-      int a_st = 0, a_ph = 0, b_st = 0, b_ph = 0;
-      bool first = true;
+      int a_st = 0, a_ph = 0;
       int pit = 0;
-      const uint32_t slab = static_cast<uint32_t>(p.nt * SLAB_ROW_BYTES);
       for (int tile = first_tile; tile < p.total_tiles; tile += tile_step, ++pit) {
         TileCoord tc = decode_tile(p, tile);
-        const uint8_t *wbase = p.w + tc.rep * p.w_rep_stride + tc.nt * p.w_ntile_stride;
-        long long step_base = 0;
-        if (p.resident) b_st = 0;
         for (int g = 0; g < p.n_groups; ++g) {
           GroupInfo gi = group_info(p, g);
-          mbar_wait(&a_empty[a_st], a_ph ^ 1);
+          mbar_wait_sleep(&a_empty[a_st], a_ph ^ 1);
           if (g == 0) dbg_mark(p, pit, 0);
-          mbar_expect_tx(&a_full[a_st], gi.nch * p.chunk_bytes);
+          // pair mode: the leader's barrier counts both CTAs' bytes
+          if (p.dbg_mode & 2) {
+            if (!PAIR || crank == 0) mbar_arrive(&a_full[a_st]);
+            if (++a_st == p.na) {
+              a_st = 0;
+              a_ph ^= 1;
+            }
+            continue;
+          }
+          if (!PAIR || crank == 0)
+            mbar_expect_tx(&a_full[a_st], gi.nch * p.chunk_bytes * (PAIR ? 2 : 1));
           const int *off = p.seg_off[gi.seg];
           const int cx = tc.x0 - p.pad[0] + off[0];
           const int cy = tc.y0 - p.pad[1] + off[1];
           const int cz = (tc.z0 - p.pad[2] + off[2]) * LANES;
           for (int ci = 0; ci < gi.nch; ++ci) {
             const int chunk = tc.b * p.seg_bstride[gi.seg] + gi.chunk0 + ci;
-            tma_load_4d(a_buf + a_st * p.a_stage_bytes + ci * p.chunk_stride, &maps.m[gi.seg],
-                        &a_full[a_st], cz, cy, cx, chunk);
+            if (PAIR)
+              tma_load_4d_pair(a_buf + a_st * p.a_stage_bytes + ci * p.chunk_stride,
+                               &maps.m[gi.seg], &a_full[a_st], cz, cy, cx, chunk);
+            else
+              tma_load_4d(a_buf + a_st * p.a_stage_bytes + ci * p.chunk_stride, &maps.m[gi.seg],
+                          &a_full[a_st], cz, cy, cx, chunk);
           }
           if (++a_st == p.na) {
             a_st = 0;
             a_ph ^= 1;
           }
-          if (!p.resident || first) {
-            for (int s0 = 0; s0 < gi.steps; s0 += p.bsteps) {
-              const int n = min(p.bsteps, gi.steps - s0);
-              const uint32_t bytes = n * slab;
-              mbar_wait(&b_empty[b_st], b_ph ^ 1);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 2) {
+    // ===================== B producer: weight slabs (bulk copies) ==========
+    // independent of the A producer so halo loads are never queued behind
+    // the weight stream of the current group
+    if (lane == 0) {
+      int b_st = 0, b_ph = 0;
+      const uint32_t slab = static_cast<uint32_t>(p.nt * SLAB_ROW_BYTES);
+      for (int tile = first_tile; tile < p.total_tiles; tile += tile_step) {
+        if (p.resident && tile != first_tile) break;   // resident bank: loaded once
+        TileCoord tc = decode_tile(p, tile);
+        const uint8_t *wbase = p.w + tc.rep * p.w_rep_stride + tc.nt * p.w_ntile_stride;
+        long long step_base = 0;
+        for (int g = 0; g < p.n_groups; ++g) {
+          GroupInfo gi = group_info(p, g);
+          for (int s0 = 0; s0 < gi.steps; s0 += p.bsteps) {
+            const int n = min(p.bsteps, gi.steps - s0);
+            const uint32_t bytes = n * slab;
+            mbar_wait_sleep(&b_empty[b_st], b_ph ^ 1);
+            if (p.dbg_mode & 4) {
+              if (!PAIR || crank == 0) mbar_arrive(&b_full[b_st]);
+            } else if (PAIR) {
+              // this CTA's half (rows [crank*nt/2, ..)) of bsteps slabs; the
+              // box always spans bsteps steps (extra steps are never read)
+              if (crank == 0) mbar_expect_tx(&b_full[b_st], 2 * p.b_stage_bytes);
+              const int step0 = static_cast<int>((static_cast<long long>(tc.rep) * p.n_tiles +
+                                                  tc.nt) * p.w_steps + step_base + s0);
+              tma_load_4d_pair(b_buf + b_st * p.b_stage_bytes, &maps.w, &b_full[b_st], 0, 0,
+                               crank, step0);
+            } else if (p.cluster == 2) {
               mbar_expect_tx(&b_full[b_st], bytes);
-              if (p.cluster == 2) {
-                // each CTA of the pair fetches one half and multicasts it to both
-                const uint32_t hb = bytes >> 1;
-                bulk_load_mc(b_buf + b_st * p.b_stage_bytes + crank * hb,
-                             wbase + (step_base + s0) * slab + crank * hb, hb, &b_full[b_st],
-                             pair_mask);
-              } else {
-                bulk_load(b_buf + b_st * p.b_stage_bytes, wbase + (step_base + s0) * slab, bytes,
-                          &b_full[b_st]);
-              }
-              if (++b_st == p.nb_stages) {
-                b_st = 0;
-                b_ph ^= 1;
-              }
+              // each CTA of the pair fetches one half and multicasts it to both
+              const uint32_t hb = bytes >> 1;
+              bulk_load_mc(b_buf + b_st * p.b_stage_bytes + crank * hb,
+                           wbase + (step_base + s0) * slab + crank * hb, hb, &b_full[b_st],
+                           pair_mask);
+            } else {
+              mbar_expect_tx(&b_full[b_st], bytes);
+              bulk_load(b_buf + b_st * p.b_stage_bytes, wbase + (step_base + s0) * slab, bytes,
+                        &b_full[b_st]);
+            }
+            if (++b_st == p.nb_stages) {
+              b_st = 0;
+              b_ph ^= 1;
             }
           }
           step_base += gi.steps;
         }
-        first = false;
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    // The whole warp walks the schedule (so descriptor arithmetic stays
-    // warp-uniform); one elected lane issues each tcgen05 instruction.
-    const uint32_t idesc = idesc_bf16(128, p.nt);
-    const uint32_t a_base0 = smem_u32(a_buf);
-    const uint32_t b_base0 = smem_u32(b_buf);
-    const uint32_t sbo_a = p.hz * 16;
-    const uint64_t slice_inc = static_cast<uint64_t>((p.hy * p.hz * 16) >> 4);
-    const uint64_t slab_inc = static_cast<uint64_t>((p.nt * SLAB_ROW_BYTES) >> 4);
-    int a_st = 0, a_ph = 0, b_st = 0, b_ph = 0;
-    int it = 0;
-    for (int tile = first_tile; tile < p.total_tiles; tile += tile_step, ++it) {
-      const int acc = it % p.acc_stages;
-      mbar_wait(&t_empty[acc], ((it / p.acc_stages) & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t d_base = tmem_base + acc * acc_cols;
-      uint32_t accumulate = 0;
-      if (p.resident) b_st = 0;
-      for (int g = 0; g < p.n_groups; ++g) {
-        GroupInfo gi = group_info(p, g);
-        mbar_wait(&a_full[a_st], a_ph);
-        if (g == 0 && lane == 0) dbg_mark(p, it, 1);
+    // The issue loop paces N >= 128 convs (one tcgen05.mma per ~64 cycles).
+    // The whole warp walks the schedule in convergent, warp-uniform control
+    // flow so ptxas keeps descriptors in uniform registers; the MMA asm
+    // elects one lane.  Descriptors are split in a loop-invariant high word
+    // and a low word advanced by constants; the x-slice loop is unrolled.
+    if (!PAIR || crank == 0) {
+      const uint32_t idesc = idesc_bf16(PAIR ? 256 : 128, p.nt);
+      const uint32_t a_base0 = smem_u32(a_buf);
+      const uint32_t b_base0 = smem_u32(b_buf);
+      const uint32_t slice_inc = (p.hy * p.hz * 16) >> 4;
+      const uint32_t b_inc = (p.nt * SLAB_ROW_BYTES / (PAIR ? 2 : 1)) >> 4;
+      const uint32_t a_hi = desc_hi(p.hz * 16);
+      const uint32_t b_hi = desc_hi(256u);
+      MmaCtx cx;
+      cx.b_full = b_full;
+      cx.b_empty = b_empty;
+      cx.nb_stages = p.nb_stages;
+      cx.bsteps = p.bsteps;
+      cx.resident = p.resident;
+      cx.cluster = p.cluster;
+      int a_st = 0, a_ph = 0, b_st = 0, b_ph = 0;
+      int it = 0;
+      for (int tile = first_tile; tile < p.total_tiles; tile += tile_step, ++it) {
+        const int acc = it % p.acc_stages;
+        mbar_wait(&t_empty[acc], ((it / p.acc_stages) & 1) ^ 1);
         tc_fence_after();
-        const bool pair = gi.nch == 2;
-        const uint32_t *tab = pair ? tab_pair : tab_odd;
-        const uint64_t adesc0 =
-            smem_desc(a_base0 + a_st * p.a_stage_bytes, pair ? p.chunk_stride : 16u, sbo_a);
-        for (int s0 = 0; s0 < gi.steps; s0 += p.bsteps) {
-          const int n = min(p.bsteps, gi.steps - s0);
-          if (p.resident) {
-            if (it == 0) mbar_wait(&b_full[b_st], 0);
-          } else {
-            mbar_wait(&b_full[b_st], b_ph);
-          }
+        const uint32_t d_base = tmem_base + acc * acc_cols;
+        uint32_t accumulate = 0;
+        if (p.resident) b_st = 0;
+        cx.first_tile_iter = it == 0;
+        for (int g = 0; g < p.n_groups; ++g) {
+          GroupInfo gi = group_info(p, g);
+          mbar_wait(&a_full[a_st], a_ph);
           tc_fence_after();
-          uint64_t bdesc = smem_desc(b_base0 + b_st * p.b_stage_bytes, 128u, 256u);
-          for (int i = 0; i < n; ++i, bdesc += slab_inc) {
-            uint64_t adesc = adesc0 + (tab[s0 + i] >> 4);
-            uint32_t d = d_base;
-            for (int s = 0; s < p.bx; ++s, adesc += slice_inc, d += p.nt)
-              umma_bf16_elect(d, adesc, bdesc, idesc, accumulate);
-            accumulate = 1;
+          const bool pair = gi.nch == 2;
+          const int tz_n = pair ? p.kz : (p.kz + 1) >> 1;
+          const uint32_t dz_step = pair ? 1u : 2u;
+          const uint32_t a_lo0 =
+              desc_lo(a_base0 + a_st * p.a_stage_bytes, pair ? p.chunk_stride : 16u);
+          const uint32_t dy_wrap = p.hz - tz_n * dz_step, dx_wrap = (p.hy - p.ky) * p.hz;
+#define VXB_GROUP(BXV)                                                                          \
+  mma_group<BXV, PAIR>(a_lo0, a_hi, b_base0, p.b_stage_bytes, b_hi, b_inc, slice_inc, d_base,    \
+                       p.nt, idesc, gi.steps, tz_n, dz_step, dy_wrap, dx_wrap, p.ky, cx, b_st,  \
+                       b_ph, accumulate)
+          switch (p.bx) {
+            case 1: VXB_GROUP(1); break;
+            case 2: VXB_GROUP(2); break;
+            case 4: VXB_GROUP(4); break;
+            default: VXB_GROUP(8); break;
           }
-          if (!p.resident) {
-            if (p.cluster == 2)
-              umma_commit_mc_elect(&b_empty[b_st], pair_mask);   // frees the slot in both CTAs
-            else
-              umma_commit_elect(&b_empty[b_st]);
-          }
-          if (++b_st == p.nb_stages) {
-            b_st = 0;
-            b_ph ^= 1;
+#undef VXB_GROUP
+          if (PAIR)
+            umma_commit_pair_elect(&a_empty[a_st], pair_mask);
+          else
+            umma_commit_elect(&a_empty[a_st]);
+          if (++a_st == p.na) {
+            a_st = 0;
+            a_ph ^= 1;
           }
         }
-        umma_commit_elect(&a_empty[a_st]);
-        if (++a_st == p.na) {
-          a_st = 0;
-          a_ph ^= 1;
-        }
+        if (PAIR)
+          umma_commit_pair_elect(&t_full[acc], pair_mask);
+        else
+          umma_commit_elect(&t_full[acc]);
       }
-      umma_commit_elect(&t_full[acc]);
-      if (lane == 0) dbg_mark(p, it, 2);
     }
     __syncwarp();
   } else {
@@ -414,7 +524,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // loads of item k+1 are in flight while item k is finished (software
     // pipeline, two register sets).
     const int q = warp & 3;                   // TMEM lane quarter this warp may access
-    const int sub = (warp - 2) >> 2;          // which share of the work items
+    const int sub = (warp - 3) >> 2;          // which share of the work items
     constexpr int NSUB = EPI_WARPS / 4;
     const int row = q * 32 + lane;            // MMA row == TMEM lane
     const int yy = row >> 3, zz = row & 7;
@@ -433,8 +543,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const long long brow =
           p.base_rep_off[tc.rep] + tc.b * bvw.s[0] + y * bvw.s[3] + z * bvw.s[4];
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * acc_cols;
-      mbar_wait(&t_full[acc], (it / p.acc_stages) & 1);
-      if (warp == 2 && lane == 0) dbg_mark(p, it, 3);
+      mbar_wait_sleep(&t_full[acc], (it / p.acc_stages) & 1);
+      if (warp == 3 && lane == 0) dbg_mark(p, it, 3);
       tc_fence_after();
 
       auto taddr_of = [&](int item) {
@@ -509,7 +619,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
       uint32_t ra[16], rb[16];
       float ba[16], bb2[16];
-      int item = sub;
+      int item = (p.dbg_mode & 1) ? items : sub;
       if (item < items) {
         tmem_ld16_issue(taddr_of(item), ra);
         if (BASE) load_base(item, ba);
@@ -534,8 +644,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&t_empty[acc]);
-      if (warp == 2 && lane == 0) dbg_mark(p, it, 4);
+      if (lane == 0) {
+        if (PAIR)
+          mbar_arrive_cta(&t_empty[acc], 0);   // the leader's MMA waits for both CTAs
+        else
+          mbar_arrive(&t_empty[acc]);
+      }
+      if (warp == 3 && lane == 0) dbg_mark(p, it, 4);
     }
   }
 
@@ -543,7 +658,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (p.cluster == 2) cluster_sync_all();   // no CTA leaves while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, tmem_cols);
+    if (PAIR)
+      tmem_dealloc_pair(tmem_base, tmem_cols);
+    else
+      tmem_dealloc(tmem_base, tmem_cols);
   }
 }
 
@@ -553,10 +671,10 @@ size_t tc_smem_bytes(const TcParams &p) {
   return smem_map(p).bars + (2 * p.na + 2 * p.nb_stages + 4) * sizeof(uint64_t) + 16;
 }
 
-template <int ACT, bool FASTOUT, bool BASE>
+template <int ACT, bool FASTOUT, bool BASE, bool PAIR>
 static int launch_variant(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t stream,
                           size_t smem) {
-  auto kern = conv3d_tc_kernel<ACT, FASTOUT, BASE>;
+  auto kern = conv3d_tc_kernel<ACT, FASTOUT, BASE, PAIR>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -579,24 +697,31 @@ static int launch_variant(const TcParams &p, const TcMaps &maps, int grid, cudaS
   return check_cuda(cudaLaunchKernelEx(&cfg, kern, p, maps), "conv3d_tc_kernel launch");
 }
 
-template <bool BASE>
+template <bool BASE, bool PAIR>
 static int launch_act(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t s,
                       size_t smem) {
   const bool fast = p.out.dtype == VXB_BF16 && p.out.blocked;
-  if (!fast) return launch_variant<-1, false, BASE>(p, maps, grid, s, smem);
+  if (!fast) {
+    if (PAIR) return set_error(VXB_EUNSUPPORTED, "pair mode needs a blocked bf16 output");
+    return launch_variant<-1, false, BASE, false>(p, maps, grid, s, smem);
+  }
   switch (p.act) {
-    case VXB_ACT_RELU: return launch_variant<VXB_ACT_RELU, true, BASE>(p, maps, grid, s, smem);
-    case VXB_ACT_ELU: return launch_variant<VXB_ACT_ELU, true, BASE>(p, maps, grid, s, smem);
+    case VXB_ACT_RELU:
+      return launch_variant<VXB_ACT_RELU, true, BASE, PAIR>(p, maps, grid, s, smem);
+    case VXB_ACT_ELU: return launch_variant<VXB_ACT_ELU, true, BASE, PAIR>(p, maps, grid, s, smem);
     case VXB_ACT_SIGMOID:
-      return launch_variant<VXB_ACT_SIGMOID, true, BASE>(p, maps, grid, s, smem);
-    default: return launch_variant<VXB_ACT_NONE, true, BASE>(p, maps, grid, s, smem);
+      return launch_variant<VXB_ACT_SIGMOID, true, BASE, PAIR>(p, maps, grid, s, smem);
+    default: return launch_variant<VXB_ACT_NONE, true, BASE, PAIR>(p, maps, grid, s, smem);
   }
 }
 
 int launch_conv3d_tc(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t stream) {
   const size_t smem = tc_smem_bytes(p);
-  return p.has_base ? launch_act<true>(p, maps, grid, stream, smem)
-                    : launch_act<false>(p, maps, grid, stream, smem);
+  if (p.pair)
+    return p.has_base ? launch_act<true, true>(p, maps, grid, stream, smem)
+                      : launch_act<false, true>(p, maps, grid, stream, smem);
+  return p.has_base ? launch_act<true, false>(p, maps, grid, stream, smem)
+                    : launch_act<false, false>(p, maps, grid, stream, smem);
 }
 
 }  // namespace vxb

@@ -355,7 +355,17 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   p.reps = a.reps;
   const long long spatial = static_cast<long long>(p.tiles_x) * p.tiles_y * p.tiles_z * p.nb;
   // weight-streaming convs run as CTA pairs sharing one multicast B stream
-  p.cluster = (!c.resident && env_int("VXB_TC_CLUSTER", 2) == 2 && spatial >= 2) ? 2 : 1;
+  // cta_group::2 pairs: M = 256 per MMA, each CTA ingests and reads only half
+  // of every weight slab (halves the smem traffic that bounds high-fmap convs)
+  p.pair = (!c.resident && spatial >= 2 && L.nt % 16 == 0 && L.nt / 8 <= 256 &&
+            a.out.dtype == VXB_BF16 && a.out.blocked &&
+            env_int("VXB_TC_PAIR", 1) == 1) ? 1 : 0;
+  p.cluster = p.pair || (!c.resident && env_int("VXB_TC_CLUSTER", 1) == 2 && spatial >= 2) ? 2 : 1;
+  if (p.pair) {
+    c.b_stage /= 2;
+    const int budget = 227 * 1024 - 6144;
+    c.nb = std::max(2, std::min(6, (budget - c.na * c.a_stage) / c.b_stage));
+  }
   const long long spatial_pad = (spatial + p.cluster - 1) / p.cluster * p.cluster;
   long long total = spatial_pad * p.n_tiles * p.reps;
   if (total > 0x7fffffffLL) return set_error(VXB_EUNSUPPORTED, "too many tiles");
@@ -389,6 +399,22 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   p.bsteps = c.bsteps;
   p.resident = c.resident;
   p.w = static_cast<const uint8_t *>(a.w);
+  p.w_steps = static_cast<int>(L.steps);
+  if (p.pair) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return set_error(VXB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t slab = static_cast<cuuint64_t>(L.nt) * SLAB_ROW_BYTES;
+    cuuint64_t dims[4] = {128, static_cast<cuuint64_t>(L.nt / 8), 2,
+                          static_cast<cuuint64_t>(a.reps) * L.n_tiles * L.steps};
+    cuuint64_t strides[3] = {128, slab / 2, slab};
+    cuuint32_t box[4] = {128, static_cast<cuuint32_t>(L.nt / 8), 1,
+                         static_cast<cuuint32_t>(c.bsteps)};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(&maps.w, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(a.w), dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(VXB_ECUDA, "weight tensor map failed (%d)", (int)r);
+  }
   p.w_ntile_stride = L.steps * L.nt * SLAB_ROW_BYTES;
   p.w_rep_stride = static_cast<long long>(tc_bytes_per_rep(L));
   p.bias = a.bias;
@@ -405,6 +431,7 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   p.alpha = a.alpha;
   int sms = device_sms();
   if (sms <= 0) return set_error(VXB_ECUDA, "no CUDA device");
+  p.dbg_mode = env_int("VXB_TC_DBGMODE", 0);
   if (env_int("VXB_TC_DEBUG", 0)) {
     if (!g_dbg) {
       cudaError_t e = cudaMalloc(&g_dbg, kDbgBytes);

@@ -29,6 +29,7 @@ struct TcParams {
   int n_tiles, reps, total_tiles;
   int spatial_real, spatial_pad;  // tiles per (rep, ntile); padded to the cluster size
   int cluster;                    // 1, or 2 = CTA pair sharing B via TMA multicast
+  int pair;                       // cta_group::2 MMA (M = 256), each CTA holds half of B
   int bx;                      // x-slices per CTA tile (each slice = 128 MMA rows)
   int nt;                      // N per tile (multiple of 16)
   int acc_stages;              // TMEM accumulator stages
@@ -49,6 +50,7 @@ struct TcParams {
   int resident;                // weights loaded once, kept in smem
   const uint8_t *w;
   long long w_ntile_stride, w_rep_stride;   // bytes
+  int w_steps;                 // K steps per (rep, ntile)
   const float *bias, *scale;
   EpiView out, base;
   long long out_rep_off[MAX_REPS], base_rep_off[MAX_REPS];
@@ -56,10 +58,12 @@ struct TcParams {
   float alpha;
   int has_base;
   unsigned long long *dbg;     // optional per-tile phase timestamps (VXB_TC_DEBUG)
+  int dbg_mode;                // VXB_TC_DBGMODE bits: 1 no epilogue, 2 no A loads, 4 no B loads
 };
 
 struct TcMaps {
   CUtensorMap m[2];
+  CUtensorMap w;   // packed weights (pair mode): (128 B, nt/8, half, step)
 };
 
 
