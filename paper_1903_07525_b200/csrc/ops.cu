@@ -97,22 +97,19 @@ __device__ __forceinline__ float act_fn(float v, int act, float alpha) {
   return v;
 }
 
-// flat index -> (b, chunk, x, y, z) with z fastest
+// 3-D launch grid: x covers y*z (z fastest, coalesced), y = x, z = batch*chunk
 struct ChunkIdx {
   int b, ch, x, y, z;
 };
-__device__ __forceinline__ bool chunk_index(long long i, int n, int nch, int X, int Y, int Z,
-                                            ChunkIdx &o) {
-  long long total = static_cast<long long>(n) * nch * X * Y * Z;
-  if (i >= total) return false;
-  o.z = static_cast<int>(i % Z);
-  i /= Z;
-  o.y = static_cast<int>(i % Y);
-  i /= Y;
-  o.x = static_cast<int>(i % X);
-  i /= X;
-  o.ch = static_cast<int>(i % nch);
-  o.b = static_cast<int>(i / nch);
+
+__device__ __forceinline__ bool chunk_index3(int nch, int Y, int Z, ChunkIdx &o) {
+  const int yz = blockIdx.x * blockDim.x + threadIdx.x;
+  if (yz >= Y * Z) return false;
+  o.y = yz / Z;
+  o.z = yz - o.y * Z;
+  o.x = blockIdx.y;
+  o.b = blockIdx.z / nch;
+  o.ch = blockIdx.z - o.b * nch;
   return true;
 }
 
@@ -126,9 +123,7 @@ __device__ __forceinline__ void zero_tail_lanes(float (&r)[8], int ch, int c) {
 __global__ void copy_kernel(DView src, DView dst) {
   ChunkIdx k;
   int nch = (dst.c + 7) >> 3;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-       chunk_index(i, dst.n, nch, dst.x, dst.y, dst.z, k);
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  if (chunk_index3(nch, dst.y, dst.z, k)) {
     float r[8];
     ld_chunk(src, k.b, k.ch, k.x, k.y, k.z, r);
     zero_tail_lanes(r, k.ch, dst.c);
@@ -139,9 +134,7 @@ __global__ void copy_kernel(DView src, DView dst) {
 __global__ void zero_kernel(DView dst) {
   ChunkIdx k;
   int nch = (dst.c + 7) >> 3;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-       chunk_index(i, dst.n, nch, dst.x, dst.y, dst.z, k);
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  if (chunk_index3(nch, dst.y, dst.z, k)) {
     float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (dst.blocked) {
       st_chunk(dst, k.b, k.ch, k.x, k.y, k.z, r);
@@ -159,9 +152,7 @@ __global__ void pool_kernel(DView in, DView out, int kx, int ky, int kz, int sx,
                             int mode) {
   ChunkIdx k;
   int nch = (out.c + 7) >> 3;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-       chunk_index(i, out.n, nch, out.x, out.y, out.z, k);
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  if (chunk_index3(nch, out.y, out.z, k)) {
     float r[8], t[8];
     bool first = true;
     for (int dx = 0; dx < kx; ++dx)
@@ -194,9 +185,7 @@ __global__ void pool_kernel(DView in, DView out, int kx, int ky, int kz, int sx,
 __global__ void eltwise_kernel(DView a, DView b, DView out, int op) {
   ChunkIdx k;
   int nch = (out.c + 7) >> 3;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-       chunk_index(i, out.n, nch, out.x, out.y, out.z, k);
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  if (chunk_index3(nch, out.y, out.z, k)) {
     float ra[8], rb[8], r[8];
     ld_chunk(a, k.b, k.ch, k.x, k.y, k.z, ra);
     ld_chunk(b, k.b, k.ch, k.x, k.y, k.z, rb);
@@ -213,9 +202,7 @@ __global__ void affine_act_kernel(DView in, DView out, const float *mult, const 
                                   float alpha) {
   ChunkIdx k;
   int nch = (out.c + 7) >> 3;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-       chunk_index(i, out.n, nch, out.x, out.y, out.z, k);
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  if (chunk_index3(nch, out.y, out.z, k)) {
     float r[8];
     ld_chunk(in, k.b, k.ch, k.x, k.y, k.z, r);
 #pragma unroll
@@ -238,9 +225,7 @@ __global__ void mergecrop_kernel(DView a, DView b, DView out, int oax, int oay, 
                                  int oby, int obz) {
   ChunkIdx k;
   int nch = (out.c + 7) >> 3;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-       chunk_index(i, out.n, nch, out.x, out.y, out.z, k);
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  if (chunk_index3(nch, out.y, out.z, k)) {
     float r[8];
     if ((a.c & 7) == 0 && a.blocked && b.blocked) {
       int ach = a.c >> 3;
@@ -269,9 +254,7 @@ __global__ void mergecrop_kernel(DView a, DView b, DView out, int oax, int oay, 
 __global__ void pad_copy_kernel(DView in, DView out, int px, int py, int pz) {
   ChunkIdx k;
   int nch = (out.c + 7) >> 3;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-       chunk_index(i, out.n, nch, out.x, out.y, out.z, k);
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  if (chunk_index3(nch, out.y, out.z, k)) {
     float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int x = k.x - px, y = k.y - py, z = k.z - pz;
     if (x >= 0 && y >= 0 && z >= 0 && x < in.x && y < in.y && z < in.z)
@@ -415,9 +398,7 @@ __global__ void subimage_kernel(SubParams p) {
 __global__ void deconv_gather_kernel(GatherDeconvParams p) {
   ChunkIdx k;
   int nch = (p.out.c + 7) >> 3;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-       chunk_index(i, p.out.n, nch, p.out.x, p.out.y, p.out.z, k);
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  if (chunk_index3(nch, p.out.y, p.out.z, k)) {
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int dx = 0; dx < p.kx; ++dx) {
       int ix = k.x - dx;
@@ -467,49 +448,42 @@ __global__ void deconv_gather_kernel(GatherDeconvParams p) {
 }
 
 // ------------------------------------------------------------------ launchers
-static int grid_for(long long work, int threads) {
-  long long g = (work + threads - 1) / threads;
-  long long cap = 148LL * 16;
-  if (g > cap) g = cap;
-  if (g < 1) g = 1;
-  return static_cast<int>(g);
-}
 
-static long long chunk_work(const DView &v) {
-  return static_cast<long long>(v.n) * ((v.c + 7) / 8) * v.x * v.y * v.z;
+static dim3 grid3(const DView &v, int threads) {
+  return dim3((v.y * v.z + threads - 1) / threads, v.x, v.n * ((v.c + 7) / 8));
 }
 
 int launch_copy(const DView &src, const DView &dst, cudaStream_t s) {
-  copy_kernel<<<grid_for(chunk_work(dst), 256), 256, 0, s>>>(src, dst);
+  copy_kernel<<<grid3(dst, 256), 256, 0, s>>>(src, dst);
   return check_cuda(cudaGetLastError(), "copy_kernel");
 }
 int launch_zero(const DView &dst, cudaStream_t s) {
-  zero_kernel<<<grid_for(chunk_work(dst), 256), 256, 0, s>>>(dst);
+  zero_kernel<<<grid3(dst, 256), 256, 0, s>>>(dst);
   return check_cuda(cudaGetLastError(), "zero_kernel");
 }
 int launch_pool(const DView &in, const DView &out, const int *w, const int *st, int mode,
                 cudaStream_t s) {
-  pool_kernel<<<grid_for(chunk_work(out), 256), 256, 0, s>>>(in, out, w[0], w[1], w[2], st[0],
+  pool_kernel<<<grid3(out, 256), 256, 0, s>>>(in, out, w[0], w[1], w[2], st[0],
                                                               st[1], st[2], mode);
   return check_cuda(cudaGetLastError(), "pool_kernel");
 }
 int launch_eltwise(const DView &a, const DView &b, const DView &out, int op, cudaStream_t s) {
-  eltwise_kernel<<<grid_for(chunk_work(out), 256), 256, 0, s>>>(a, b, out, op);
+  eltwise_kernel<<<grid3(out, 256), 256, 0, s>>>(a, b, out, op);
   return check_cuda(cudaGetLastError(), "eltwise_kernel");
 }
 int launch_affine_act(const DView &in, const DView &out, const float *m, const float *a, int act,
                       float alpha, cudaStream_t s) {
-  affine_act_kernel<<<grid_for(chunk_work(out), 256), 256, 0, s>>>(in, out, m, a, act, alpha);
+  affine_act_kernel<<<grid3(out, 256), 256, 0, s>>>(in, out, m, a, act, alpha);
   return check_cuda(cudaGetLastError(), "affine_act_kernel");
 }
 int launch_mergecrop(const DView &a, const DView &b, const DView &out, const int *oa,
                      const int *ob, cudaStream_t s) {
-  mergecrop_kernel<<<grid_for(chunk_work(out), 256), 256, 0, s>>>(a, b, out, oa[0], oa[1], oa[2],
+  mergecrop_kernel<<<grid3(out, 256), 256, 0, s>>>(a, b, out, oa[0], oa[1], oa[2],
                                                                    ob[0], ob[1], ob[2]);
   return check_cuda(cudaGetLastError(), "mergecrop_kernel");
 }
 int launch_pad_copy(const DView &in, const DView &out, const int *pads, cudaStream_t s) {
-  pad_copy_kernel<<<grid_for(chunk_work(out), 256), 256, 0, s>>>(in, out, pads[0], pads[1],
+  pad_copy_kernel<<<grid3(out, 256), 256, 0, s>>>(in, out, pads[0], pads[1],
                                                                   pads[2]);
   return check_cuda(cudaGetLastError(), "pad_copy_kernel");
 }
@@ -545,7 +519,7 @@ int launch_subimage(const SubParams &p, cudaStream_t s) {
 }
 
 int launch_deconv_gather(const GatherDeconvParams &p, cudaStream_t s) {
-  deconv_gather_kernel<<<grid_for(chunk_work(p.out), 128), 128, 0, s>>>(p);
+  deconv_gather_kernel<<<grid3(p.out, 128), 128, 0, s>>>(p);
   return check_cuda(cudaGetLastError(), "deconv_gather_kernel");
 }
 

@@ -379,20 +379,16 @@ class PlanRunner:
 
     def run(self, inputs) -> dict:
         """Reference-compatible forward (executor.py:168-198): host in, host out.
-        Inputs go host -> pinned staging -> HBM, outputs the reverse."""
-        torch = _torch()
+        Inputs go host -> pinned staging -> HBM and outputs the reverse, in
+        chunks that overlap the host copies with PCIe (staging.py)."""
+        from . import staging
         inputs = self._normalize(inputs)
         for name, arr in inputs.items():
-            self._in_pinned[name].numpy()[...] = np.asarray(arr, dtype=np.float32)
-        with torch.cuda.stream(self.stream):
-            for name, t in self._in_pinned.items():
-                self._in_std[name].copy_(t, non_blocking=True)
+            staging.upload(arr, self._in_pinned[name], self._in_std[name], self.stream)
         self._replay()
-        with torch.cuda.stream(self.stream):
-            for name, t in self._out_std.items():
-                self._out_pinned[name].copy_(t, non_blocking=True)
-        self.stream.synchronize()
-        return {name: t.numpy().copy() for name, t in self._out_pinned.items()}
+        outs = {name: staging.download(t, self._out_pinned[name], self.stream)
+                for name, t in self._out_std.items()}
+        return outs
 
     @property
     def h2d_bytes(self) -> int:
