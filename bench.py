@@ -267,7 +267,7 @@ def kernel_roofline(L, dev, peaks):
     from paper_1903_07525_b200.netspec import LayerKind
     runner = L["runner"]
     # the conv call is the op between the input pack and output unpack
-    conv_calls = [c for c, (kind, st, info) in zip(runner._calls[1:-1], runner._ops)
+    conv_calls = [c for c, (kind, st, info) in zip(runner.op_calls, runner._ops)
                   if kind is LayerKind.CONVOLUTION]
     call = conv_calls[0]
     s = torch.cuda.Stream(device=dev)

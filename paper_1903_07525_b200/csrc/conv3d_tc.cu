@@ -609,9 +609,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int i = 0; i < 8; ++i)
               if (i >= nvalid) r[i] = 0.f;
           }
-          if (FASTOUT)
-            store8_bf16_blocked(ov, obase + (c0 >> 3) * ov.s[1], r);
-          else
+          if (FASTOUT) {
+            if (ov.blocked) {
+              store8_bf16_blocked(ov, obase + (c0 >> 3) * ov.s[1], r);
+            } else {
+              // fused unpack: fp32 NCDHW network output written directly
+              float *op = static_cast<float *>(ov.data) + obase + c0 * ov.s[1];
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (i < nvalid) op[i * ov.s[1]] = r[i];
+            }
+          } else
             store8(ov, obase + (ov.blocked ? (c0 >> 3) * ov.s[1] : c0 * ov.s[1]), ov.blocked,
                    nvalid, r);
         }
@@ -700,7 +708,8 @@ static int launch_variant(const TcParams &p, const TcMaps &maps, int grid, cudaS
 template <bool BASE, bool PAIR>
 static int launch_act(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t s,
                       size_t smem) {
-  const bool fast = p.out.dtype == VXB_BF16 && p.out.blocked;
+  const bool fast = (p.out.dtype == VXB_BF16 && p.out.blocked) ||
+                    (p.out.dtype == VXB_F32 && !p.out.blocked);
   if (!fast) {
     if (PAIR) return set_error(VXB_EUNSUPPORTED, "pair mode needs a blocked bf16 output");
     return launch_variant<-1, false, BASE, false>(p, maps, grid, s, smem);

@@ -453,7 +453,91 @@ static dim3 grid3(const DView &v, int threads) {
   return dim3((v.y * v.z + threads - 1) / threads, v.x, v.n * ((v.c + 7) / 8));
 }
 
+// Network-boundary pack: fp32 NCDHW (z contiguous) -> bf16 blocked.  Each
+// thread converts 4 consecutive z of one 8-fmap chunk: 8 float4 loads (one
+// per fmap plane, 512 B per warp instruction) and 4 16-byte stores.
+__global__ void pack_std_f32_kernel(DView src, DView dst) {
+  const int zq = dst.z >> 2;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= dst.y * zq) return;
+  const int y = i / zq, z = (i - y * zq) * 4, x = blockIdx.y;
+  const int nch = (dst.c + 7) >> 3;
+  const int b = blockIdx.z / nch, ch = blockIdx.z - b * nch;
+  float v[8][4];
+#pragma unroll
+  for (int l = 0; l < 8; ++l) {
+    const int c = ch * 8 + l;
+    if (c < src.c) {
+      const float4 f = *reinterpret_cast<const float4 *>(
+          static_cast<const float *>(src.data) + b * src.s[0] + c * src.s[1] + x * src.s[2] +
+          y * src.s[3] + z);
+      v[l][0] = f.x; v[l][1] = f.y; v[l][2] = f.z; v[l][3] = f.w;
+    } else {
+      v[l][0] = v[l][1] = v[l][2] = v[l][3] = 0.f;
+    }
+  }
+  __nv_bfloat16 *o = static_cast<__nv_bfloat16 *>(dst.data) + b * dst.s[0] + ch * dst.s[1] +
+                     x * dst.s[2] + y * dst.s[3] + z * dst.s[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u;
+    __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[2 * k][q], v[2 * k + 1][q]);
+    *reinterpret_cast<uint4 *>(o + q * dst.s[4]) = u;
+  }
+}
+
+// The reverse at the output boundary: bf16 blocked -> fp32 NCDHW.
+__global__ void unpack_std_f32_kernel(DView src, DView dst) {
+  const int zq = src.z >> 2;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= src.y * zq) return;
+  const int y = i / zq, z = (i - y * zq) * 4, x = blockIdx.y;
+  const int nch = (src.c + 7) >> 3;
+  const int b = blockIdx.z / nch, ch = blockIdx.z - b * nch;
+  const __nv_bfloat16 *p = static_cast<const __nv_bfloat16 *>(src.data) + b * src.s[0] +
+                           ch * src.s[1] + x * src.s[2] + y * src.s[3] + z * src.s[4];
+  float v[4][8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 u = *reinterpret_cast<const uint4 *>(p + q * src.s[4]);
+    const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __bfloat1622float2(h[k]);
+      v[q][2 * k] = f.x;
+      v[q][2 * k + 1] = f.y;
+    }
+  }
+#pragma unroll
+  for (int l = 0; l < 8; ++l) {
+    const int c = ch * 8 + l;
+    if (c < dst.c)
+      *reinterpret_cast<float4 *>(static_cast<float *>(dst.data) + b * dst.s[0] + c * dst.s[1] +
+                                  x * dst.s[2] + y * dst.s[3] + z) =
+          make_float4(v[0][l], v[1][l], v[2][l], v[3][l]);
+  }
+}
+
+static bool std_f32_vec4(const DView &t) {
+  return !t.blocked && t.dtype == VXB_F32 && t.s[4] == 1 && (t.z & 3) == 0 &&
+         (reinterpret_cast<uintptr_t>(t.data) & 15) == 0 && (t.s[0] & 3) == 0 &&
+         (t.s[1] & 3) == 0 && (t.s[2] & 3) == 0 && (t.s[3] & 3) == 0;
+}
+static bool blocked_bf16(const DView &t) { return t.blocked && t.dtype == VXB_BF16; }
+
 int launch_copy(const DView &src, const DView &dst, cudaStream_t s) {
+  if (std_f32_vec4(src) && blocked_bf16(dst)) {
+    dim3 g((dst.y * (dst.z >> 2) + 127) / 128, dst.x, dst.n * ((dst.c + 7) / 8));
+    pack_std_f32_kernel<<<g, 128, 0, s>>>(src, dst);
+    return check_cuda(cudaGetLastError(), "pack_std_f32_kernel");
+  }
+  if (blocked_bf16(src) && std_f32_vec4(dst)) {
+    dim3 g((src.y * (src.z >> 2) + 127) / 128, src.x, src.n * ((src.c + 7) / 8));
+    unpack_std_f32_kernel<<<g, 128, 0, s>>>(src, dst);
+    return check_cuda(cudaGetLastError(), "unpack_std_f32_kernel");
+  }
   copy_kernel<<<grid3(dst, 256), 256, 0, s>>>(src, dst);
   return check_cuda(cudaGetLastError(), "copy_kernel");
 }

@@ -358,7 +358,7 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   // cta_group::2 pairs: M = 256 per MMA, each CTA ingests and reads only half
   // of every weight slab (halves the smem traffic that bounds high-fmap convs)
   p.pair = (!c.resident && spatial >= 2 && L.nt % 16 == 0 && L.nt / 8 <= 256 &&
-            a.out.dtype == VXB_BF16 && a.out.blocked &&
+            ((a.out.dtype == VXB_BF16 && a.out.blocked) || (a.out.dtype == VXB_F32 && !a.out.blocked)) &&
             env_int("VXB_TC_PAIR", 1) == 1) ? 1 : 0;
   p.cluster = p.pair || (!c.resident && env_int("VXB_TC_CLUSTER", 1) == 2 && spatial >= 2) ? 2 : 1;
   if (p.pair) {

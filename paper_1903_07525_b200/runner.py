@@ -265,8 +265,19 @@ class PlanRunner:
         for name, v in self._in_values.items():
             src = standard(self._in_std[name])
             calls.append(lambda s=src, d=v.dt: _copy(s, d))
+        # fused unpack: a conv/deconv whose result is only a network output
+        # writes the fp32 NCDHW output tensor directly from its epilogue
+        fused_out = {}
+        for name, v in self._out_values.items():
+            if v.readers == 1:
+                fused_out[id(v)] = name
+        self._fused_outputs = set()
         for kind, st, info in self._ops:
             out = info["out"].dt
+            oname = fused_out.get(id(info["out"]))
+            if oname is not None and kind in (LayerKind.CONVOLUTION, LayerKind.DECONVOLUTION):
+                out = standard(self._out_std[oname])
+                self._fused_outputs.add(oname)
             if kind is LayerKind.CONVOLUTION:
                 base = info["base"].dt if "base" in info else None
                 scale = st.base_scale if st.additive else None
@@ -321,7 +332,11 @@ class PlanRunner:
                              K.affine_act(x, out, None, None, act, alpha))
             else:
                 raise ExecutionError("plan step %r has unrunnable kind %s" % (st.name, kind))
+        n_in = len(self._in_values)
+        self.op_calls = calls[n_in:n_in + len(self._ops)]   # one device call per lowered op
         for name, v in self._out_values.items():
+            if name in self._fused_outputs:
+                continue
             dst = standard(self._out_std[name])
             calls.append(lambda s=v.dt, d=dst: _copy(s, d))
         self._calls = calls

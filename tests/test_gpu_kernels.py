@@ -257,6 +257,16 @@ def test_mergecrop_eltwise_affine_exact(golden_ops):
     np.testing.assert_allclose(D.to_host_standard(o), g["elu_y"], atol=1e-6, rtol=0)
 
 
+@pytest.mark.parametrize("shape", [(1, 13, 3, 5, 8), (2, 16, 2, 3, 12), (1, 1, 4, 4, 4)])
+def test_pack_unpack_vectorized_path_exact(shape, rng):
+    """z % 4 == 0 takes the float4 pack/unpack kernels; results bit-exact."""
+    D, _ = _dev()
+    x = R.bf16_round(rng.standard_normal(shape).astype(np.float32))
+    t = D.to_device_blocked(x)
+    assert not t.t[:, -1, ..., (shape[1] % 8 or 8):].float().abs().sum().item()
+    np.testing.assert_array_equal(D.to_host_standard(t), x)
+
+
 def test_layout_round_trip_exact(rng):
     D, _ = _dev()
     x = R.bf16_round(rng.standard_normal((2, 11, 3, 5, 7)).astype(np.float32))
