@@ -7,9 +7,9 @@
 // cross-correlation (no flip), stride 1, zero padding virtual.
 //
 // Mapping:
-//   M  = output voxels.  A CTA tile is bx x-slices x 16 (y) x 8 (z); every
-//        x-slice is one 128-row UMMA (rows = y*8 + z) with its own TMEM
-//        accumulator of nt fp32 columns.
+//   M  = output voxels.  A CTA tile is bx slices x 16 x 8 (z); every
+//        slice is one 128-row UMMA (rows = y*8 + z for x-slices) with its own
+//        TMEM accumulator of nt fp32 columns.
 //   N  = output fmaps (nt per tile, padded to 16).
 //   K  = input fmaps x taps, consumed in "steps" of 16 bf16: either two
 //        8-fmap chunks at one tap, or (odd last chunk) one chunk at two
@@ -25,10 +25,15 @@
 //   B operand: weights pre-packed on the host into per-step slabs in the
 //        core-matrix layout; streamed with cp.async.bulk (or loaded once and
 //        kept resident when the whole filter bank fits).
-// Warp roles: w0 = TMA producer, w1 = MMA issuer (+TMEM owner), w2..w5 =
-// epilogue (TMEM -> regs -> bias/base/act -> global).  Persistent CTAs walk
-// the tile list; TMEM accumulators are double buffered when they fit so the
-// epilogue of tile i overlaps the MMAs of tile i+1.
+//   Low/mid fmap counts (3*nt <= 256) fold the 3 taps along the slice axis
+//        into N (mma_group_fold): slices along x for 3x3x3, along y for
+//        1x3x3 (rows are then 16 x by 8 z).
+// Warp roles: w0 = A (halo) TMA producer, w1 = MMA issuer (+TMEM owner),
+// w2 = B (weights) producer, w3..w14 = epilogue (TMEM -> regs -> bias/base/
+// act -> global).  Persistent CTAs walk the tile list; TMEM accumulators are
+// double buffered when they fit so the epilogue of tile i overlaps the MMAs
+// of tile i+1.  CTA pairs (cta_group::2, M = 256) split the weight stream of
+// unfolded convs.
 #include <cuda_bf16.h>
 #include "vxb_internal.h"
 #include "vxb_ptx.cuh"
@@ -46,6 +51,7 @@ __device__ __forceinline__ GroupInfo group_info(const TcParams &p, int g) {
   int c = p.seg_chunks[seg];
   int nch = min(2, c - 2 * j);
   int steps = nch == 2 ? p.kx * p.ky * p.kz : p.kx * p.ky * ((p.kz + 1) >> 1);
+  if (p.fold) steps /= 3;   // the slice-axis taps ride in N
   GroupInfo gi{seg, 2 * j, nch, steps};
   return gi;
 }
@@ -72,20 +78,28 @@ __device__ __forceinline__ TileCoord decode_tile(const TcParams &p, int t) {
   t /= p.nb;
   c.nt = t % p.n_tiles;
   c.rep = t / p.n_tiles;
-  c.x0 = tx * p.bx;
-  c.y0 = ty * TILE_Y;
+  c.x0 = tx * p.ex;
+  c.y0 = ty * p.ey;
   c.z0 = tz * TILE_Z;
   return c;
 }
 
 // Fast activations for bf16 outputs: relative error < 3e-5, far below the
 // bf16 store rounding (3.9e-3); fp32 outputs use the libm forms below.
+// Branch-free (both forms computed, then selected): a data-dependent branch
+// per value here tripled the epilogue time of ELU layers.
 __device__ __forceinline__ float fast_expm1(float v) {
-  return fabsf(v) < 1e-2f ? fmaf(0.5f * v, v, v) : __expf(v) - 1.f;
+  const float e = __expf(fminf(v, 0.f)) - 1.f;
+  const float t = fmaf(0.5f * v, v, v);
+  return fabsf(v) < 1e-2f ? t : e;
+}
+__device__ __forceinline__ float fast_elu(float v, float alpha) {
+  const float m = alpha * fast_expm1(v);
+  return v > 0.f ? v : m;
 }
 __device__ __forceinline__ float apply_act_fast(float v, int act, float alpha) {
   if (act == VXB_ACT_RELU) return fmaxf(v, 0.f);
-  if (act == VXB_ACT_ELU) return v > 0.f ? v : alpha * fast_expm1(v);
+  if (act == VXB_ACT_ELU) return fast_elu(v, alpha);
   if (act == VXB_ACT_SIGMOID) return __fdividef(1.f, 1.f + __expf(-v));
   return v;
 }
@@ -171,7 +185,7 @@ constexpr int TC_THREADS = 96 + 32 * EPI_WARPS;   // A-TMA, MMA, B-TMA + epilogu
 
 // Byte offsets inside the dynamic smem block (all derivable from p).
 struct SmemMap {
-  uint32_t a, b, bias, scale, tab_pair, tab_odd, bars;
+  uint32_t a, b, bias, scale, bars;
 };
 __host__ __device__ inline SmemMap smem_map(const TcParams &p) {
   SmemMap m;
@@ -180,9 +194,7 @@ __host__ __device__ inline SmemMap smem_map(const TcParams &p) {
   m.bias = m.b + p.nb_stages * p.b_stage_bytes;
   const uint32_t cpad = p.n_tiles * p.nt;
   m.scale = m.bias + cpad * 4;
-  m.tab_pair = m.scale + cpad * 4;
-  m.tab_odd = m.tab_pair + p.kx * p.ky * p.kz * 4;
-  m.bars = (m.tab_odd + p.kx * p.ky * ((p.kz + 1) / 2) * 4 + 15) & ~15u;
+  m.bars = (m.scale + cpad * 4 + 15) & ~15u;
   return m;
 }
 
@@ -265,6 +277,70 @@ __device__ __forceinline__ void mma_group(
   }
 }
 
+// Folded variant: K steps run over the taps across the slice axis's
+// neighbours (dy or dx) and z only; the 3 slice-axis taps are stacked in the
+// B slab as N blocks [w(d=2); w(d=1); w(d=0)].  Input slice j feeds output
+// slices j-2..j, so one MMA of N = (#valid d) x nt writes the contiguous
+// accumulator columns of those slices: BX+2 MMAs per step instead of 3*BX.
+// The first step of a tile initialises every slice with its d=0 term
+// (accumulate = 0) before the overlapping MMAs accumulate on top.
+template <int BX>
+__device__ __forceinline__ void mma_group_fold(
+    const uint32_t a_lo0, const uint32_t a_hi, const uint32_t b_base0, const uint32_t b_stage_bytes,
+    const uint32_t b_hi, const uint32_t slab_inc, const uint32_t blk_inc, const uint32_t slice_inc,
+    const uint32_t d_base, const uint32_t nt, const uint32_t id1, const uint32_t id2,
+    const uint32_t id3, const int steps, const int tz_n, const uint32_t dz_step,
+    const uint32_t a_wrap, const MmaCtx &cx, int &b_st, int &b_ph, uint32_t &first) {
+  int tz = 0;
+  uint32_t off = 0;
+  for (int s0 = 0; s0 < steps; s0 += cx.bsteps) {
+    const int n = min(cx.bsteps, steps - s0);
+    if (cx.resident) {
+      if (cx.first_tile_iter) mbar_wait(&cx.b_full[b_st], 0);
+    } else {
+      mbar_wait(&cx.b_full[b_st], b_ph);
+    }
+    tc_fence_after();
+    uint32_t b_lo = desc_lo(b_base0 + b_st * b_stage_bytes, 128u);
+    for (int i = 0; i < n; ++i) {
+      const uint32_t a_lo = a_lo0 + off;
+      if (first) {
+#pragma unroll
+        for (int x = 0; x < BX; ++x)
+          umma_bf16_lohi_elect(d_base + x * nt, a_lo + x * slice_inc, a_hi, b_lo + 2 * blk_inc,
+                               b_hi, id1, 0u);
+#pragma unroll
+        for (int j = 1; j < BX + 2; ++j) {
+          const int dlo = j - BX + 1 > 1 ? j - BX + 1 : 1, dhi = j < 2 ? j : 2;
+          const uint32_t idn = dhi - dlo == 0 ? id1 : id2;
+          umma_bf16_lohi_elect(d_base + (j - dhi) * nt, a_lo + j * slice_inc, a_hi,
+                               b_lo + (2 - dhi) * blk_inc, b_hi, idn, 1u);
+        }
+        first = 0;
+      } else {
+#pragma unroll
+        for (int j = 0; j < BX + 2; ++j) {
+          const int dlo = j - BX + 1 > 0 ? j - BX + 1 : 0, dhi = j < 2 ? j : 2;
+          const uint32_t idn = dhi - dlo == 0 ? id1 : (dhi - dlo == 1 ? id2 : id3);
+          umma_bf16_lohi_elect(d_base + (j - dhi) * nt, a_lo + j * slice_inc, a_hi,
+                               b_lo + (2 - dhi) * blk_inc, b_hi, idn, 1u);
+        }
+      }
+      b_lo += slab_inc;
+      off += dz_step;
+      if (++tz == tz_n) {
+        tz = 0;
+        off += a_wrap;
+      }
+    }
+    if (!cx.resident) umma_commit_elect(&cx.b_empty[b_st]);
+    if (++b_st == cx.nb_stages) {
+      b_st = 0;
+      b_ph ^= 1;
+    }
+  }
+}
+
 template <int ACT, bool FASTOUT, bool BASE, bool PAIR>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     conv3d_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps) {
@@ -272,13 +348,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const SmemMap sm = smem_map(p);
+  if (threadIdx.x == 0) dbg_mark(p, 0, 5);
 
   uint8_t *a_buf = smem + sm.a;
   uint8_t *b_buf = smem + sm.b;
   float *s_bias = reinterpret_cast<float *>(smem + sm.bias);
   float *s_scale = reinterpret_cast<float *>(smem + sm.scale);
-  uint32_t *tab_pair = reinterpret_cast<uint32_t *>(smem + sm.tab_pair);
-  uint32_t *tab_odd = reinterpret_cast<uint32_t *>(smem + sm.tab_odd);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + sm.bars);
   uint64_t *a_full = bars;
   uint64_t *a_empty = a_full + p.na;
@@ -299,8 +374,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   while (tmem_cols < static_cast<uint32_t>(acc_cols * p.acc_stages)) tmem_cols <<= 1;
 
   // one-time setup by all threads: guard bytes behind every chunk array
-  // (read with zero weight by odd-chunk z-pair steps), per-fmap epilogue
-  // vectors, and the per-step A-operand byte offsets (no divisions later)
+  // (read with zero weight by odd-chunk z-pair steps) and the per-fmap
+  // epilogue vectors
   for (int s = 0; s < p.na; ++s)
     for (int c = 0; c < p.chunk_slots; ++c) {
       uint8_t *g = a_buf + s * p.a_stage_bytes + c * p.chunk_stride + p.chunk_bytes;
@@ -310,17 +385,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   for (int c = threadIdx.x; c < cpad; c += blockDim.x) {
     s_bias[c] = c < p.cout ? p.bias[c] : 0.f;
     s_scale[c] = (c < p.cout && p.scale) ? p.scale[c] : 1.f;
-  }
-  {
-    const int kzh = (p.kz + 1) >> 1;
-    for (int t = threadIdx.x; t < p.kx * p.ky * p.kz; t += blockDim.x) {
-      int dz = t % p.kz, dy = (t / p.kz) % p.ky, dx = t / (p.kz * p.ky);
-      tab_pair[t] = ((dx * p.hy + dy) * p.hz + dz) * 16;
-    }
-    for (int t = threadIdx.x; t < p.kx * p.ky * kzh; t += blockDim.x) {
-      int dz = 2 * (t % kzh), dy = (t / kzh) % p.ky, dx = t / (kzh * p.ky);
-      tab_odd[t] = ((dx * p.hy + dy) * p.hz + dz) * 16;
-    }
   }
   fence_proxy_async_smem();
 
@@ -405,7 +469,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // the weight stream of the current group
     if (lane == 0) {
       int b_st = 0, b_ph = 0;
-      const uint32_t slab = static_cast<uint32_t>(p.nt * SLAB_ROW_BYTES);
+      const uint32_t slab = static_cast<uint32_t>(p.slab_bytes);
       for (int tile = first_tile; tile < p.total_tiles; tile += tile_step) {
         if (p.resident && tile != first_tile) break;   // resident bank: loaded once
         TileCoord tc = decode_tile(p, tile);
@@ -460,9 +524,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t idesc = idesc_bf16(PAIR ? 256 : 128, p.nt);
       const uint32_t a_base0 = smem_u32(a_buf);
       const uint32_t b_base0 = smem_u32(b_buf);
-      const uint32_t slice_inc = (p.hy * p.hz * 16) >> 4;
-      const uint32_t b_inc = (p.nt * SLAB_ROW_BYTES / (PAIR ? 2 : 1)) >> 4;
-      const uint32_t a_hi = desc_hi(p.hz * 16);
+      const uint32_t slice_inc = p.a_slice_inc >> 4;
+      const uint32_t b_inc = (p.slab_bytes / (PAIR ? 2 : 1)) >> 4;
+      const uint32_t a_hi = desc_hi(p.a_sbo);
+      const uint32_t blk_inc = (p.nt * SLAB_ROW_BYTES) >> 4;
+      const uint32_t id1 = idesc_bf16(128, p.nt), id2 = idesc_bf16(128, 2 * p.nt),
+                     id3 = idesc_bf16(128, p.fold ? 3 * p.nt : p.nt);
+      // folded walk: z taps inside, the other non-slice axis outside
+      const uint32_t fold_stride = (p.slice_y ? p.hy * p.hz : p.hz);
       const uint32_t b_hi = desc_hi(256u);
       MmaCtx cx;
       cx.b_full = b_full;
@@ -478,13 +547,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_wait(&t_empty[acc], ((it / p.acc_stages) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_base = tmem_base + acc * acc_cols;
-        uint32_t accumulate = 0;
+        uint32_t accumulate = 0, first = 1;
         if (p.resident) b_st = 0;
         cx.first_tile_iter = it == 0;
         for (int g = 0; g < p.n_groups; ++g) {
           GroupInfo gi = group_info(p, g);
           mbar_wait(&a_full[a_st], a_ph);
           tc_fence_after();
+          if (g == 0 && lane == 0) dbg_mark(p, it, 1);
           const bool pair = gi.nch == 2;
           const int tz_n = pair ? p.kz : (p.kz + 1) >> 1;
           const uint32_t dz_step = pair ? 1u : 2u;
@@ -495,7 +565,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   mma_group<BXV, PAIR>(a_lo0, a_hi, b_base0, p.b_stage_bytes, b_hi, b_inc, slice_inc, d_base,    \
                        p.nt, idesc, gi.steps, tz_n, dz_step, dy_wrap, dx_wrap, p.ky, cx, b_st,  \
                        b_ph, accumulate)
-          switch (p.bx) {
+          if ((p.dbg_mode & 8) && p.resident) {
+            // debug: no MMAs (epilogue-only timing; resident weights only)
+          } else if (!PAIR && p.fold) {
+            const uint32_t a_wrap = fold_stride - tz_n * dz_step;
+#define VXB_FOLD(BXV)                                                                           \
+  mma_group_fold<BXV>(a_lo0, a_hi, b_base0, p.b_stage_bytes, b_hi, b_inc, blk_inc, slice_inc,    \
+                      d_base, p.nt, id1, id2, id3, gi.steps, tz_n, dz_step, a_wrap, cx, b_st,   \
+                      b_ph, first)
+            switch (p.bx) {
+              case 1: VXB_FOLD(1); break;
+              case 2: VXB_FOLD(2); break;
+              case 4: VXB_FOLD(4); break;
+              default: VXB_FOLD(8); break;
+            }
+#undef VXB_FOLD
+          } else switch (p.bx) {
             case 1: VXB_GROUP(1); break;
             case 2: VXB_GROUP(2); break;
             case 4: VXB_GROUP(4); break;
@@ -515,6 +600,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           umma_commit_pair_elect(&t_full[acc], pair_mask);
         else
           umma_commit_elect(&t_full[acc]);
+        if (lane == 0) dbg_mark(p, it, 2);
       }
     }
     __syncwarp();
@@ -527,7 +613,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int sub = (warp - 3) >> 2;          // which share of the work items
     constexpr int NSUB = EPI_WARPS / 4;
     const int row = q * 32 + lane;            // MMA row == TMEM lane
-    const int yy = row >> 3, zz = row & 7;
+    const int ra = row >> 3, zz = row & 7;    // row-axis offset (y, or x with slice_y), z
     const int col_items = p.nt >> 4;
     const int items = p.bx * col_items;
     const EpiView &ov = p.out;
@@ -537,11 +623,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     for (int tile = first_tile; tile < p.total_tiles; tile += tile_step, ++it) {
       TileCoord tc = decode_tile(p, tile);
       const int acc = it % p.acc_stages;
-      const int y = tc.y0 + yy, z = tc.z0 + zz;
-      const bool yz_ok = y < p.oy && z < p.oz && !tc.dummy;
-      const long long orow = p.out_rep_off[tc.rep] + tc.b * ov.s[0] + y * ov.s[3] + z * ov.s[4];
+      const int rc = (p.slice_y ? tc.x0 : tc.y0) + ra, z = tc.z0 + zz;
+      const int sc0 = p.slice_y ? tc.y0 : tc.x0, slim = p.slice_y ? p.oy : p.ox;
+      const bool yz_ok = rc < (p.slice_y ? p.ox : p.oy) && z < p.oz && !tc.dummy;
+      const int ra_dim = p.slice_y ? 2 : 3, sl_dim = p.slice_y ? 3 : 2;
+      const long long orow =
+          p.out_rep_off[tc.rep] + tc.b * ov.s[0] + rc * ov.s[ra_dim] + z * ov.s[4];
       const long long brow =
-          p.base_rep_off[tc.rep] + tc.b * bvw.s[0] + y * bvw.s[3] + z * bvw.s[4];
+          p.base_rep_off[tc.rep] + tc.b * bvw.s[0] + rc * bvw.s[ra_dim] + z * bvw.s[4];
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * acc_cols;
       mbar_wait_sleep(&t_full[acc], (it / p.acc_stages) & 1);
       if (warp == 3 && lane == 0) dbg_mark(p, it, 3);
@@ -553,14 +642,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       };
       auto load_base = [&](int item, float (&bv)[16]) {
         const int s = item / col_items, cc = (item % col_items) << 4;
-        const int x = tc.x0 + s;
-        const bool ok = yz_ok && x < p.ox;
+        const int x = sc0 + s;
+        const bool ok = yz_ok && x < slim;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           float t8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
           const int c0 = tc.nt * p.nt + cc + h * 8;
           if (ok && c0 < p.cout)
-            load8(bvw, brow + x * bvw.s[2] + (bvw.blocked ? (c0 >> 3) * bvw.s[1] : c0 * bvw.s[1]),
+            load8(bvw, brow + x * bvw.s[sl_dim] + (bvw.blocked ? (c0 >> 3) * bvw.s[1] : c0 * bvw.s[1]),
                   bvw.blocked, t8);
 #pragma unroll
           for (int i = 0; i < 8; ++i) bv[h * 8 + i] = t8[i];
@@ -568,9 +657,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       };
       auto finish = [&](int item, const uint32_t (&rv)[16], const float (&bv)[16]) {
         const int s = item / col_items, cc = (item % col_items) << 4;
-        const int x = tc.x0 + s;
-        if (!(yz_ok && x < p.ox)) return;
-        const long long obase = orow + x * ov.s[2];
+        const int x = sc0 + s;
+        if (!(yz_ok && x < slim)) return;
+        const long long obase = orow + x * ov.s[sl_dim];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c0 = tc.nt * p.nt + cc + h * 8;
@@ -595,7 +684,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               for (int i = 0; i < 8; ++i) r[i] = fmaxf(r[i], 0.f);
             } else if (act == VXB_ACT_ELU) {
 #pragma unroll
-              for (int i = 0; i < 8; ++i) r[i] = r[i] > 0.f ? r[i] : p.alpha * fast_expm1(r[i]);
+              for (int i = 0; i < 8; ++i) r[i] = fast_elu(r[i], p.alpha);
             } else if (act == VXB_ACT_SIGMOID) {
 #pragma unroll
               for (int i = 0; i < 8; ++i) r[i] = __fdividef(1.f, 1.f + __expf(-r[i]));
@@ -635,6 +724,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       while (item < items) {
         const int nxt = item + NSUB;
         tmem_wait_ld16(ra);
+        if (warp == 3 && lane == 0 && item == sub) dbg_mark(p, it, 7);
         if (nxt < items) {
           tmem_ld16_issue(taddr_of(nxt), rb);
           if (BASE) load_base(nxt, bb2);
@@ -663,6 +753,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 
   __syncthreads();
+  if (threadIdx.x == 0) dbg_mark(p, 0, 6);
   if (p.cluster == 2) cluster_sync_all();   // no CTA leaves while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();

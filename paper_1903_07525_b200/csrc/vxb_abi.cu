@@ -90,16 +90,30 @@ struct TcGroup {
 
 struct TcLayout {
   int npad, n_tiles, nt;
+  int fold;         // 0, 1 = x taps folded into N (slices along x), 2 = y taps (slices along y)
+  int slab;         // B bytes per device K step
   int seg_chunks[2];
   std::vector<TcGroup> groups;
-  long long steps;  // per (rep, ntile)
+  long long steps;  // device K steps per (rep, ntile)
 };
+
+// Tap folding (conv3d_tc.cu mma_group_fold): with 3 taps along the slice axis
+// and 3*nt <= 256, one MMA per input slice serves up to 3 output slices.
+// 3x3x3 folds x (slices along x); 1x3x3 folds y (slices along y).
+static int tc_fold_axis(int nt, const int k[3]) {
+  if (env_int("VXB_TC_FOLD", 1) == 0 || 3 * nt > 256) return 0;
+  if (k[0] == 3) return 1;
+  if (k[0] == 1 && k[1] == 3) return 2;
+  return 0;
+}
 
 static TcLayout tc_layout(int cin0, int cin1, int cout, const int k[3]) {
   TcLayout L;
   L.npad = round_up(cout, 16);
   L.n_tiles = ceil_div(L.npad, 256);
   L.nt = round_up(ceil_div(L.npad, L.n_tiles), 16);
+  L.fold = L.n_tiles == 1 ? tc_fold_axis(L.nt, k) : 0;
+  L.slab = (L.fold ? 3 : 1) * L.nt * SLAB_ROW_BYTES;
   L.seg_chunks[0] = ceil_div(cin0, 8);
   L.seg_chunks[1] = cin1 > 0 ? ceil_div(cin1, 8) : 0;
   L.steps = 0;
@@ -111,6 +125,7 @@ static TcLayout tc_layout(int cin0, int cin1, int cout, const int k[3]) {
       g.chunk0 = 2 * j;
       g.nch = std::min(2, c - 2 * j);
       g.steps = g.nch == 2 ? k[0] * k[1] * k[2] : k[0] * k[1] * ceil_div(k[2], 2);
+      if (L.fold) g.steps /= 3;
       L.groups.push_back(g);
       L.steps += g.steps;
     }
@@ -119,7 +134,7 @@ static TcLayout tc_layout(int cin0, int cin1, int cout, const int k[3]) {
 }
 
 static size_t tc_bytes_per_rep(const TcLayout &L) {
-  return static_cast<size_t>(L.n_tiles) * L.steps * L.nt * SLAB_ROW_BYTES;
+  return static_cast<size_t>(L.n_tiles) * L.steps * L.slab;
 }
 
 static inline uint16_t f32_to_bf16_bits(float f) {
@@ -140,15 +155,15 @@ static inline uint16_t f32_to_bf16_bits(float f) {
 template <class WFn>
 static void tc_pack(const TcLayout &L, int cin0, int cin1, int cout, const int k[3], WFn wtap,
                     uint8_t *dst) {
-  const int slab = L.nt * SLAB_ROW_BYTES;
+  const int slab = L.slab;
   const int kzh = ceil_div(k[2], 2);
-  long long step_idx = 0;
   for (int nti = 0; nti < L.n_tiles; ++nti) {
-    step_idx = static_cast<long long>(nti) * L.steps;
+    long long step_base = static_cast<long long>(nti) * L.steps;
     for (const TcGroup &g : L.groups) {
       const int cin_seg = g.seg == 0 ? cin0 : cin1;
       const int cbase = g.seg == 0 ? 0 : cin0;
-      for (int t = 0; t < g.steps; ++t, ++step_idx) {
+      const int taps = g.steps * (L.fold ? 3 : 1);
+      for (int t = 0; t < taps; ++t) {
         int dx, dy, dz;
         if (g.nch == 2) {
           dz = t % k[2];
@@ -159,7 +174,18 @@ static void tc_pack(const TcLayout &L, int cin0, int cin1, int cout, const int k
           dy = (t / kzh) % k[1];
           dx = t / (kzh * k[1]);
         }
-        uint16_t *s = reinterpret_cast<uint16_t *>(dst + step_idx * slab);
+        // device step and N block of this tap (unfolded: the tap order itself)
+        const int tzn = g.nch == 2 ? k[2] : kzh, tzi = g.nch == 2 ? dz : dz / 2;
+        int step = t, blk = 0;
+        if (L.fold == 1) {
+          step = dy * tzn + tzi;
+          blk = 2 - dx;
+        } else if (L.fold == 2) {
+          step = dx * tzn + tzi;
+          blk = 2 - dy;
+        }
+        uint16_t *s = reinterpret_cast<uint16_t *>(dst + (step_base + step) * slab) +
+                      blk * L.nt * SLAB_ROW_BYTES / 2;
         for (int n = 0; n < L.nt; ++n) {
           const int co = nti * L.nt + n;
           for (int kk = 0; kk < 16; ++kk) {
@@ -177,6 +203,7 @@ static void tc_pack(const TcLayout &L, int cin0, int cin1, int cout, const int k
           }
         }
       }
+      step_base += g.steps;
     }
   }
 }
@@ -187,13 +214,14 @@ struct TcConfig {
   size_t smem;
 };
 
-static int tc_configure(const TcLayout &L, const int k[3], int ox, int reps, TcConfig &c) {
+static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, int reps,
+                        TcConfig &c) {
   const int budget = 227 * 1024 - 6144;  // room for bias/scale/tap tables/barriers
   c.acc = env_int("VXB_TC_ACC", 2);
   if (c.acc != 1 && c.acc != 2) c.acc = 2;
   int bx_cap = env_int("VXB_TC_BX", 8);
   c.bx = 1;
-  while (c.bx * 2 <= bx_cap && c.bx * 2 * L.nt * c.acc <= 512 && c.bx < ox) c.bx *= 2;
+  while (c.bx * 2 <= bx_cap && c.bx * 2 * L.nt * c.acc <= 512 && c.bx < slice_extent) c.bx *= 2;
   if (c.bx * L.nt * c.acc > 512) return set_error(VXB_EUNSUPPORTED, "TMEM overflow");
   bool any_pair = false;
   int max_steps = 1;
@@ -201,10 +229,11 @@ static int tc_configure(const TcLayout &L, const int k[3], int ox, int reps, TcC
     any_pair |= g.nch == 2;
     max_steps = std::max(max_steps, g.steps);
   }
-  const int slab = L.nt * SLAB_ROW_BYTES;
+  const int slab = L.slab;
   int na_cap = std::max(2, std::min(6, env_int("VXB_TC_NA", 3)));
   for (;;) {
-    const int hx = c.bx + k[0] - 1, hy = TILE_Y + k[1] - 1, hz = TILE_Z + k[2] - 1;
+    const int sx = L.fold == 2 ? TILE_Y : c.bx, sy = L.fold == 2 ? c.bx : TILE_Y;
+    const int hx = sx + k[0] - 1, hy = sy + k[1] - 1, hz = TILE_Z + k[2] - 1;
     c.chunk_bytes = hx * hy * hz * 16;
     c.chunk_stride = round_up(c.chunk_bytes + 128, 128);
     c.chunk_slots = any_pair ? 2 : 1;
@@ -337,7 +366,8 @@ struct TcLaunch {
 static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   TcLayout L = tc_layout(a.cin0, a.cin1, a.cout, a.k);
   TcConfig c;
-  int rc = tc_configure(L, a.k, a.ox, a.reps, c);
+  const int slice_y = L.fold == 2;
+  int rc = tc_configure(L, a.k, slice_y ? a.oy : a.ox, a.reps, c);
   if (rc) return rc;
   TcParams p;
   memset(&p, 0, sizeof(p));
@@ -348,8 +378,13 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   p.bx = c.bx;
   p.nt = L.nt;
   p.acc_stages = c.acc;
-  p.tiles_x = ceil_div(a.ox, c.bx);
-  p.tiles_y = ceil_div(a.oy, TILE_Y);
+  p.slice_y = slice_y;
+  p.fold = L.fold != 0;
+  p.ex = slice_y ? TILE_Y : c.bx;
+  p.ey = slice_y ? c.bx : TILE_Y;
+  p.slab_bytes = L.slab;
+  p.tiles_x = ceil_div(a.ox, p.ex);
+  p.tiles_y = ceil_div(a.oy, p.ey);
   p.tiles_z = ceil_div(a.oz, TILE_Z);
   p.n_tiles = L.n_tiles;
   p.reps = a.reps;
@@ -357,14 +392,20 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   // weight-streaming convs run as CTA pairs sharing one multicast B stream
   // cta_group::2 pairs: M = 256 per MMA, each CTA ingests and reads only half
   // of every weight slab (halves the smem traffic that bounds high-fmap convs)
-  p.pair = (!c.resident && spatial >= 2 && L.nt % 16 == 0 && L.nt / 8 <= 256 &&
+  // Resident-weight (low-fmap) convs pair up too: their MMAs are bound by a
+  // per-instruction cost (~48 cycles at N <= 32), so one M = 256 instruction
+  // serving two SMs halves the MMA time per tile.
+  const int pair_env = env_int("VXB_TC_PAIR", 1);
+  p.pair = (!p.fold && spatial >= 2 && L.nt % 16 == 0 && L.nt / 8 <= 256 &&
             ((a.out.dtype == VXB_BF16 && a.out.blocked) || (a.out.dtype == VXB_F32 && !a.out.blocked)) &&
-            env_int("VXB_TC_PAIR", 1) == 1) ? 1 : 0;
+            (pair_env == 1 || (pair_env == 2 && !c.resident))) ? 1 : 0;
   p.cluster = p.pair || (!c.resident && env_int("VXB_TC_CLUSTER", 1) == 2 && spatial >= 2) ? 2 : 1;
   if (p.pair) {
     c.b_stage /= 2;
-    const int budget = 227 * 1024 - 6144;
-    c.nb = std::max(2, std::min(6, (budget - c.na * c.a_stage) / c.b_stage));
+    if (!c.resident) {
+      const int budget = 227 * 1024 - 6144;
+      c.nb = std::max(2, std::min(6, (budget - c.na * c.a_stage) / c.b_stage));
+    }
   }
   const long long spatial_pad = (spatial + p.cluster - 1) / p.cluster * p.cluster;
   long long total = spatial_pad * p.n_tiles * p.reps;
@@ -375,9 +416,11 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   p.kx = a.k[0];
   p.ky = a.k[1];
   p.kz = a.k[2];
-  p.hx = c.bx + a.k[0] - 1;
-  p.hy = TILE_Y + a.k[1] - 1;
+  p.hx = p.ex + a.k[0] - 1;
+  p.hy = p.ey + a.k[1] - 1;
   p.hz = TILE_Z + a.k[2] - 1;
+  p.a_slice_inc = (slice_y ? p.hz : p.hy * p.hz) * 16;
+  p.a_sbo = (slice_y ? p.hy * p.hz : p.hz) * 16;
   for (int i = 0; i < 3; ++i) p.pad[i] = a.pad[i];
   TcMaps maps;
   memset(&maps, 0, sizeof(maps));
@@ -415,7 +458,7 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_error(VXB_ECUDA, "weight tensor map failed (%d)", (int)r);
   }
-  p.w_ntile_stride = L.steps * L.nt * SLAB_ROW_BYTES;
+  p.w_ntile_stride = L.steps * L.slab;
   p.w_rep_stride = static_cast<long long>(tc_bytes_per_rep(L));
   p.bias = a.bias;
   p.scale = a.scale;
@@ -440,14 +483,11 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
     cudaMemsetAsync(g_dbg, 0, kDbgBytes, stream);
     p.dbg = static_cast<unsigned long long *>(g_dbg);
   }
-  uint32_t tmem_cols = 32;
-  while (tmem_cols < static_cast<uint32_t>(c.bx * L.nt * c.acc)) tmem_cols <<= 1;
   c.smem = tc_smem_bytes(p);
   if (c.smem > 227 * 1024) return set_error(VXB_EUNSUPPORTED, "conv needs %zu B smem", c.smem);
-  int per_sm = std::min<int>(static_cast<int>((228 * 1024) / (c.smem + 1024)),
-                             static_cast<int>(512 / tmem_cols));
-  per_sm = std::max(1, std::min(per_sm, env_int("VXB_TC_CTAS_PER_SM", 4)));
-  int grid = static_cast<int>(std::min<long long>(total, static_cast<long long>(sms) * per_sm));
+  // persistent: one CTA per SM (480 threads x ~100 registers leaves no room
+  // for a second one, and the smem ring is sized for the whole SM)
+  int grid = static_cast<int>(std::min<long long>(total, static_cast<long long>(sms)));
   grid = std::max(p.cluster, grid / p.cluster * p.cluster);
   return launch_conv3d_tc(p, maps, grid, stream);
 }

@@ -30,8 +30,15 @@ struct TcParams {
   int spatial_real, spatial_pad;  // tiles per (rep, ntile); padded to the cluster size
   int cluster;                    // 1, or 2 = CTA pair sharing B via TMA multicast
   int pair;                       // cta_group::2 MMA (M = 256), each CTA holds half of B
-  int bx;                      // x-slices per CTA tile (each slice = 128 MMA rows)
+  int bx;                      // slices per CTA tile (each slice = 128 MMA rows)
   int nt;                      // N per tile (multiple of 16)
+  // Slice axis: slices run along x (rows = 16 y x 8 z) or, with slice_y,
+  // along y (rows = 16 x x 8 z).  fold: the 3 taps along the slice axis are
+  // folded into N (one MMA per input slice covers up to 3 output slices).
+  int slice_y, fold;
+  int ex, ey;                  // tile extents along x and y
+  int slab_bytes;              // B bytes per K step (nt rows, or 3*nt when folded)
+  int a_slice_inc, a_sbo;      // smem bytes between slices / between 8-row groups
   int acc_stages;              // TMEM accumulator stages
   int kx, ky, kz;
   int hx, hy, hz;              // halo tile extents

@@ -46,9 +46,27 @@ def _par_copy(dst: np.ndarray, src: np.ndarray) -> None:
     dst[:] = src
 
 
-def upload(host: np.ndarray, pinned, device_tensor, stream) -> None:
-    """host (any float32-convertible array) -> device_tensor via pinned chunks."""
+def pinned_empty(shape) -> np.ndarray:
+    """Page-locked float32 host array: ``upload``/``download`` move it with one
+    DMA each way, skipping the staging copy."""
     import torch
+    return torch.empty(tuple(shape), dtype=torch.float32, pin_memory=True).numpy()
+
+
+def is_pinned(a: np.ndarray) -> bool:
+    import torch
+    return (isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous
+            and torch.from_numpy(a).is_pinned())
+
+
+def upload(host: np.ndarray, pinned, device_tensor, stream) -> None:
+    """host (any float32-convertible array) -> device_tensor via pinned chunks
+    (a page-locked float32 array goes in one DMA)."""
+    import torch
+    if is_pinned(host):
+        with torch.cuda.stream(stream):
+            device_tensor.copy_(torch.from_numpy(host), non_blocking=True)
+        return
     src = np.ascontiguousarray(host, dtype=np.float32).reshape(-1).view(np.uint8)
     stage = pinned.reshape(-1).view(torch.uint8)
     stage_np = stage.numpy()
@@ -61,9 +79,19 @@ def upload(host: np.ndarray, pinned, device_tensor, stream) -> None:
             dst[o:o + n].copy_(stage[o:o + n], non_blocking=True)
 
 
-def download(device_tensor, pinned, stream) -> np.ndarray:
-    """device_tensor -> new host float32 array via pinned chunks."""
+def download(device_tensor, pinned, stream, out=None) -> np.ndarray:
+    """device_tensor -> host float32 array via pinned chunks; ``out`` (a
+    page-locked array from ``pinned_empty``) receives it in one DMA."""
     import torch
+    if out is not None:
+        if tuple(out.shape) != tuple(device_tensor.shape) or not is_pinned(out):
+            from .errors import ExecutionError
+            raise ExecutionError("out= must be a pinned float32 array of shape %s"
+                                 % (tuple(device_tensor.shape),))
+        with torch.cuda.stream(stream):
+            torch.from_numpy(out).copy_(device_tensor, non_blocking=True)
+        stream.synchronize()
+        return out
     src = device_tensor.reshape(-1).view(torch.uint8)
     stage = pinned.reshape(-1).view(torch.uint8)
     stage_np = stage.numpy()

@@ -65,6 +65,9 @@ CASES = [
     (80, 80, (6, 24, 24), (1, 3, 3), (0, 1, 1), "elu", True),
     (256, 512, (3, 11, 11), (3, 3, 3), (0, 0, 0), "relu", False),
     (5, 7, (8, 8, 8), (3, 3, 3), (0, 0, 0), None, False),
+    # 1x3x3 folded along y with x > 16 (two partial row tiles) and y < slices
+    (24, 40, (21, 7, 9), (1, 3, 3), (0, 1, 1), "relu", True),
+    (48, 48, (7, 30, 13), (3, 3, 3), (1, 1, 1), "elu", False),
 ]
 
 
@@ -83,6 +86,20 @@ def test_tc_conv_matches_oracle(case):
     want = _ref_bf16(x, w, b, pad, act, base, scale)
     mx, l2 = R.normalized_error(got, want)
     assert mx < BF16_TOL and l2 < 3e-3, (mx, l2)
+
+
+@pytest.mark.parametrize("k,pad", [((3, 3, 3), (1, 1, 1)), ((1, 3, 3), (0, 1, 1))])
+def test_tap_fold_matches_unfolded(k, pad, monkeypatch):
+    """Folding the slice-axis taps into N only reorders the fp32 sums."""
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-1, 1, (2, 16, 9, 21, 10)).astype(np.float32)
+    w = (rng.standard_normal((16, 16) + k) * 0.1).astype(np.float32)
+    b = rng.standard_normal(16).astype(np.float32)
+    folded, _ = _conv_bf16(x, w, b, pad, "elu", out_dtype="fp32")
+    monkeypatch.setenv("VXB_TC_FOLD", "0")
+    plain, _ = _conv_bf16(x, w, b, pad, "elu", out_dtype="fp32")
+    mx, _ = R.normalized_error(folded, plain)
+    assert mx < 1e-5, mx
 
 
 def test_tc_conv_fp32_output_and_batch2():

@@ -12,6 +12,7 @@ BASELINE config networks at reduced sizes.  Tolerances:
 
 import numpy as np
 import pytest
+import torch
 
 from vxb_testutil import cuda_ready
 
@@ -97,6 +98,20 @@ def test_runner_graph_replay_deterministic_and_validates():
         runner.run({"nope": x})
     with pytest.raises(P.ExecutionError):
         runner.run(x[:, :, :4])
+    # page-locked in/out (one DMA each way) and device-resident static buffers
+    from paper_1903_07525_b200 import staging
+    xp = staging.pinned_empty(x.shape)
+    xp[...] = x
+    op = staging.pinned_empty(a.shape)
+    c = runner.run(xp, out={"out_elu": op})["out_elu"]
+    assert c is op
+    np.testing.assert_array_equal(c, a)
+    with pytest.raises(P.ExecutionError):
+        runner.run(x, out={"out_elu": np.empty_like(a)})
+    bufs = runner.input_buffers()
+    bufs["data"].copy_(torch.from_numpy(x))
+    d = runner.run_device(bufs)["out_elu"].cpu().numpy()
+    np.testing.assert_array_equal(d, a)
 
 
 def test_run_tiled_equals_manual_assembly():

@@ -51,14 +51,35 @@ def test_host_packing_sizes_and_selection():
     n = L.vxb_conv_weights_bytes(16, 16, k3, s1, 0)
     dst = np.zeros(n, np.uint8)
     assert L.vxb_conv_pack_weights(w.ctypes.data, 16, 16, k3, s1, 0, dst.ctypes.data, n) == 0
-    # slab for step 0 (tap 0,0,0): row n, k-half h, lane l at (n/8)*256 + h*128 + (n%8)*16 + 2l
+    # C16 3x3x3 folds the x taps into N: device step (dy, dz) holds three
+    # nt-row blocks [dx=2; dx=1; dx=0].  Inside a block: row n, k-half h,
+    # lane l at (n/8)*256 + h*128 + (n%8)*16 + 2l
     bf = dst.view(np.uint16)
     from oracle.ref_numpy import bf16_round
+
+    def at(buf, byte):
+        return (np.array([buf[byte // 2]], np.uint16).astype(np.uint32) << 16).view(np.float32)[0]
+
     for (co, ci) in [(0, 0), (5, 3), (9, 12), (15, 15)]:
         h, l = ci // 8, ci % 8
-        off = ((co // 8) * 256 + h * 128 + (co % 8) * 16 + 2 * l) // 2
-        val = np.array([bf[off]], np.uint16).astype(np.uint32) << 16
-        assert val.view(np.float32)[0] == bf16_round(w[co, ci, 0, 0, 0])
+        row = (co // 8) * 256 + h * 128 + (co % 8) * 16 + 2 * l
+        for dx in range(3):
+            for (dy, dz) in [(0, 0), (1, 2), (2, 1)]:
+                step = dy * 3 + dz
+                byte = step * 3 * 16 * 32 + (2 - dx) * 16 * 32 + row
+                assert at(bf, byte) == bf16_round(w[co, ci, dx, dy, dz])
+    # C128 (3*nt > 256) stays unfolded: step = (dx, dy, dz) tap order
+    w2 = np.random.default_rng(1).standard_normal((128, 16, 3, 3, 3)).astype(np.float32)
+    n2 = L.vxb_conv_weights_bytes(16, 128, k3, s1, 0)
+    assert n2 == 27 * 128 * 32
+    dst2 = np.zeros(n2, np.uint8)
+    assert L.vxb_conv_pack_weights(w2.ctypes.data, 16, 128, k3, s1, 0, dst2.ctypes.data, n2) == 0
+    bf2 = dst2.view(np.uint16)
+    for (co, ci, dx, dy, dz) in [(0, 0, 0, 0, 0), (77, 9, 2, 1, 0), (127, 15, 1, 2, 2)]:
+        h, l = ci // 8, ci % 8
+        step = (dx * 3 + dy) * 3 + dz
+        byte = step * 128 * 32 + (co // 8) * 256 + h * 128 + (co % 8) * 16 + 2 * l
+        assert at(bf2, byte) == bf16_round(w2[co, ci, dx, dy, dz])
     assert L.vxb_conv_pack_weights(w.ctypes.data, 16, 16, k3, s1, 0, dst.ctypes.data, 10) != 0
     assert b"need" in L.vxb_last_error()
 
