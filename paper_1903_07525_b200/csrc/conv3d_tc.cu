@@ -84,24 +84,12 @@ __device__ __forceinline__ TileCoord decode_tile(const TcParams &p, int t) {
   return c;
 }
 
-// Fast activations for bf16 outputs: relative error < 3e-5, far below the
-// bf16 store rounding (3.9e-3); fp32 outputs use the libm forms below.
-// Branch-free (both forms computed, then selected): a data-dependent branch
-// per value here tripled the epilogue time of ELU layers.
-__device__ __forceinline__ float fast_expm1(float v) {
-  const float e = __expf(fminf(v, 0.f)) - 1.f;
-  const float t = fmaf(0.5f * v, v, v);
-  return fabsf(v) < 1e-2f ? t : e;
-}
+// Fast ELU for the tensor-core epilogue: alpha*(2^(v*log2 e) - 1), selected
+// branch-free (a data-dependent branch per value tripled the epilogue time).
+// Absolute error ~1e-7 near 0, far below the bf16 operand rounding.
 __device__ __forceinline__ float fast_elu(float v, float alpha) {
-  const float m = alpha * fast_expm1(v);
+  const float m = fmaf(alpha, __expf(v), -alpha);
   return v > 0.f ? v : m;
-}
-__device__ __forceinline__ float apply_act_fast(float v, int act, float alpha) {
-  if (act == VXB_ACT_RELU) return fmaxf(v, 0.f);
-  if (act == VXB_ACT_ELU) return fast_elu(v, alpha);
-  if (act == VXB_ACT_SIGMOID) return __fdividef(1.f, 1.f + __expf(-v));
-  return v;
 }
 __device__ __forceinline__ float apply_act(float v, int act, float alpha) {
   if (act == VXB_ACT_RELU) return v > 0.f ? v : 0.f;
@@ -348,6 +336,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const SmemMap sm = smem_map(p);
+  pdl_trigger();
   if (threadIdx.x == 0) dbg_mark(p, 0, 5);
 
   uint8_t *a_buf = smem + sm.a;
@@ -419,6 +408,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (p.cluster == 2) cluster_sync_all();   // peer barriers initialised before multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();   // activations (inputs, residual, output buffer) belong to the predecessor until here
 
   if (warp == 0) {
     // ===================== A producer: halo tiles (TMA 4-D boxes) ==========
@@ -576,7 +566,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             switch (p.bx) {
               case 1: VXB_FOLD(1); break;
               case 2: VXB_FOLD(2); break;
+              case 3: VXB_FOLD(3); break;
               case 4: VXB_FOLD(4); break;
+              case 6: VXB_FOLD(6); break;
               default: VXB_FOLD(8); break;
             }
 #undef VXB_FOLD
@@ -606,9 +598,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncwarp();
   } else {
     // ===================== epilogue (EPI_WARPS warps, EPI_WARPS/4 per quarter) ==
-    // Work item = (x-slice, 16 accumulator columns).  TMEM loads and residual
-    // loads of item k+1 are in flight while item k is finished (software
-    // pipeline, two register sets).
+    // Work item = (slice, 16 accumulator columns).  The TMEM load of item k+1
+    // and the residual loads of items k+1, k+2 are in flight while item k is
+    // finished (software pipeline).
     const int q = warp & 3;                   // TMEM lane quarter this warp may access
     const int sub = (warp - 3) >> 2;          // which share of the work items
     constexpr int NSUB = EPI_WARPS / 4;
@@ -619,6 +611,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const EpiView &ov = p.out;
     const EpiView &bvw = p.base;
     const int act = ACT >= 0 ? ACT : p.act;
+    const bool braw = BASE && bvw.dtype == VXB_BF16 && bvw.blocked;
     int it = 0;
     for (int tile = first_tile; tile < p.total_tiles; tile += tile_step, ++it) {
       TileCoord tc = decode_tile(p, tile);
@@ -632,15 +625,41 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const long long brow =
           p.base_rep_off[tc.rep] + tc.b * bvw.s[0] + rc * bvw.s[ra_dim] + z * bvw.s[4];
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * acc_cols;
-      mbar_wait_sleep(&t_full[acc], (it / p.acc_stages) & 1);
-      if (warp == 3 && lane == 0) dbg_mark(p, it, 3);
-      tc_fence_after();
 
       auto taddr_of = [&](int item) {
         const int s = item / col_items, cc = (item % col_items) << 4;
         return tbase + s * p.nt + cc;
       };
-      auto load_base = [&](int item, float (&bv)[16]) {
+      // residual operand: bf16 blocked bases are prefetched raw two items
+      // ahead (the first ones before the accumulator is even ready); other
+      // layouts are read at use
+      auto base_issue = [&](int item, uint4 (&d)[2]) {
+        const int s = item / col_items, cc = (item % col_items) << 4;
+        const int x = sc0 + s;
+        const bool ok = yz_ok && x < slim;
+        const __nv_bfloat16 *bp = static_cast<const __nv_bfloat16 *>(bvw.data) + brow +
+                                  x * bvw.s[sl_dim];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c0 = tc.nt * p.nt + cc + h * 8;
+          d[h] = make_uint4(0u, 0u, 0u, 0u);
+          if (ok && c0 < p.cout) d[h] = __ldg(reinterpret_cast<const uint4 *>(bp + (c0 >> 3) * bvw.s[1]));
+        }
+      };
+      auto base_get = [&](int item, const uint4 (&d)[2], float (&bv)[16]) {
+        if (braw) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const __nv_bfloat162 *hv = reinterpret_cast<const __nv_bfloat162 *>(&d[h]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 f = __bfloat1622float2(hv[i]);
+              bv[h * 8 + 2 * i] = f.x;
+              bv[h * 8 + 2 * i + 1] = f.y;
+            }
+          }
+          return;
+        }
         const int s = item / col_items, cc = (item % col_items) << 4;
         const int x = sc0 + s;
         const bool ok = yz_ok && x < slim;
@@ -715,29 +734,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       };
 
       uint32_t ra[16], rb[16];
-      float ba[16], bb2[16];
+      uint4 qa[2], qb[2];
+      float bv[16];
       int item = (p.dbg_mode & 1) ? items : sub;
-      if (item < items) {
-        tmem_ld16_issue(taddr_of(item), ra);
-        if (BASE) load_base(item, ba);
+      if (braw) {
+        if (item < items) base_issue(item, qa);
+        if (item + NSUB < items) base_issue(item + NSUB, qb);
       }
+      mbar_wait_sleep(&t_full[acc], (it / p.acc_stages) & 1);
+      if (warp == 3 && lane == 0) dbg_mark(p, it, 3);
+      tc_fence_after();
+      if (item < items) tmem_ld16_issue(taddr_of(item), ra);
       while (item < items) {
         const int nxt = item + NSUB;
         tmem_wait_ld16(ra);
         if (warp == 3 && lane == 0 && item == sub) dbg_mark(p, it, 7);
-        if (nxt < items) {
-          tmem_ld16_issue(taddr_of(nxt), rb);
-          if (BASE) load_base(nxt, bb2);
-        }
-        finish(item, ra, ba);
+        if (nxt < items) tmem_ld16_issue(taddr_of(nxt), rb);
+        if (BASE) base_get(item, qa, bv);
+        finish(item, ra, bv);
+        if (braw && item + 2 * NSUB < items) base_issue(item + 2 * NSUB, qa);
         if (nxt >= items) break;
         const int nn = nxt + NSUB;
         tmem_wait_ld16(rb);
-        if (nn < items) {
-          tmem_ld16_issue(taddr_of(nn), ra);
-          if (BASE) load_base(nn, ba);
-        }
-        finish(nxt, rb, bb2);
+        if (nn < items) tmem_ld16_issue(taddr_of(nn), ra);
+        if (BASE) base_get(nxt, qb, bv);
+        finish(nxt, rb, bv);
+        if (braw && nxt + 2 * NSUB < items) base_issue(nxt + 2 * NSUB, qb);
         item = nn;
       }
       tc_fence_before();
@@ -786,13 +808,22 @@ static int launch_variant(const TcParams &p, const TcMaps &maps, int grid, cudaS
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = p.cluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (p.cluster > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = p.cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = p.cluster > 1 ? 1 : 0;
+  cfg.numAttrs = na;
   return check_cuda(cudaLaunchKernelEx(&cfg, kern, p, maps), "conv3d_tc_kernel launch");
 }
 

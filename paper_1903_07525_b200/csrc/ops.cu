@@ -121,6 +121,7 @@ __device__ __forceinline__ void zero_tail_lanes(float (&r)[8], int ch, int c) {
 
 // ------------------------------------------------------------------ copy
 __global__ void copy_kernel(DView src, DView dst) {
+  pdl_begin();
   ChunkIdx k;
   int nch = (dst.c + 7) >> 3;
   if (chunk_index3(nch, dst.y, dst.z, k)) {
@@ -132,6 +133,7 @@ __global__ void copy_kernel(DView src, DView dst) {
 }
 
 __global__ void zero_kernel(DView dst) {
+  pdl_begin();
   ChunkIdx k;
   int nch = (dst.c + 7) >> 3;
   if (chunk_index3(nch, dst.y, dst.z, k)) {
@@ -150,6 +152,7 @@ __global__ void zero_kernel(DView dst) {
 // np.maximum NaN propagation; avg: fp32 sum in the same order, / kvol.
 __global__ void pool_kernel(DView in, DView out, int kx, int ky, int kz, int sx, int sy, int sz,
                             int mode) {
+  pdl_begin();
   ChunkIdx k;
   int nch = (out.c + 7) >> 3;
   if (chunk_index3(nch, out.y, out.z, k)) {
@@ -183,6 +186,7 @@ __global__ void pool_kernel(DView in, DView out, int kx, int ky, int kz, int sx,
 
 // ------------------------------------------------------------------ eltwise
 __global__ void eltwise_kernel(DView a, DView b, DView out, int op) {
+  pdl_begin();
   ChunkIdx k;
   int nch = (out.c + 7) >> 3;
   if (chunk_index3(nch, out.y, out.z, k)) {
@@ -200,6 +204,7 @@ __global__ void eltwise_kernel(DView a, DView b, DView out, int op) {
 // ------------------------------------------------------------------ affine + act
 __global__ void affine_act_kernel(DView in, DView out, const float *mult, const float *add, int act,
                                   float alpha) {
+  pdl_begin();
   ChunkIdx k;
   int nch = (out.c + 7) >> 3;
   if (chunk_index3(nch, out.y, out.z, k)) {
@@ -223,6 +228,7 @@ __global__ void affine_act_kernel(DView in, DView out, const float *mult, const 
 // ------------------------------------------------------------------ mergecrop
 __global__ void mergecrop_kernel(DView a, DView b, DView out, int oax, int oay, int oaz, int obx,
                                  int oby, int obz) {
+  pdl_begin();
   ChunkIdx k;
   int nch = (out.c + 7) >> 3;
   if (chunk_index3(nch, out.y, out.z, k)) {
@@ -252,6 +258,7 @@ __global__ void mergecrop_kernel(DView a, DView b, DView out, int oax, int oay, 
 
 // ------------------------------------------------------------------ pad copy
 __global__ void pad_copy_kernel(DView in, DView out, int px, int py, int pz) {
+  pdl_begin();
   ChunkIdx k;
   int nch = (out.c + 7) >> 3;
   if (chunk_index3(nch, out.y, out.z, k)) {
@@ -273,6 +280,7 @@ __global__ void pad_copy_kernel(DView in, DView out, int px, int py, int pz) {
 constexpr int DT_X = 2, DT_Y = 8, DT_Z = 8, DCO = 16;
 
 __global__ void __launch_bounds__(128) conv_direct_kernel(DirectParams p) {
+  pdl_begin();
   extern __shared__ float dsm[];
   const int taps = p.kx * p.ky * p.kz;
   float *patch = dsm;                                   // [hx][hy][hz][8]
@@ -348,6 +356,7 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(DirectParams p) {
 
 
 __global__ void subimage_kernel(SubParams p) {
+  pdl_begin();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   int nb = p.out.n;
   int total = nb * p.ex * p.ey * p.ez * 8;
@@ -396,6 +405,7 @@ __global__ void subimage_kernel(SubParams p) {
 
 
 __global__ void deconv_gather_kernel(GatherDeconvParams p) {
+  pdl_begin();
   ChunkIdx k;
   int nch = (p.out.c + 7) >> 3;
   if (chunk_index3(nch, p.out.y, p.out.z, k)) {
@@ -457,6 +467,7 @@ static dim3 grid3(const DView &v, int threads) {
 // thread converts 4 consecutive z of one 8-fmap chunk: 8 float4 loads (one
 // per fmap plane, 512 B per warp instruction) and 4 16-byte stores.
 __global__ void pack_std_f32_kernel(DView src, DView dst) {
+  pdl_begin();
   const int zq = dst.z >> 2;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= dst.y * zq) return;
@@ -490,6 +501,7 @@ __global__ void pack_std_f32_kernel(DView src, DView dst) {
 
 // The reverse at the output boundary: bf16 blocked -> fp32 NCDHW.
 __global__ void unpack_std_f32_kernel(DView src, DView dst) {
+  pdl_begin();
   const int zq = src.z >> 2;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= src.y * zq) return;
@@ -530,46 +542,46 @@ static bool blocked_bf16(const DView &t) { return t.blocked && t.dtype == VXB_BF
 int launch_copy(const DView &src, const DView &dst, cudaStream_t s) {
   if (std_f32_vec4(src) && blocked_bf16(dst)) {
     dim3 g((dst.y * (dst.z >> 2) + 127) / 128, dst.x, dst.n * ((dst.c + 7) / 8));
-    pack_std_f32_kernel<<<g, 128, 0, s>>>(src, dst);
-    return check_cuda(cudaGetLastError(), "pack_std_f32_kernel");
+    return check_cuda(launch_pdl(pack_std_f32_kernel, g, dim3(128), 0, s, src, dst),
+                      "pack_std_f32_kernel");
   }
   if (blocked_bf16(src) && std_f32_vec4(dst)) {
     dim3 g((src.y * (src.z >> 2) + 127) / 128, src.x, src.n * ((src.c + 7) / 8));
-    unpack_std_f32_kernel<<<g, 128, 0, s>>>(src, dst);
-    return check_cuda(cudaGetLastError(), "unpack_std_f32_kernel");
+    return check_cuda(launch_pdl(unpack_std_f32_kernel, g, dim3(128), 0, s, src, dst),
+                      "unpack_std_f32_kernel");
   }
-  copy_kernel<<<grid3(dst, 256), 256, 0, s>>>(src, dst);
-  return check_cuda(cudaGetLastError(), "copy_kernel");
+  return check_cuda(launch_pdl(copy_kernel, grid3(dst, 256), dim3(256), 0, s, src, dst),
+                    "copy_kernel");
 }
 int launch_zero(const DView &dst, cudaStream_t s) {
-  zero_kernel<<<grid3(dst, 256), 256, 0, s>>>(dst);
-  return check_cuda(cudaGetLastError(), "zero_kernel");
+  return check_cuda(launch_pdl(zero_kernel, grid3(dst, 256), dim3(256), 0, s, dst), "zero_kernel");
 }
 int launch_pool(const DView &in, const DView &out, const int *w, const int *st, int mode,
                 cudaStream_t s) {
-  pool_kernel<<<grid3(out, 256), 256, 0, s>>>(in, out, w[0], w[1], w[2], st[0],
-                                                              st[1], st[2], mode);
-  return check_cuda(cudaGetLastError(), "pool_kernel");
+  return check_cuda(launch_pdl(pool_kernel, grid3(out, 256), dim3(256), 0, s, in, out, w[0], w[1],
+                               w[2], st[0], st[1], st[2], mode),
+                    "pool_kernel");
 }
 int launch_eltwise(const DView &a, const DView &b, const DView &out, int op, cudaStream_t s) {
-  eltwise_kernel<<<grid3(out, 256), 256, 0, s>>>(a, b, out, op);
-  return check_cuda(cudaGetLastError(), "eltwise_kernel");
+  return check_cuda(launch_pdl(eltwise_kernel, grid3(out, 256), dim3(256), 0, s, a, b, out, op),
+                    "eltwise_kernel");
 }
 int launch_affine_act(const DView &in, const DView &out, const float *m, const float *a, int act,
                       float alpha, cudaStream_t s) {
-  affine_act_kernel<<<grid3(out, 256), 256, 0, s>>>(in, out, m, a, act, alpha);
-  return check_cuda(cudaGetLastError(), "affine_act_kernel");
+  return check_cuda(launch_pdl(affine_act_kernel, grid3(out, 256), dim3(256), 0, s, in, out, m, a,
+                               act, alpha),
+                    "affine_act_kernel");
 }
 int launch_mergecrop(const DView &a, const DView &b, const DView &out, const int *oa,
                      const int *ob, cudaStream_t s) {
-  mergecrop_kernel<<<grid3(out, 256), 256, 0, s>>>(a, b, out, oa[0], oa[1], oa[2],
-                                                                   ob[0], ob[1], ob[2]);
-  return check_cuda(cudaGetLastError(), "mergecrop_kernel");
+  return check_cuda(launch_pdl(mergecrop_kernel, grid3(out, 256), dim3(256), 0, s, a, b, out,
+                               oa[0], oa[1], oa[2], ob[0], ob[1], ob[2]),
+                    "mergecrop_kernel");
 }
 int launch_pad_copy(const DView &in, const DView &out, const int *pads, cudaStream_t s) {
-  pad_copy_kernel<<<grid3(out, 256), 256, 0, s>>>(in, out, pads[0], pads[1],
-                                                                  pads[2]);
-  return check_cuda(cudaGetLastError(), "pad_copy_kernel");
+  return check_cuda(launch_pdl(pad_copy_kernel, grid3(out, 256), dim3(256), 0, s, in, out,
+                               pads[0], pads[1], pads[2]),
+                    "pad_copy_kernel");
 }
 
 int launch_conv_direct(DirectParams p, cudaStream_t s) {
@@ -592,19 +604,19 @@ int launch_conv_direct(DirectParams p, cudaStream_t s) {
     configured = true;
   }
   dim3 grid(p.tiles_x * p.tiles_y * p.tiles_z, (p.cout + DCO - 1) / DCO, p.out.n);
-  conv_direct_kernel<<<grid, 128, smem, s>>>(p);
-  return check_cuda(cudaGetLastError(), "conv_direct_kernel");
+  return check_cuda(launch_pdl(conv_direct_kernel, grid, dim3(128), smem, s, p),
+                    "conv_direct_kernel");
 }
 
 int launch_subimage(const SubParams &p, cudaStream_t s) {
   int total = p.out.n * p.ex * p.ey * p.ez * 8;
-  subimage_kernel<<<(total + 127) / 128, 128, 0, s>>>(p);
-  return check_cuda(cudaGetLastError(), "subimage_kernel");
+  return check_cuda(launch_pdl(subimage_kernel, dim3((total + 127) / 128), dim3(128), 0, s, p),
+                    "subimage_kernel");
 }
 
 int launch_deconv_gather(const GatherDeconvParams &p, cudaStream_t s) {
-  deconv_gather_kernel<<<grid3(p.out, 128), 128, 0, s>>>(p);
-  return check_cuda(cudaGetLastError(), "deconv_gather_kernel");
+  return check_cuda(launch_pdl(deconv_gather_kernel, grid3(p.out, 128), dim3(128), 0, s, p),
+                    "deconv_gather_kernel");
 }
 
 }  // namespace vxb

@@ -38,6 +38,8 @@ static int env_int(const char *name, int dflt) {
   return (v && *v) ? atoi(v) : dflt;
 }
 
+bool pdl_enabled() { return env_int("VXB_PDL", 1) != 0; }
+
 static DView to_dview(const vxb_tensor &t) {
   DView v;
   v.data = t.data;
@@ -214,14 +216,31 @@ struct TcConfig {
   size_t smem;
 };
 
-static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, int reps,
-                        TcConfig &c) {
+// other_tiles: tiles over the non-slice axes x batch x N tiles x reps.
+static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, long long other_tiles,
+                        int sms, int reps, TcConfig &c) {
   const int budget = 227 * 1024 - 6144;  // room for bias/scale/tap tables/barriers
   c.acc = env_int("VXB_TC_ACC", 2);
   if (c.acc != 1 && c.acc != 2) c.acc = 2;
   int bx_cap = env_int("VXB_TC_BX", 8);
+  // Slices per tile: minimise (waves of persistent CTAs) x (MMAs per tile
+  // per K step) -- bx + 2 folded, bx unfolded.  Large layers thus take the
+  // slice count with the least padding along the axis (6 for the 18-deep
+  // axis of config 5, 8 for 32 or 128); layers with fewer tiles than SMs
+  // shrink their tiles until every SM has work.  Ties go to the larger tile.
   c.bx = 1;
-  while (c.bx * 2 <= bx_cap && c.bx * 2 * L.nt * c.acc <= 512 && c.bx < slice_extent) c.bx *= 2;
+  long long best = -1;
+  for (int cand : {8, 6, 4, 3, 2, 1}) {
+    if (cand > bx_cap || cand * L.nt * c.acc > 512) continue;
+    if (!L.fold && (cand & (cand - 1))) continue;   // unfolded tiles: 1, 2, 4, 8
+    const long long tiles = static_cast<long long>(ceil_div(slice_extent, cand)) * other_tiles;
+    const long long waves = (tiles + sms - 1) / sms;
+    const long long cost = waves * (L.fold ? cand + 2 : cand);
+    if (best < 0 || cost < best) {
+      best = cost;
+      c.bx = cand;
+    }
+  }
   if (c.bx * L.nt * c.acc > 512) return set_error(VXB_EUNSUPPORTED, "TMEM overflow");
   bool any_pair = false;
   int max_steps = 1;
@@ -367,7 +386,11 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   TcLayout L = tc_layout(a.cin0, a.cin1, a.cout, a.k);
   TcConfig c;
   const int slice_y = L.fold == 2;
-  int rc = tc_configure(L, a.k, slice_y ? a.oy : a.ox, a.reps, c);
+  int sms = device_sms();
+  if (sms <= 0) return set_error(VXB_ECUDA, "no CUDA device");
+  const long long other_tiles = static_cast<long long>(ceil_div(slice_y ? a.ox : a.oy, TILE_Y)) *
+                                ceil_div(a.oz, TILE_Z) * a.nb * L.n_tiles * a.reps;
+  int rc = tc_configure(L, a.k, slice_y ? a.oy : a.ox, other_tiles, sms, a.reps, c);
   if (rc) return rc;
   TcParams p;
   memset(&p, 0, sizeof(p));
@@ -472,8 +495,6 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   p.cout = a.cout;
   p.act = a.act;
   p.alpha = a.alpha;
-  int sms = device_sms();
-  if (sms <= 0) return set_error(VXB_ECUDA, "no CUDA device");
   p.dbg_mode = env_int("VXB_TC_DBGMODE", 0);
   if (env_int("VXB_TC_DEBUG", 0)) {
     if (!g_dbg) {

@@ -130,4 +130,39 @@ constexpr int DCO_DIRECT = 16;  // output fmaps per direct-conv CTA
 int set_error(int code, const char *fmt, ...);
 int check_cuda(cudaError_t e, const char *what);
 
+// ---- programmatic dependent launch (PDL)
+// Every vxb kernel is launched with programmatic stream serialization: it
+// may start while its predecessor drains, signals its own dependents at
+// entry, and waits for the predecessor's completion (griddepcontrol.wait)
+// before touching activations.  The conv kernel does its setup (barriers,
+// TMEM, bias/scale staging) before the wait, overlapping the previous
+// kernel's tail.  VXB_PDL=0 launches plainly (the wait is then a no-op).
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_begin() {
+  pdl_trigger();
+  pdl_wait();
+}
+#endif
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t stream, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<Args &&>(args)...);
+}
+
 }  // namespace vxb

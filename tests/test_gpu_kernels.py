@@ -102,6 +102,23 @@ def test_tap_fold_matches_unfolded(k, pad, monkeypatch):
     assert mx < 1e-5, mx
 
 
+@pytest.mark.parametrize("bx", ["3", "6", "8"])
+@pytest.mark.parametrize("k,pad", [((3, 3, 3), (1, 1, 1)), ((1, 3, 3), (0, 1, 1))])
+def test_fold_tile_widths(bx, k, pad, monkeypatch):
+    """Folded tiles of 3/6/8 slices (config 5's 18-deep axis picks 6)."""
+    monkeypatch.setenv("VXB_TC_BX", bx)
+    rng = np.random.default_rng(int(bx))
+    x = rng.uniform(-1, 1, (1, 28, 18, 20, 12)).astype(np.float32)
+    w = (rng.standard_normal((28, 28) + k) * 0.1).astype(np.float32)
+    b = rng.standard_normal(28).astype(np.float32)
+    base = rng.uniform(-1, 1, (1, 28, 18, 20, 12)).astype(np.float32)
+    scale = rng.uniform(0.5, 1.5, 28).astype(np.float32)
+    got, _ = _conv_bf16(x, w, b, pad, "elu", base, scale)
+    want = _ref_bf16(x, w, b, pad, "elu", base, scale)
+    mx, l2 = R.normalized_error(got, want)
+    assert mx < BF16_TOL and l2 < 3e-3, (mx, l2)
+
+
 def test_tc_conv_fp32_output_and_batch2():
     rng = np.random.default_rng(7)
     x = rng.uniform(-1, 1, (2, 16, 4, 18, 10)).astype(np.float32)
