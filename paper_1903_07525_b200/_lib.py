@@ -21,6 +21,7 @@ VXB_F32 = 1
 ACT_CODE = {None: 0, "relu": 1, "elu": 2, "sigmoid": 3}   # kernels_cy.py:19
 PATH_TC = 1
 PATH_DIRECT = 2
+PATH_TC_UNFOLDED = 3
 POOL_CODE = {"max": 0, "avg": 1}
 ELT_CODE = {"add": 0, "mul": 1, "div": 2}
 
@@ -86,6 +87,7 @@ SIGNATURES = [
     ("vxb_device_sms", c_int, []),
     ("vxb_debug_read", c_size_t, [c_void_p, c_size_t]),
     ("vxb_conv_select", c_int, [c_int, c_int, I3, I3]),
+    ("vxb_conv_select_shape", c_int, [c_int, c_int, I3, I3, I3]),
     ("vxb_conv_weights_bytes", c_size_t, [c_int, c_int, I3, I3, c_int]),
     ("vxb_conv_pack_weights", c_int, [c_void_p, c_int, c_int, I3, I3, c_int, c_void_p, c_size_t]),
     ("vxb_conv_weights_bytes2", c_size_t, [c_int, c_int, c_int, I3, I3, c_int]),

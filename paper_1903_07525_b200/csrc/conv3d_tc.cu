@@ -306,8 +306,17 @@ __device__ __forceinline__ void mma_group_fold(
         }
         first = 0;
       } else {
+        // interior input slices first: they share B (all 3 blocks) and the
+        // instruction descriptor, so consecutive MMAs only move A and D
 #pragma unroll
-        for (int j = 0; j < BX + 2; ++j) {
+        for (int j = 2; j < BX; ++j)
+          umma_bf16_lohi_elect(d_base + (j - 2) * nt, a_lo + j * slice_inc, a_hi, b_lo, b_hi, id3,
+                               1u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = e < 2 ? e : BX + e - 2;
+          if (j >= 2 && j < BX) continue;   // BX < 2: the edges are everything
+          if (e >= 2 && j < 2) continue;
           const int dlo = j - BX + 1 > 0 ? j - BX + 1 : 0, dhi = j < 2 ? j : 2;
           const uint32_t idn = dhi - dlo == 0 ? id1 : (dhi - dlo == 1 ? id2 : id3);
           umma_bf16_lohi_elect(d_base + (j - dhi) * nt, a_lo + j * slice_inc, a_hi,
@@ -518,8 +527,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t b_inc = (p.slab_bytes / (PAIR ? 2 : 1)) >> 4;
       const uint32_t a_hi = desc_hi(p.a_sbo);
       const uint32_t blk_inc = (p.nt * SLAB_ROW_BYTES) >> 4;
-      const uint32_t id1 = idesc_bf16(128, p.nt), id2 = idesc_bf16(128, 2 * p.nt),
-                     id3 = idesc_bf16(128, p.fold ? 3 * p.nt : p.nt);
+      // (debug mode 16: every folded MMA at N = nt, to time the issue loop)
+      const uint32_t id1 = idesc_bf16(128, p.nt),
+                     id2 = (p.dbg_mode & 16) ? id1 : idesc_bf16(128, 2 * p.nt),
+                     id3 = (p.dbg_mode & 16) ? id1 : idesc_bf16(128, p.fold ? 3 * p.nt : p.nt);
       // folded walk: z taps inside, the other non-slice axis outside
       const uint32_t fold_stride = (p.slice_y ? p.hy * p.hz : p.hz);
       const uint32_t b_hi = desc_hi(256u);

@@ -109,12 +109,14 @@ static int tc_fold_axis(int nt, const int k[3]) {
   return 0;
 }
 
-static TcLayout tc_layout(int cin0, int cin1, int cout, const int k[3]) {
+static bool is_tc(int path) { return path == VXB_PATH_TC || path == VXB_PATH_TC_UNFOLDED; }
+
+static TcLayout tc_layout(int cin0, int cin1, int cout, const int k[3], bool allow_fold = true) {
   TcLayout L;
   L.npad = round_up(cout, 16);
   L.n_tiles = ceil_div(L.npad, 256);
   L.nt = round_up(ceil_div(L.npad, L.n_tiles), 16);
-  L.fold = L.n_tiles == 1 ? tc_fold_axis(L.nt, k) : 0;
+  L.fold = (allow_fold && L.n_tiles == 1) ? tc_fold_axis(L.nt, k) : 0;
   L.slab = (L.fold ? 3 : 1) * L.nt * SLAB_ROW_BYTES;
   L.seg_chunks[0] = ceil_div(cin0, 8);
   L.seg_chunks[1] = cin1 > 0 ? ceil_div(cin1, 8) : 0;
@@ -217,17 +219,21 @@ struct TcConfig {
 };
 
 // other_tiles: tiles over the non-slice axes x batch x N tiles x reps.
+static const int kTileOverhead = 3;
+
 static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, long long other_tiles,
                         int sms, int reps, TcConfig &c) {
   const int budget = 227 * 1024 - 6144;  // room for bias/scale/tap tables/barriers
   c.acc = env_int("VXB_TC_ACC", 2);
   if (c.acc != 1 && c.acc != 2) c.acc = 2;
   int bx_cap = env_int("VXB_TC_BX", 8);
-  // Slices per tile: minimise (waves of persistent CTAs) x (MMAs per tile
-  // per K step) -- bx + 2 folded, bx unfolded.  Large layers thus take the
-  // slice count with the least padding along the axis (6 for the 18-deep
-  // axis of config 5, 8 for 32 or 128); layers with fewer tiles than SMs
-  // shrink their tiles until every SM has work.  Ties go to the larger tile.
+  // Slices per tile: minimise (waves of persistent CTAs) x (per-tile cost):
+  // MMAs per K step (bx + 2 folded, bx unfolded) plus a fixed per-tile
+  // overhead (decode, barrier round trips, epilogue drain) worth ~3 slices.
+  // Large layers thus take the slice count with the least padding along the
+  // axis (6 for the 18-deep axis of config 5, 8 for 32 or 128); layers with
+  // fewer tiles than SMs shrink their tiles until every SM has work.  Ties go
+  // to the larger tile.
   c.bx = 1;
   long long best = -1;
   for (int cand : {8, 6, 4, 3, 2, 1}) {
@@ -235,7 +241,7 @@ static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, lon
     if (!L.fold && (cand & (cand - 1))) continue;   // unfolded tiles: 1, 2, 4, 8
     const long long tiles = static_cast<long long>(ceil_div(slice_extent, cand)) * other_tiles;
     const long long waves = (tiles + sms - 1) / sms;
-    const long long cost = waves * (L.fold ? cand + 2 : cand);
+    const long long cost = waves * ((L.fold ? cand + 2 : cand) + kTileOverhead);
     if (best < 0 || cost < best) {
       best = cost;
       c.bx = cand;
@@ -380,10 +386,11 @@ struct TcLaunch {
   const float *bias, *scale;
   int act;
   float alpha;
+  bool allow_fold;
 };
 
 static int run_tc(const TcLaunch &a, cudaStream_t stream) {
-  TcLayout L = tc_layout(a.cin0, a.cin1, a.cout, a.k);
+  TcLayout L = tc_layout(a.cin0, a.cin1, a.cout, a.k, a.allow_fold);
   TcConfig c;
   const int slice_y = L.fold == 2;
   int sms = device_sms();
@@ -540,6 +547,16 @@ int vxb_conv_select(int cin, int cout, const int k[3], const int stride[3]) {
   return VXB_PATH_DIRECT;
 }
 
+int vxb_conv_select_shape(int cin, int cout, const int k[3], const int stride[3],
+                          const int out_xyz[3]) {
+  int path = vxb_conv_select(cin, cout, k, stride);
+  if (path != VXB_PATH_TC || !out_xyz) return path;
+  const TcLayout L = tc_layout(cin, 0, cout, k);
+  if (L.fold == 2 && out_xyz[0] > 0 && ceil_div(out_xyz[0], TILE_Y) * TILE_Y * 4 > out_xyz[0] * 5)
+    return VXB_PATH_TC_UNFOLDED;   // > 25% of the 16-row x tiles would be padding
+  return path;
+}
+
 static size_t direct_bytes(int cin, int cout, const int k[3]) {
   return static_cast<size_t>(ceil_div(cout, DCO_DIRECT)) * ceil_div(cin, 8) * k[0] * k[1] * k[2] *
          8 * DCO_DIRECT * sizeof(float);
@@ -548,7 +565,7 @@ static size_t direct_bytes(int cin, int cout, const int k[3]) {
 size_t vxb_conv_weights_bytes2(int cin0, int cin1, int cout, const int k[3], const int stride[3],
                                int path) {
   if (path == 0) path = vxb_conv_select(cin0 + cin1, cout, k, stride);
-  if (path == VXB_PATH_TC) return tc_bytes_per_rep(tc_layout(cin0, cin1, cout, k));
+  if (is_tc(path)) return tc_bytes_per_rep(tc_layout(cin0, cin1, cout, k, path == VXB_PATH_TC));
   return direct_bytes(cin0 + cin1, cout, k);
 }
 
@@ -566,8 +583,8 @@ int vxb_conv_pack_weights2(const float *w, int cin0, int cin1, int cout, const i
   auto wtap = [&](int co, int ci, int dx, int dy, int dz) {
     return w[((((static_cast<size_t>(co) * cin) + ci) * k[0] + dx) * k[1] + dy) * k[2] + dz];
   };
-  if (path == VXB_PATH_TC) {
-    TcLayout L = tc_layout(cin0, cin1, cout, k);
+  if (is_tc(path)) {
+    TcLayout L = tc_layout(cin0, cin1, cout, k, path == VXB_PATH_TC);
     tc_pack(L, cin0, cin1, cout, k, wtap, static_cast<uint8_t *>(dst));
     return VXB_OK;
   }
@@ -614,11 +631,12 @@ int vxb_conv3d(const vxb_conv_desc *d, void *stream) {
   if (d->act < 0 || d->act > 3) return set_error(VXB_EINVAL, "conv3d: bad act %d", d->act);
   const int path = d->path ? d->path : vxb_conv_select(d->cin, d->cout, d->k, d->stride);
   cudaStream_t s = as_stream(stream);
-  if (path == VXB_PATH_TC) {
+  if (is_tc(path)) {
     if (d->stride[0] != 1 || d->stride[1] != 1 || d->stride[2] != 1)
       return set_error(VXB_EUNSUPPORTED, "tensor-core conv requires stride 1");
     TcLaunch a;
     memset(&a, 0, sizeof(a));
+    a.allow_fold = path == VXB_PATH_TC;
     a.in[0] = &d->in0;
     a.in[1] = two ? &d->in1 : nullptr;
     for (int i = 0; i < 3; ++i) {

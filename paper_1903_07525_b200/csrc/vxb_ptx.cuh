@@ -40,9 +40,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
-// Wait with a suspend-time hint: the warp sleeps in hardware until the phase
-// completes (or ~hint ns pass) instead of spinning, so idle waiters do not
-// steal issue slots from the single-thread MMA issuer on the same SMSP.
 __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -54,8 +51,17 @@ __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: the thread is parked until the phase
+// completes (woken by the barrier, not by a timer), so idle waiters neither
+// spin nor oversleep past the phase flip.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
-  while (!mbar_test(bar, parity)) __nanosleep(256);
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(10000000u)
+      : "memory");
 }
 
 // ---------------------------------------------------------------- TMA

@@ -54,8 +54,10 @@ class PackedConv:
 
 
 def pack_conv(kernel, bias, *, stride=(1, 1, 1), base_scale=None, cin_split=None,
-              path=0, device=None) -> PackedConv:
-    """Pack a standard (cout, cin, kx, ky, kz) fp32 kernel bank for vxb_conv3d."""
+              path=0, out_shape=None, device=None) -> PackedConv:
+    """Pack a standard (cout, cin, kx, ky, kz) fp32 kernel bank for vxb_conv3d.
+    ``out_shape`` (x, y, z) of the output, when known, lets the library pick
+    the tile layout (vxb_conv_select_shape)."""
     import torch
     L = _lib.lib()
     w = np.ascontiguousarray(np.asarray(kernel, dtype=np.float32))
@@ -67,8 +69,12 @@ def pack_conv(kernel, bias, *, stride=(1, 1, 1), base_scale=None, cin_split=None
     cin1 = cin - cin0
     stride = tuple(int(s) for s in stride)
     if path == 0:
-        path = L.vxb_conv_select(cin, cout, _lib.i3(k), _lib.i3(stride))
-    if cin1 and path != _lib.PATH_TC:
+        if out_shape is not None:
+            path = L.vxb_conv_select_shape(cin, cout, _lib.i3(k), _lib.i3(stride),
+                                           _lib.i3(tuple(out_shape)))
+        else:
+            path = L.vxb_conv_select(cin, cout, _lib.i3(k), _lib.i3(stride))
+    if cin1 and path not in (_lib.PATH_TC, _lib.PATH_TC_UNFOLDED):
         raise ExecutionError("a two-input (fused concat) conv needs the tensor-core path")
     nbytes = L.vxb_conv_weights_bytes2(cin0, cin1, cout, _lib.i3(k), _lib.i3(stride), path)
     host = np.zeros(nbytes, dtype=np.uint8)

@@ -292,7 +292,8 @@ class PlanRunner:
                                                             x2=b, off=oa, off2=ob))
                 else:
                     pk = K.pack_conv(kern, w.tensor(st.name, ROLE_BIAS), stride=stride,
-                                     base_scale=scale, path=self._conv_path, device=dev)
+                                     base_scale=scale, path=self._conv_path,
+                                     out_shape=tuple(info["out"].dims[2:]), device=dev)
                     calls.append(lambda x=info["x"].dt, pk=pk, out=out, base=base,
                                  pad=info["pad"], act=st.fused_act:
                                  K.conv3d(x, pk, out, pad=pad, base=base, fused_act=act))

@@ -119,6 +119,27 @@ def test_fold_tile_widths(bx, k, pad, monkeypatch):
     assert mx < BF16_TOL and l2 < 3e-3, (mx, l2)
 
 
+def test_unfolded_path_for_badly_padded_rows():
+    """x = 18 makes y-sliced folding pad 14 of 32 rows: select_shape picks the
+    unfolded layout, which must match the oracle (and the folded result)."""
+    import torch
+    D, K = _dev()
+    rng = np.random.default_rng(21)
+    x = rng.uniform(-1, 1, (1, 28, 18, 24, 16)).astype(np.float32)
+    w = (rng.standard_normal((28, 28, 1, 3, 3)) * 0.1).astype(np.float32)
+    b = rng.standard_normal(28).astype(np.float32)
+    want = _ref_bf16(x, w, b, (0, 1, 1), "elu")
+    xd = D.to_device_blocked(x)
+    for out_shape, path in [((18, 24, 16), 3), (None, 1)]:
+        out = D.empty_blocked(1, 28, (18, 24, 16))
+        pk = K.pack_conv(w, b, out_shape=out_shape)
+        assert pk.path == path
+        K.conv3d(xd, pk, out, pad=(0, 1, 1), fused_act=("elu", 1.0))
+        torch.cuda.synchronize()
+        mx, l2 = R.normalized_error(D.to_host_standard(out), want)
+        assert mx < BF16_TOL and l2 < 3e-3, (path, mx, l2)
+
+
 def test_tc_conv_fp32_output_and_batch2():
     rng = np.random.default_rng(7)
     x = rng.uniform(-1, 1, (2, 16, 4, 18, 10)).astype(np.float32)

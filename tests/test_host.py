@@ -80,6 +80,23 @@ def test_host_packing_sizes_and_selection():
         step = (dx * 3 + dy) * 3 + dz
         byte = step * 128 * 32 + (co // 8) * 256 + h * 128 + (co % 8) * 16 + 2 * l
         assert at(bf2, byte) == bf16_round(w2[co, ci, dx, dy, dz])
+    # 1x3x3 folds along y with 16-row x tiles; x = 18 would pad 14 of 32 rows
+    k133 = _lib.i3((1, 3, 3))
+    assert L.vxb_conv_select_shape(28, 28, k133, s1, _lib.i3((18, 192, 192))) == _lib.PATH_TC_UNFOLDED
+    assert L.vxb_conv_select_shape(28, 28, k133, s1, _lib.i3((32, 128, 128))) == _lib.PATH_TC
+    assert L.vxb_conv_select_shape(28, 28, k3, s1, _lib.i3((18, 192, 192))) == _lib.PATH_TC
+    assert L.vxb_conv_select_shape(28, 28, k3, _lib.i3((2, 2, 2)), _lib.i3((9, 9, 9))) == \
+        _lib.PATH_DIRECT
+    # unfolded C16 image: same size, plain tap order
+    du = np.zeros(n, np.uint8)
+    assert L.vxb_conv_pack_weights(w.ctypes.data, 16, 16, k3, s1, _lib.PATH_TC_UNFOLDED,
+                                   du.ctypes.data, n) == 0
+    bu = du.view(np.uint16)
+    for (co, ci, dx, dy, dz) in [(0, 0, 0, 0, 0), (9, 12, 2, 1, 0), (15, 15, 1, 2, 2)]:
+        h, l = ci // 8, ci % 8
+        step = (dx * 3 + dy) * 3 + dz
+        byte = step * 16 * 32 + (co // 8) * 256 + h * 128 + (co % 8) * 16 + 2 * l
+        assert at(bu, byte) == bf16_round(w[co, ci, dx, dy, dz])
     assert L.vxb_conv_pack_weights(w.ctypes.data, 16, 16, k3, s1, 0, dst.ctypes.data, 10) != 0
     assert b"need" in L.vxb_last_error()
 
