@@ -299,7 +299,11 @@ def kernel_roofline(L, dev, peaks):
     flops = L["flops"]
     n, c, x, y, z = L["plan"].inputs[0][2]
     cout = L["plan"].steps[-1].output.dims[1]
-    alg_bytes = (c + cout) * x * y * z * 2   # bf16 in + out, weights negligible
+    # bf16 blocked input (packed by the preceding kernel); the output is the
+    # network's fp32 NCDHW tensor when the runner fused the unpack into the
+    # conv epilogue, else bf16 blocked; weights negligible
+    out_b = 4 if runner._fused_outputs else 2
+    alg_bytes = (c * 2 + cout * out_b) * x * y * z
     ai = flops / alg_bytes
     ridge = peaks["bf16"] * 1e12 / (peaks["hbm"] * 1e9)
     if ai >= ridge:
