@@ -170,16 +170,21 @@ __device__ __forceinline__ void dbg_mark(const TcParams &p, int it, int slot) {
 
 constexpr int EPI_WARPS = 12;
 constexpr int TC_THREADS = 96 + 32 * EPI_WARPS;   // A-TMA, MMA, B-TMA + epilogue
+constexpr int CVT_WARPS = 2;                      // fp32-input converters (F32IN)
+__host__ __device__ constexpr int tc_threads(bool f32in) {
+  return TC_THREADS + (f32in ? 32 * CVT_WARPS : 0);
+}
 
 // Byte offsets inside the dynamic smem block (all derivable from p).
 struct SmemMap {
-  uint32_t a, b, bias, scale, bars;
+  uint32_t a, b, stg, bias, scale, bars;
 };
 __host__ __device__ inline SmemMap smem_map(const TcParams &p) {
   SmemMap m;
   m.a = 0;
   m.b = p.na * p.a_stage_bytes;
-  m.bias = m.b + p.nb_stages * p.b_stage_bytes;
+  m.stg = m.b + p.nb_stages * p.b_stage_bytes;
+  m.bias = m.stg + p.n_stg * p.stg_bytes;
   const uint32_t cpad = p.n_tiles * p.nt;
   m.scale = m.bias + cpad * 4;
   m.bars = (m.scale + cpad * 4 + 15) & ~15u;
@@ -338,8 +343,8 @@ __device__ __forceinline__ void mma_group_fold(
   }
 }
 
-template <int ACT, bool FASTOUT, bool BASE, bool PAIR>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN>
+__global__ void __launch_bounds__(tc_threads(F32IN), 1)
     conv3d_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
@@ -359,7 +364,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t *b_empty = b_full + p.nb_stages;
   uint64_t *t_full = b_empty + p.nb_stages;
   uint64_t *t_empty = t_full + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(t_empty + 2);
+  uint64_t *stg_full = t_empty + 2;                 // F32IN staging ring
+  uint64_t *stg_empty = stg_full + p.n_stg;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(stg_empty + p.n_stg);
+  uint8_t *stg_buf = smem + sm.stg;
 
   // CTA pairs (cluster 2) walk pairs of tiles in lockstep so they can share
   // one B (weight) stream through TMA multicast
@@ -390,8 +398,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     prefetch_tmap(&maps.m[0]);
     if (p.seg_chunks[1] > 0) prefetch_tmap(&maps.m[1]);
     for (int i = 0; i < p.na; ++i) {
-      mbar_init(&a_full[i], 1);
+      // F32IN: the stage is full once every converter warp (of both CTAs of a
+      // pair) has written its rows; otherwise the TMA bytes complete it
+      mbar_init(&a_full[i], F32IN ? CVT_WARPS * (PAIR ? 2 : 1) : 1);
       mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < p.n_stg; ++i) {
+      mbar_init(&stg_full[i], 1);
+      mbar_init(&stg_empty[i], CVT_WARPS);
     }
     for (int i = 0; i < p.nb_stages; ++i) {
       mbar_init(&b_full[i], 1);
@@ -422,7 +436,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0) {
     // ===================== A producer: halo tiles (TMA 4-D boxes) ==========
     if (lane == 0) {
-      int a_st = 0, a_ph = 0;
+      int a_st = 0, a_ph = 0, s_st = 0, s_ph = 0;
       int pit = 0;
       for (int tile = first_tile; tile < p.total_tiles; tile += tile_step, ++pit) {
         TileCoord tc = decode_tile(p, tile);
@@ -433,6 +447,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           // pair mode: the leader's barrier counts both CTAs' bytes
           if (p.dbg_mode & 2) {
             if (!PAIR || crank == 0) mbar_arrive(&a_full[a_st]);
+            if (++a_st == p.na) {
+              a_st = 0;
+              a_ph ^= 1;
+            }
+            continue;
+          }
+          if (F32IN) {
+            // fp32 NCDHW input: one (hzb, hy, 1, 8) box per chunk and halo
+            // x-slice into the staging ring; the converter warps fill the stage
+            const int *off = p.seg_off[0];
+            const int cx = tc.x0 - p.pad[0] + off[0];
+            const int cy = tc.y0 - p.pad[1] + off[1];
+            const int cz = tc.z0 - p.pad[2] + off[2] - p.f32in_zshift;   // 16-byte aligned
+            for (int ci = 0; ci < gi.nch; ++ci)
+              for (int xs = 0; xs < p.hx; xs += p.f32in_xb) {
+                mbar_wait_sleep(&stg_empty[s_st], s_ph ^ 1);
+                if (p.dbg_mode & 128) {
+                  mbar_arrive(&stg_full[s_st]);
+                } else {
+                  mbar_expect_tx(&stg_full[s_st], p.stg_bytes);
+                  // (batch folded into the channel coordinate: c + b * C)
+                  tma_load_4d(stg_buf + s_st * p.stg_bytes, &maps.m[0], &stg_full[s_st], cz, cy,
+                              cx + xs, (gi.chunk0 + ci) * LANES + tc.b * p.f32in_cstride);
+                }
+                if (++s_st == p.n_stg) {
+                  s_st = 0;
+                  s_ph ^= 1;
+                }
+              }
             if (++a_st == p.na) {
               a_st = 0;
               a_ph ^= 1;
@@ -607,6 +650,64 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
     __syncwarp();
+  } else if (F32IN && warp >= 3 + EPI_WARPS) {
+    // ===================== fp32 -> bf16 chunk converters (F32IN) ============
+    // Staging slot = (8 c, xb, hy, hzb) fp32 of xb halo x-slices; every row
+    // (x, y, z < hz) becomes one 16-byte bf16x8 row of the A stage's chunk array.
+    const int ct = threadIdx.x - 32 * (3 + EPI_WARPS);   // 0 .. 32*CVT_WARPS-1
+    constexpr int NT = 32 * CVT_WARPS;
+    const int rows = p.hy * p.hz;
+    const int ddy = NT / p.hz, ddz = NT % p.hz;
+    const int cstride = p.f32in_xb * p.hy * p.hzb;       // fp32 elements per channel plane
+    int a_st = 0, s_st = 0, s_ph = 0;
+    for (int tile = first_tile; tile < p.total_tiles; tile += tile_step) {
+      for (int g = 0; g < p.n_groups; ++g) {
+        GroupInfo gi = group_info(p, g);
+        uint8_t *abase = a_buf + a_st * p.a_stage_bytes;
+        for (int ci = 0; ci < gi.nch; ++ci)
+          for (int xs0 = 0; xs0 < p.hx; xs0 += p.f32in_xb) {
+            mbar_wait(&stg_full[s_st], s_ph);
+            const float *src0 = reinterpret_cast<const float *>(stg_buf + s_st * p.stg_bytes);
+            const int nxs = min(p.f32in_xb, p.hx - xs0);
+            for (int xi = 0; xi < nxs; ++xi) {
+            const float *src = src0 + xi * p.hy * p.hzb;
+            uint4 *dst = reinterpret_cast<uint4 *>(abase + ci * p.chunk_stride) + (xs0 + xi) * rows;
+            int y = ct / p.hz, z = ct % p.hz;
+            for (int r = (p.dbg_mode & 64) ? rows : ct; r < rows; r += NT) {
+              const float *q = src + y * p.hzb + z + p.f32in_zshift;
+              uint4 u;
+              __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&u);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                h[i] = __floats2bfloat162_rn(q[(2 * i) * cstride], q[(2 * i + 1) * cstride]);
+              dst[r] = u;
+              y += ddy;
+              z += ddz;
+              if (z >= p.hz) {
+                z -= p.hz;
+                ++y;
+              }
+            }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&stg_empty[s_st]);
+            if (++s_st == p.n_stg) {
+              s_st = 0;
+              s_ph ^= 1;
+            }
+          }
+        // the tensor core reads the stage through the async proxy
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (PAIR)
+            mbar_arrive_cta_release(&a_full[a_st], 0);
+          else
+            mbar_arrive(&a_full[a_st]);
+        }
+        if (++a_st == p.na) a_st = 0;
+      }
+    }
   } else {
     // ===================== epilogue (EPI_WARPS warps, EPI_WARPS/4 per quarter) ==
     // Work item = (slice, 16 accumulator columns).  The TMEM load of item k+1
@@ -800,13 +901,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 // ---------------------------------------------------------------- host side
 
 size_t tc_smem_bytes(const TcParams &p) {
-  return smem_map(p).bars + (2 * p.na + 2 * p.nb_stages + 4) * sizeof(uint64_t) + 16;
+  return smem_map(p).bars + (2 * p.na + 2 * p.nb_stages + 4 + 2 * p.n_stg) * sizeof(uint64_t) +
+         16;
 }
 
-template <int ACT, bool FASTOUT, bool BASE, bool PAIR>
+template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN = false>
 static int launch_variant(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t stream,
                           size_t smem) {
-  auto kern = conv3d_tc_kernel<ACT, FASTOUT, BASE, PAIR>;
+  auto kern = conv3d_tc_kernel<ACT, FASTOUT, BASE, PAIR, F32IN>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -816,7 +918,7 @@ static int launch_variant(const TcParams &p, const TcMaps &maps, int grid, cudaS
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(TC_THREADS);
+  cfg.blockDim = dim3(tc_threads(F32IN));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
@@ -838,11 +940,31 @@ static int launch_variant(const TcParams &p, const TcMaps &maps, int grid, cudaS
   return check_cuda(cudaLaunchKernelEx(&cfg, kern, p, maps), "conv3d_tc_kernel launch");
 }
 
+template <bool PAIR>
+static int launch_f32in(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t s,
+                        size_t smem) {
+  switch (p.act) {
+    case VXB_ACT_RELU:
+      return launch_variant<VXB_ACT_RELU, true, false, PAIR, true>(p, maps, grid, s, smem);
+    case VXB_ACT_ELU:
+      return launch_variant<VXB_ACT_ELU, true, false, PAIR, true>(p, maps, grid, s, smem);
+    case VXB_ACT_SIGMOID:
+      return launch_variant<VXB_ACT_SIGMOID, true, false, PAIR, true>(p, maps, grid, s, smem);
+    default: return launch_variant<VXB_ACT_NONE, true, false, PAIR, true>(p, maps, grid, s, smem);
+  }
+}
+
 template <bool BASE, bool PAIR>
 static int launch_act(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t s,
                       size_t smem) {
   const bool fast = (p.out.dtype == VXB_BF16 && p.out.blocked) ||
                     (p.out.dtype == VXB_F32 && !p.out.blocked);
+  if (p.f32in) {
+    if (BASE || !fast)
+      return set_error(VXB_EUNSUPPORTED,
+                       "fp32-input conv: no residual operand, output bf16 blocked or fp32 NCDHW");
+    return launch_f32in<PAIR>(p, maps, grid, s, smem);
+  }
   if (!fast) {
     if (PAIR) return set_error(VXB_EUNSUPPORTED, "pair mode needs a blocked bf16 output");
     return launch_variant<-1, false, BASE, false>(p, maps, grid, s, smem);

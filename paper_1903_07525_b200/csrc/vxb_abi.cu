@@ -222,8 +222,9 @@ struct TcConfig {
 static const int kTileOverhead = 3;
 
 static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, long long other_tiles,
-                        int sms, int reps, TcConfig &c) {
-  const int budget = 227 * 1024 - 6144;  // room for bias/scale/tap tables/barriers
+                        int sms, int reps, int reserved, TcConfig &c) {
+  // room for bias/scale/barriers, plus the fp32-input staging ring if any
+  const int budget = 227 * 1024 - 6144 - reserved;
   c.acc = env_int("VXB_TC_ACC", 2);
   if (c.acc != 1 && c.acc != 2) c.acc = 2;
   int bx_cap = env_int("VXB_TC_BX", 8);
@@ -255,7 +256,8 @@ static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, lon
     max_steps = std::max(max_steps, g.steps);
   }
   const int slab = L.slab;
-  int na_cap = std::max(2, std::min(6, env_int("VXB_TC_NA", 3)));
+  // fp32-input convs buffer their input in the staging ring: two A stages
+  int na_cap = reserved ? 2 : std::max(2, std::min(6, env_int("VXB_TC_NA", 3)));
   for (;;) {
     const int sx = L.fold == 2 ? TILE_Y : c.bx, sy = L.fold == 2 ? c.bx : TILE_Y;
     const int hx = sx + k[0] - 1, hy = sy + k[1] - 1, hz = TILE_Z + k[2] - 1;
@@ -397,7 +399,29 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   if (sms <= 0) return set_error(VXB_ECUDA, "no CUDA device");
   const long long other_tiles = static_cast<long long>(ceil_div(slice_y ? a.ox : a.oy, TILE_Y)) *
                                 ceil_div(a.oz, TILE_Z) * a.nb * L.n_tiles * a.reps;
-  int rc = tc_configure(L, a.k, slice_y ? a.oy : a.ox, other_tiles, sms, a.reps, c);
+  // fp32 NCDHW input (the network's own input tensor): converted in-kernel
+  const vxb_tensor &x0 = *a.in[0];
+  const bool f32in = x0.dtype == VXB_F32 && !x0.blocked;
+  // staging ring: ~80 KB of fp32 boxes in flight covers the TMA latency at
+  // the input rate of the low-fmap convs (each box <= 16 KB: xb x-slices)
+  const int kStgBudget = 80 * 1024;
+  int stg_bytes = 0, hzb = 0, zshift = 0;
+  if (f32in) {
+    if (a.in[1] || a.has_base)
+      return set_error(VXB_EUNSUPPORTED,
+                       "fp32-input conv supports one input segment and no residual operand");
+    if (x0.s[4] != 1 || (reinterpret_cast<uintptr_t>(x0.data) & 15) || (x0.s[3] * 4) % 16 ||
+        (x0.s[2] * 4) % 16 || (x0.s[1] * 4) % 16 || (x0.n > 1 && (x0.s[0] * 4) % 16))
+      return set_error(VXB_EINVAL,
+                       "fp32-input conv needs a z-contiguous view with 16-byte aligned rows");
+    // TMA needs the box's innermost (z) start 16-byte aligned: boxes start at
+    // the halo origin rounded down to 4 floats (tile origins are multiples of
+    // 8, so the shift is a per-layer constant) and rows are 16-byte multiples
+    zshift = (((a.off[0][2] - a.pad[2]) % 4) + 4) % 4;
+    hzb = round_up(zshift + TILE_Z + a.k[2] - 1, 4);
+    stg_bytes = kStgBudget;
+  }
+  int rc = tc_configure(L, a.k, slice_y ? a.oy : a.ox, other_tiles, sms, a.reps, stg_bytes, c);
   if (rc) return rc;
   TcParams p;
   memset(&p, 0, sizeof(p));
@@ -458,8 +482,48 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
     p.seg_chunks[s] = L.seg_chunks[s];
     if (!p.seg_chunks[s]) continue;
     for (int i = 0; i < 3; ++i) p.seg_off[s][i] = a.off[s][i];
+    if (f32in) continue;
     rc = make_input_map(*a.in[s], p.hx, p.hy, p.hz, &maps.m[s], &p.seg_bstride[s]);
     if (rc) return rc;
+  }
+  if (f32in) {
+    p.f32in = 1;
+    p.hzb = hzb;
+    const int slice_bytes = LANES * p.hy * hzb * 4;
+    p.f32in_xb = std::max(1, std::min(p.hx, 16384 / slice_bytes));
+    p.stg_bytes = p.f32in_xb * slice_bytes;
+    p.n_stg = std::max(2, std::min(8, kStgBudget / p.stg_bytes));
+    p.f32in_zshift = zshift;
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return set_error(VXB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    // 4-D (z, y, x, batch*channel): lanes past C must read as zero, so a
+    // batch > 1 needs whole chunks (C % 8 == 0) and a channel-stride batch
+    if (x0.n > 1 && (x0.c % LANES || x0.s[0] != x0.s[1] * x0.c))
+      return set_error(VXB_EUNSUPPORTED,
+                       "fp32-input conv with batch > 1 needs C %% 8 == 0 and packed batches");
+    p.f32in_cstride = x0.c;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(x0.z), static_cast<cuuint64_t>(x0.y),
+                          static_cast<cuuint64_t>(x0.x),
+                          static_cast<cuuint64_t>(x0.c) * x0.n};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(x0.s[3]) * 4,
+                             static_cast<cuuint64_t>(x0.s[2]) * 4,
+                             static_cast<cuuint64_t>(x0.s[1]) * 4};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(hzb), static_cast<cuuint32_t>(p.hy),
+                         static_cast<cuuint32_t>(p.f32in_xb), static_cast<cuuint32_t>(LANES)};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(&maps.m[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, x0.data, dims, strides, box,
+                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return set_error(VXB_ECUDA, "fp32 input tensor map failed (%d)", static_cast<int>(r));
+    if (env_int("VXB_PRINT", 0))
+      fprintf(stderr, "f32in map dims %llu %llu %llu %llu str %llu %llu %llu box %u %u %u %u "
+              "hx %d hy %d hz %d bx %d stg %d smem-a %d nb %d bst %d na %d\n",
+              (unsigned long long)dims[0], (unsigned long long)dims[1], (unsigned long long)dims[2],
+              (unsigned long long)dims[3], (unsigned long long)strides[0],
+              (unsigned long long)strides[1], (unsigned long long)strides[2], box[0], box[1],
+              box[2], box[3], p.hx, p.hy, p.hz, c.bx, p.stg_bytes, c.a_stage, c.nb, c.b_stage,
+              c.na);
   }
   p.n_groups = static_cast<int>(L.groups.size());
   p.chunk_bytes = c.chunk_bytes;

@@ -39,6 +39,13 @@ struct TcParams {
   int ex, ey;                  // tile extents along x and y
   int slab_bytes;              // B bytes per K step (nt rows, or 3*nt when folded)
   int a_slice_inc, a_sbo;      // smem bytes between slices / between 8-row groups
+  // fp32 NCDHW input converted in the kernel (no separate pack): TMA boxes of
+  // (hzb z, hy y, 1 x, 8 c) fp32 land in a staging ring, converter warps write
+  // the bf16 chunk rows of the A stage
+  int f32in, stg_bytes, n_stg, hzb;
+  int f32in_cstride;           // channel-coordinate distance between batches
+  int f32in_zshift;            // box z start is rounded down to 16 B: rows start this far in
+  int f32in_xb;                // halo x-slices per staging box
   int acc_stages;              // TMEM accumulator stages
   int kx, ky, kz;
   int hx, hy, hz;              // halo tile extents

@@ -76,6 +76,14 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *m, uin
       "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *m, uint64_t *bar,
+                                            int c0, int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+      : "memory");
+}
 // plain bulk copy global -> shared, completes on the mbarrier
 __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes,
                                           uint64_t *bar) {
@@ -124,6 +132,16 @@ __device__ __forceinline__ void tma_load_4d_pair(void *dst, const CUtensorMap *m
       : "memory");
 }
 // arrive on the mbarrier at the same offset in CTA `cta` of the cluster
+// arrive on CTA `cta`'s barrier at the same smem offset, releasing this
+// thread's prior shared-memory writes at cluster scope
+__device__ __forceinline__ void mbar_arrive_cta_release(uint64_t *bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cta(uint64_t *bar, uint32_t cta) {
   asm volatile(
       "{\n\t.reg .b32 ra;\n\t"

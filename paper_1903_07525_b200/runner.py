@@ -67,7 +67,8 @@ class _Value:
 class PlanRunner:
     """Executes one ExecutionPlan on one B200; reusable, deterministic."""
 
-    def __init__(self, plan, backend=None, *, device=None, use_graph=True, fuse_concat=True):
+    def __init__(self, plan, backend=None, *, device=None, use_graph=True, fuse_concat=True,
+                 fuse_input=False):
         torch = _torch()
         from .backend import resolve_device_backend
         self.backend = resolve_device_backend(backend)
@@ -79,6 +80,7 @@ class PlanRunner:
         self.use_graph = use_graph
         self.precision = self.backend.precision
         self.fuse_concat = fuse_concat and self.precision == "bf16"
+        self.fuse_input = fuse_input
         self._conv_path = _lib.PATH_DIRECT if self.precision == "fp32" else 0
         self.stream = torch.cuda.Stream(device=self.device)
         with torch.cuda.device(self.device):
@@ -262,9 +264,26 @@ class PlanRunner:
         w = self.plan.weights
         dev = self.device
         calls = []
+        # fused input pack (opt-in, fuse_input=True): a network input read only
+        # by one tensor-core conv goes to that conv as the fp32 NCDHW tensor
+        # itself (converted to bf16 chunks inside the conv, no pack kernel).
+        # Off by default: its fp32 TMA boxes have 48-byte rows and the staging
+        # + conversion pipeline is slower than the HBM-bound pack kernel
+        #
+        readers = {}
+        for kind, st, info in self._ops:
+            if kind is LayerKind.CONVOLUTION and info.get("x") is not None:
+                readers.setdefault(id(info["x"]), []).append((st, info))
+        fused_in = {}
         for name, v in self._in_values.items():
+            rs = readers.get(id(v), [])
+            if v.readers == 1 and len(rs) == 1 and self._f32in_ok(name, *rs[0]):
+                fused_in[id(rs[0][1])] = standard(self._in_std[name])
+                continue
             src = standard(self._in_std[name])
             calls.append(lambda s=src, d=v.dt: _copy(s, d))
+        n_in = len(calls)
+        self.fused_inputs = len(fused_in)
         # fused unpack: a conv/deconv whose result is only a network output
         # writes the fp32 NCDHW output tensor directly from its epilogue
         fused_out = {}
@@ -294,7 +313,10 @@ class PlanRunner:
                     pk = K.pack_conv(kern, w.tensor(st.name, ROLE_BIAS), stride=stride,
                                      base_scale=scale, path=self._conv_path,
                                      out_shape=tuple(info["out"].dims[2:]), device=dev)
-                    calls.append(lambda x=info["x"].dt, pk=pk, out=out, base=base,
+                    x = fused_in.get(id(info), info["x"].dt)
+                    if id(info) in fused_in and pk.path not in (_lib.PATH_TC, _lib.PATH_TC_UNFOLDED):
+                        raise ExecutionError("fused fp32 input needs the tensor-core conv path")
+                    calls.append(lambda x=x, pk=pk, out=out, base=base,
                                  pad=info["pad"], act=st.fused_act:
                                  K.conv3d(x, pk, out, pad=pad, base=base, fused_act=act))
             elif kind is LayerKind.DECONVOLUTION:
@@ -333,7 +355,6 @@ class PlanRunner:
                              K.affine_act(x, out, None, None, act, alpha))
             else:
                 raise ExecutionError("plan step %r has unrunnable kind %s" % (st.name, kind))
-        n_in = len(self._in_values)
         self.op_calls = calls[n_in:n_in + len(self._ops)]   # one device call per lowered op
         for name, v in self._out_values.items():
             if name in self._fused_outputs:
@@ -341,6 +362,24 @@ class PlanRunner:
             dst = standard(self._out_std[name])
             calls.append(lambda s=v.dt, d=dst: _copy(s, d))
         self._calls = calls
+
+    def _f32in_ok(self, name, st, info) -> bool:
+        """Can this conv read network input `name` as fp32 NCDHW directly
+        (vxb_conv3d's in-kernel conversion: stride 1, one input segment, no
+        residual, z rows of 16-byte multiples, whole chunks when batch > 1)?"""
+        if not self.fuse_input or self.precision != "bf16":
+            return False
+        if "segments" in info or "base" in info or st.additive:
+            return False
+        if tuple(st.params.get("stride", (1, 1, 1))) != (1, 1, 1):
+            return False
+        n, c, x, y, z = self._input_dims[name]
+        k = tuple(int(v) for v in self.plan.weights.tensor(st.name, ROLE_KERNEL).shape[2:])
+        if z % 4 or (n > 1 and c % LANES):
+            return False
+        L = _lib.lib()
+        return L.vxb_conv_select(c, st.output.dims[1], _lib.i3(k), _lib.i3((1, 1, 1))) == \
+            _lib.PATH_TC
 
     # ------------------------------------------------------------ running
     def _launch_all(self):

@@ -140,6 +140,65 @@ def test_unfolded_path_for_badly_padded_rows():
         assert mx < BF16_TOL and l2 < 3e-3, (path, mx, l2)
 
 
+@pytest.mark.parametrize("cin,cout,k,pad,sp,n,out_dtype", [
+    (16, 16, (3, 3, 3), (1, 1, 1), (6, 20, 16), 1, "bf16"),
+    (1, 28, (1, 3, 3), (0, 1, 1), (5, 18, 12), 1, "bf16"),       # Cin < 8: OOB lanes
+    (16, 20, (3, 3, 3), (1, 1, 1), (9, 17, 20), 2, "fp32"),      # batch 2, fp32 NCDHW out
+    (13, 20, (3, 3, 3), (1, 1, 1), (9, 17, 20), 1, "bf16"),      # ragged chunk
+    (64, 64, (3, 3, 3), (1, 1, 1), (4, 16, 16), 1, "bf16"),
+    (128, 128, (3, 3, 3), (1, 1, 1), (4, 16, 8), 1, "bf16"),     # CTA pair (streamed B)
+    (32, 32, (3, 3, 3), (0, 0, 0), (8, 20, 12), 1, "bf16"),      # valid padding
+])
+def test_fp32_input_converted_in_kernel(cin, cout, k, pad, sp, n, out_dtype):
+    """The network's fp32 NCDHW input fed straight to the tensor-core conv
+    (fp32 TMA boxes + in-kernel bf16 conversion) equals packing first."""
+    import torch
+    D, K = _dev()
+    rng = np.random.default_rng(cin * 7 + cout)
+    x = rng.uniform(-1, 1, (n, cin) + sp).astype(np.float32)
+    w = (rng.standard_normal((cout, cin) + k) * np.sqrt(2.0 / (cin * np.prod(k)))).astype(np.float32)
+    b = (rng.standard_normal(cout) * 0.1).astype(np.float32)
+    osp = tuple(s + 2 * p - kk + 1 for s, p, kk in zip(sp, pad, k))
+    pk = K.pack_conv(w, b)
+    xs = D.standard(torch.from_numpy(x).cuda())
+    if out_dtype == "fp32":
+        out_t = torch.empty((n, cout) + osp, dtype=torch.float32, device="cuda")
+        out = D.standard(out_t)
+    else:
+        out = D.empty_blocked(n, cout, osp)
+    K.conv3d(xs, pk, out, pad=pad, fused_act=("elu", 1.0))
+    torch.cuda.synchronize()
+    got = out_t.cpu().numpy() if out_dtype == "fp32" else D.to_host_standard(out)
+    # same conv from the packed (bf16 blocked) input into the same output layout
+    if out_dtype == "fp32":
+        ref_t = torch.empty_like(out_t)
+        ref = D.standard(ref_t)
+    else:
+        ref = D.empty_blocked(n, cout, osp)
+    K.conv3d(D.to_device_blocked(x), pk, ref, pad=pad, fused_act=("elu", 1.0))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(
+        got, ref_t.cpu().numpy() if out_dtype == "fp32" else D.to_host_standard(ref))
+    want = _ref_bf16(x, w, b, pad, "elu")
+    mx, l2 = R.normalized_error(got, want)
+    assert mx < BF16_TOL and l2 < 3e-3, (mx, l2)
+
+
+def test_fp32_input_unsupported_views_raise():
+    """Batch > 1 with a ragged last chunk cannot zero its tail lanes through
+    the folded (batch*channel) TMA coordinate: the library refuses it."""
+    import torch
+    from paper_1903_07525_b200 import ExecutionError
+    D, K = _dev()
+    pk = K.pack_conv(np.ones((8, 13, 3, 3, 3), np.float32), np.zeros(8, np.float32))
+    xs = D.standard(torch.zeros((2, 13, 4, 8, 8), device="cuda"))
+    with pytest.raises(ExecutionError):
+        K.conv3d(xs, pk, D.empty_blocked(2, 8, (4, 8, 8)), pad=(1, 1, 1))
+    xs = D.standard(torch.zeros((1, 13, 4, 8, 6), device="cuda"))   # z rows of 24 B
+    with pytest.raises(ExecutionError):
+        K.conv3d(xs, pk, D.empty_blocked(1, 8, (4, 8, 6)), pad=(1, 1, 1))
+
+
 def test_tc_conv_fp32_output_and_batch2():
     rng = np.random.default_rng(7)
     x = rng.uniform(-1, 1, (2, 16, 4, 18, 10)).astype(np.float32)

@@ -114,6 +114,23 @@ def test_runner_graph_replay_deterministic_and_validates():
     np.testing.assert_array_equal(d, a)
 
 
+@pytest.mark.parametrize("cfg", [1, 4])
+def test_fused_input_pack_is_bit_identical(cfg):
+    """fuse_input=True hands the fp32 network input straight to the first
+    conv (in-kernel conversion); the bf16 operands and hence the outputs are
+    identical to packing first."""
+    spec, store = _small(cfg)
+    plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
+    lo, hi = C.input_range(cfg)
+    x = C.make_input(spec, 3, lo, hi)
+    fused = P.PlanRunner(plan, fuse_input=True)
+    assert fused.fused_inputs == 1
+    plain = P.PlanRunner(plan)
+    assert plain.fused_inputs == 0 and plain.launches == fused.launches + 1
+    (n, a), = fused.run(x).items()
+    np.testing.assert_array_equal(a, plain.run(x)[n])
+
+
 def test_run_tiled_equals_manual_assembly():
     """test_acceptance.py:343-362 / test_tiling.py:111-142: tiled output equals
     the manual assembly of per-patch runs, exactly (each tile is a

@@ -19,6 +19,8 @@ for case in os.environ.get("CASES", "8:333,16:333,32:333").split(","):
     k = tuple(int(v) for v in ks)
     x = D.empty_blocked(1, c, spatial)
     x.t.copy_(torch.randn(x.t.shape, device=dev).to(torch.bfloat16))
+    if os.environ.get("F32IN"):
+        x = D.standard(torch.randn((1, c) + spatial, device=dev))
     out = D.empty_blocked(1, c, spatial)
     w = (np.random.default_rng(0).standard_normal((c, c) + k) * 0.05).astype(np.float32)
     pk = K.pack_conv(w, np.zeros(c, np.float32))
