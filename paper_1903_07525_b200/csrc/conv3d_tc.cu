@@ -233,16 +233,7 @@ __device__ __forceinline__ void mma_group(
     tc_fence_after();
     uint32_t b_lo = desc_lo(b_base0 + b_st * b_stage_bytes, 128u);
     for (int i = 0; i < n; ++i) {
-      const uint32_t a_lo = a_lo0 + off;
-#pragma unroll
-      for (int s = 0; s < BX; ++s) {
-        if (PAIRM)
-          umma_bf16_pair_lohi_elect(d_base + s * nt, a_lo + s * slice_inc, a_hi, b_lo, b_hi,
-                                    idesc, acc);
-        else
-          umma_bf16_lohi_elect(d_base + s * nt, a_lo + s * slice_inc, a_hi, b_lo, b_hi, idesc,
-                               acc);
-      }
+      umma_step_elect<BX, PAIRM>(d_base, a_lo0 + off, a_hi, b_lo, b_hi, idesc, acc, nt, slice_inc);
       acc = 1;
       b_lo += b_inc;
       off += dz_step;
@@ -430,7 +421,9 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
   __syncthreads();
   if (p.cluster == 2) cluster_sync_all();   // peer barriers initialised before multicast
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  // broadcast (not a plain smem load) so the compiler knows it is warp-uniform
+  // and keeps everything derived from it in uniform registers
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   pdl_wait();   // activations (inputs, residual, output buffer) belong to the predecessor until here
 
   if (warp == 0) {
@@ -585,8 +578,13 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
       cx.resident = p.resident;
       cx.cluster = p.cluster;
       int a_st = 0, a_ph = 0, b_st = 0, b_ph = 0;
-      int it = 0;
-      for (int tile = first_tile; tile < p.total_tiles; tile += tile_step, ++it) {
+      // Count this CTA's tiles up front: a loop bound compared against a
+      // tile index derived from blockIdx makes ptxas treat the whole loop as
+      // divergent, and every MMA operand then goes through R2UR.BROADCAST
+      // (~5 extra instructions per MMA, which bounded the N = 128 convs).
+      const int my_tiles =
+          first_tile < p.total_tiles ? (p.total_tiles - first_tile + tile_step - 1) / tile_step : 0;
+      for (int it = 0; it < my_tiles; ++it) {
         const int acc = it % p.acc_stages;
         mbar_wait(&t_empty[acc], ((it / p.acc_stages) & 1) ^ 1);
         tc_fence_after();

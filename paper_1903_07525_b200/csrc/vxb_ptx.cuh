@@ -358,6 +358,59 @@ __device__ __forceinline__ void umma_bf16_pair_lohi_elect(uint32_t d, uint32_t a
       "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// One K step of BX slices in a single asm block: one elect, then BX MMAs
+// whose A start (lo word) and D column advance by constant strides.  Keeping
+// the whole step in one block avoids re-electing and re-broadcasting the
+// loop-invariant descriptor words for every MMA (the issue loop, not the
+// tensor pipe, bounded the N = 128 convs).
+#define VXB_UMMA_HEAD                                                        \
+  "{\n\t.reg .pred e, p;\n\t.reg .b64 ad, bd;\n\t.reg .b32 al, dd;\n\t"     \
+  "elect.sync _|e, 0xffffffff;\n\t"                                          \
+  "setp.ne.b32 p, %6, 0;\n\t"                                                \
+  "mov.b32 al, %1;\n\tmov.b32 dd, %0;\n\t"                                   \
+  "mov.b64 ad, {al, %2};\n\tmov.b64 bd, {%3, %4};\n\t"
+#define VXB_UMMA_NEXT "add.u32 al, al, %8;\n\tadd.u32 dd, dd, %7;\n\tmov.b64 ad, {al, %2};\n\t"
+#define VXB_UMMA_1 "@e tcgen05.mma.cta_group::1.kind::f16 [dd], ad, bd, %5, p;\n\t"
+#define VXB_UMMA_2 "@e tcgen05.mma.cta_group::2.kind::f16 [dd], ad, bd, %5, p;\n\t"
+#define VXB_UMMA_OPS                                                                      \
+  ::"r"(d), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate), "r"(d_inc), \
+      "r"(a_inc)                                                                          \
+      : "memory"
+
+template <int BX, bool PAIR>
+__device__ __forceinline__ void umma_step_elect(uint32_t d, uint32_t a_lo, uint32_t a_hi,
+                                                uint32_t b_lo, uint32_t b_hi, uint32_t idesc,
+                                                uint32_t accumulate, uint32_t d_inc,
+                                                uint32_t a_inc) {
+  static_assert(BX == 1 || BX == 2 || BX == 4 || BX == 8, "step width");
+  if (PAIR) {
+    if (BX == 1) asm volatile(VXB_UMMA_HEAD VXB_UMMA_2 "}" VXB_UMMA_OPS);
+    if (BX == 2) asm volatile(VXB_UMMA_HEAD VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2 "}" VXB_UMMA_OPS);
+    if (BX == 4)
+      asm volatile(VXB_UMMA_HEAD VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2
+                       VXB_UMMA_NEXT VXB_UMMA_2 "}" VXB_UMMA_OPS);
+    if (BX == 8)
+      asm volatile(VXB_UMMA_HEAD VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2
+                       VXB_UMMA_NEXT VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2
+                           VXB_UMMA_NEXT VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2 "}" VXB_UMMA_OPS);
+  } else {
+    if (BX == 1) asm volatile(VXB_UMMA_HEAD VXB_UMMA_1 "}" VXB_UMMA_OPS);
+    if (BX == 2) asm volatile(VXB_UMMA_HEAD VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1 "}" VXB_UMMA_OPS);
+    if (BX == 4)
+      asm volatile(VXB_UMMA_HEAD VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1
+                       VXB_UMMA_NEXT VXB_UMMA_1 "}" VXB_UMMA_OPS);
+    if (BX == 8)
+      asm volatile(VXB_UMMA_HEAD VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1
+                       VXB_UMMA_NEXT VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1
+                           VXB_UMMA_NEXT VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1 "}" VXB_UMMA_OPS);
+  }
+}
+#undef VXB_UMMA_HEAD
+#undef VXB_UMMA_NEXT
+#undef VXB_UMMA_1
+#undef VXB_UMMA_2
+#undef VXB_UMMA_OPS
+
 __device__ __forceinline__ void umma_commit_pair(uint64_t *bar, uint16_t cta_mask) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
