@@ -449,6 +449,40 @@ class PlanRunner:
                 for name, t in self._out_std.items()}
         return outs
 
+    def run_async(self, inputs, out) -> "PendingRun":
+        """Non-blocking forward for pipelined serving: page-locked float32
+        inputs (``staging.pinned_empty``) and ``out={name: pinned array}``.
+        The H2D copies, the graph replay and the D2H copies are enqueued on
+        this runner's stream and the call returns at once; ``.wait()`` on the
+        result blocks until ``out`` holds the results.  Calls on one runner
+        are ordered by its stream; runners on different streams overlap (one
+        volume's upload with another's download and compute).  The inputs
+        must stay untouched until the run completes."""
+        from . import staging
+        torch = _torch()
+        inputs = self._normalize(inputs)
+        for name, arr in inputs.items():
+            if not staging.is_pinned(arr):
+                raise ExecutionError("run_async needs page-locked float32 inputs "
+                                     "(staging.pinned_empty)")
+        for name, t in self._out_std.items():
+            o = out.get(name) if out else None
+            if o is None or tuple(o.shape) != tuple(t.shape) or not staging.is_pinned(o):
+                raise ExecutionError("run_async needs a pinned float32 out[%r] of shape %s"
+                                     % (name, tuple(t.shape)))
+        if self._graph is None:
+            self._replay()              # first call: capture (synchronous once)
+            self.stream.synchronize()
+        with torch.cuda.stream(self.stream):
+            for name, arr in inputs.items():
+                self._in_std[name].copy_(torch.from_numpy(arr), non_blocking=True)
+            self._graph.replay() if self._graph is not None else self._launch_all()
+            for name, t in self._out_std.items():
+                torch.from_numpy(out[name]).copy_(t, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+        return PendingRun(ev, {name: out[name] for name in self._out_std})
+
     def input_buffers(self) -> dict:
         """The static device input tensors the captured graph reads.  Filling
         them in place and passing them to ``run_device`` skips its copy."""
@@ -461,6 +495,21 @@ class PlanRunner:
     @property
     def d2h_bytes(self) -> int:
         return sum(t.numel() * 4 for t in self._out_std.values())
+
+
+class PendingRun:
+    """Handle of a ``PlanRunner.run_async`` call."""
+
+    def __init__(self, event, outputs):
+        self._event = event
+        self.outputs = outputs
+
+    def done(self) -> bool:
+        return self._event.query()
+
+    def wait(self) -> dict:
+        self._event.synchronize()
+        return self.outputs
 
 
 def _copy(src: DTensor, dst: DTensor):

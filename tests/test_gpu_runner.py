@@ -108,6 +108,17 @@ def test_runner_graph_replay_deterministic_and_validates():
     np.testing.assert_array_equal(c, a)
     with pytest.raises(P.ExecutionError):
         runner.run(x, out={"out_elu": np.empty_like(a)})
+    # pipelined: two volumes in flight on one runner, stream-ordered
+    x2 = C.make_input(spec, 2)
+    xp2 = staging.pinned_empty(x2.shape)
+    xp2[...] = x2
+    o1, o2 = staging.pinned_empty(a.shape), staging.pinned_empty(a.shape)
+    h1 = runner.run_async(xp, out={"out_elu": o1})
+    h2 = runner.run_async(xp2, out={"out_elu": o2})
+    np.testing.assert_array_equal(h1.wait()["out_elu"], a)
+    np.testing.assert_array_equal(h2.wait()["out_elu"], runner.run(x2)["out_elu"])
+    with pytest.raises(P.ExecutionError):
+        runner.run_async(x, out={"out_elu": o1})           # pageable input
     bufs = runner.input_buffers()
     bufs["data"].copy_(torch.from_numpy(x))
     d = runner.run_device(bufs)["out_elu"].cpu().numpy()
