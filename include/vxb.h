@@ -56,6 +56,8 @@ extern "C" {
 #define VXB_PATH_TC 1     /* tcgen05/TMEM implicit GEMM, TMA-fed */
 #define VXB_PATH_DIRECT 2 /* CUDA-core direct convolution (Cin<8, strides, big k) */
 #define VXB_PATH_TC_UNFOLDED 3 /* tensor-core path without slice-axis tap folding */
+#define VXB_PATH_TC_N128 4     /* tensor-core path, output fmaps in N tiles of <= 128 */
+#define VXB_PATH_TC_N64 5      /* tensor-core path, output fmaps in N tiles of <= 64 */
 
 /* pooling modes: ops.py:63-86 */
 #define VXB_POOL_MAX 0
@@ -146,8 +148,10 @@ size_t vxb_debug_read(unsigned long long *host, size_t count);
 int vxb_conv_select(int cin, int cout, const int k[3], const int stride[3]);
 /* as vxb_conv_select, knowing the output extent: a 1x3x3 conv whose x extent
  * pads badly to the 16-row tiles of y-sliced folding (e.g. x = 18) gets
- * VXB_PATH_TC_UNFOLDED.  Replaces the same per-layer choice the reference
- * makes once per bind (kernels_cy.py:22-27 lane-kernel cache). */
+ * VXB_PATH_TC_UNFOLDED; a layer with too few output tiles to fill the SMs
+ * (deep U-net levels) splits its output fmaps into narrower N tiles
+ * (VXB_PATH_TC_N128 / _N64).  Replaces the same per-layer choice the
+ * reference makes once per bind (kernels_cy.py:22-27 lane-kernel cache). */
 int vxb_conv_select_shape(int cin, int cout, const int k[3], const int stride[3],
                           const int out_xyz[3]);
 /* bytes of the packed weight image for a conv of this geometry */

@@ -22,6 +22,9 @@ ACT_CODE = {None: 0, "relu": 1, "elu": 2, "sigmoid": 3}   # kernels_cy.py:19
 PATH_TC = 1
 PATH_DIRECT = 2
 PATH_TC_UNFOLDED = 3
+PATH_TC_N128 = 4
+PATH_TC_N64 = 5
+TC_PATHS = (PATH_TC, PATH_TC_UNFOLDED, PATH_TC_N128, PATH_TC_N64)
 POOL_CODE = {"max": 0, "avg": 1}
 ELT_CODE = {"add": 0, "mul": 1, "div": 2}
 

@@ -109,14 +109,22 @@ static int tc_fold_axis(int nt, const int k[3]) {
   return 0;
 }
 
-static bool is_tc(int path) { return path == VXB_PATH_TC || path == VXB_PATH_TC_UNFOLDED; }
+static bool is_tc(int path) {
+  return path == VXB_PATH_TC || path == VXB_PATH_TC_UNFOLDED || path == VXB_PATH_TC_N128 ||
+         path == VXB_PATH_TC_N64;
+}
+static bool path_folds(int path) { return path != VXB_PATH_TC_UNFOLDED; }
+static int path_nt_cap(int path) {
+  return path == VXB_PATH_TC_N64 ? 64 : path == VXB_PATH_TC_N128 ? 128 : 256;
+}
 
-static TcLayout tc_layout(int cin0, int cin1, int cout, const int k[3], bool allow_fold = true) {
+static TcLayout tc_layout(int cin0, int cin1, int cout, const int k[3], bool allow_fold = true,
+                          int nt_cap = 256) {
   TcLayout L;
   L.npad = round_up(cout, 16);
-  L.n_tiles = ceil_div(L.npad, 256);
+  L.n_tiles = ceil_div(L.npad, nt_cap);
   L.nt = round_up(ceil_div(L.npad, L.n_tiles), 16);
-  L.fold = (allow_fold && L.n_tiles == 1) ? tc_fold_axis(L.nt, k) : 0;
+  L.fold = allow_fold ? tc_fold_axis(L.nt, k) : 0;
   L.slab = (L.fold ? 3 : 1) * L.nt * SLAB_ROW_BYTES;
   L.seg_chunks[0] = ceil_div(cin0, 8);
   L.seg_chunks[1] = cin1 > 0 ? ceil_div(cin1, 8) : 0;
@@ -389,10 +397,11 @@ struct TcLaunch {
   int act;
   float alpha;
   bool allow_fold;
+  int nt_cap;
 };
 
 static int run_tc(const TcLaunch &a, cudaStream_t stream) {
-  TcLayout L = tc_layout(a.cin0, a.cin1, a.cout, a.k, a.allow_fold);
+  TcLayout L = tc_layout(a.cin0, a.cin1, a.cout, a.k, a.allow_fold, a.nt_cap > 0 ? a.nt_cap : 256);
   TcConfig c;
   const int slice_y = L.fold == 2;
   int sms = device_sms();
@@ -611,6 +620,11 @@ int vxb_conv_select(int cin, int cout, const int k[3], const int stride[3]) {
   return VXB_PATH_DIRECT;
 }
 
+static int device_sms_or(int fallback) {
+  const int n = device_sms();
+  return n > 0 ? n : fallback;
+}
+
 int vxb_conv_select_shape(int cin, int cout, const int k[3], const int stride[3],
                           const int out_xyz[3]) {
   int path = vxb_conv_select(cin, cout, k, stride);
@@ -618,7 +632,17 @@ int vxb_conv_select_shape(int cin, int cout, const int k[3], const int stride[3]
   const TcLayout L = tc_layout(cin, 0, cout, k);
   if (L.fold == 2 && out_xyz[0] > 0 && ceil_div(out_xyz[0], TILE_Y) * TILE_Y * 4 > out_xyz[0] * 5)
     return VXB_PATH_TC_UNFOLDED;   // > 25% of the 16-row x tiles would be padding
-  return path;
+  // Too few output tiles for the SMs (deep levels: 9^3 .. 16^3 voxels with
+  // 256-512 fmaps)?  Narrower N tiles multiply the tile count; every N tile
+  // re-reads the (small, L2-resident) input.  Spatial tiles are estimated
+  // at 4 slices per tile.
+  const int sms = std::max(1, device_sms_or(148));
+  const long long sp = static_cast<long long>(ceil_div(out_xyz[0], 4)) *
+                       ceil_div(out_xyz[1], TILE_Y) * ceil_div(out_xyz[2], TILE_Z);
+  if (sp * L.n_tiles >= sms || L.npad <= 64) return path;
+  const TcLayout L128 = tc_layout(cin, 0, cout, k, true, 128);
+  if (sp * L128.n_tiles >= sms || L.npad <= 128) return VXB_PATH_TC_N128;
+  return VXB_PATH_TC_N64;
 }
 
 static size_t direct_bytes(int cin, int cout, const int k[3]) {
@@ -629,7 +653,8 @@ static size_t direct_bytes(int cin, int cout, const int k[3]) {
 size_t vxb_conv_weights_bytes2(int cin0, int cin1, int cout, const int k[3], const int stride[3],
                                int path) {
   if (path == 0) path = vxb_conv_select(cin0 + cin1, cout, k, stride);
-  if (is_tc(path)) return tc_bytes_per_rep(tc_layout(cin0, cin1, cout, k, path == VXB_PATH_TC));
+  if (is_tc(path))
+    return tc_bytes_per_rep(tc_layout(cin0, cin1, cout, k, path_folds(path), path_nt_cap(path)));
   return direct_bytes(cin0 + cin1, cout, k);
 }
 
@@ -648,7 +673,7 @@ int vxb_conv_pack_weights2(const float *w, int cin0, int cin1, int cout, const i
     return w[((((static_cast<size_t>(co) * cin) + ci) * k[0] + dx) * k[1] + dy) * k[2] + dz];
   };
   if (is_tc(path)) {
-    TcLayout L = tc_layout(cin0, cin1, cout, k, path == VXB_PATH_TC);
+    TcLayout L = tc_layout(cin0, cin1, cout, k, path_folds(path), path_nt_cap(path));
     tc_pack(L, cin0, cin1, cout, k, wtap, static_cast<uint8_t *>(dst));
     return VXB_OK;
   }
@@ -700,7 +725,8 @@ int vxb_conv3d(const vxb_conv_desc *d, void *stream) {
       return set_error(VXB_EUNSUPPORTED, "tensor-core conv requires stride 1");
     TcLaunch a;
     memset(&a, 0, sizeof(a));
-    a.allow_fold = path == VXB_PATH_TC;
+    a.allow_fold = path_folds(path);
+    a.nt_cap = path_nt_cap(path);
     a.in[0] = &d->in0;
     a.in[1] = two ? &d->in1 : nullptr;
     for (int i = 0; i < 3; ++i) {

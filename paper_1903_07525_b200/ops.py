@@ -74,7 +74,7 @@ def pack_conv(kernel, bias, *, stride=(1, 1, 1), base_scale=None, cin_split=None
                                            _lib.i3(tuple(out_shape)))
         else:
             path = L.vxb_conv_select(cin, cout, _lib.i3(k), _lib.i3(stride))
-    if cin1 and path not in (_lib.PATH_TC, _lib.PATH_TC_UNFOLDED):
+    if cin1 and path not in _lib.TC_PATHS:
         raise ExecutionError("a two-input (fused concat) conv needs the tensor-core path")
     nbytes = L.vxb_conv_weights_bytes2(cin0, cin1, cout, _lib.i3(k), _lib.i3(stride), path)
     host = np.zeros(nbytes, dtype=np.uint8)

@@ -314,7 +314,7 @@ class PlanRunner:
                                      base_scale=scale, path=self._conv_path,
                                      out_shape=tuple(info["out"].dims[2:]), device=dev)
                     x = fused_in.get(id(info), info["x"].dt)
-                    if id(info) in fused_in and pk.path not in (_lib.PATH_TC, _lib.PATH_TC_UNFOLDED):
+                    if id(info) in fused_in and pk.path not in _lib.TC_PATHS:
                         raise ExecutionError("fused fp32 input needs the tensor-core conv path")
                     calls.append(lambda x=x, pk=pk, out=out, base=base,
                                  pad=info["pad"], act=st.fused_act:

@@ -199,6 +199,29 @@ def test_fp32_input_unsupported_views_raise():
         K.conv3d(xs, pk, D.empty_blocked(1, 8, (4, 8, 6)), pad=(1, 1, 1))
 
 
+@pytest.mark.parametrize("path", [4, 5])
+@pytest.mark.parametrize("cin,cout,k,pad,sp", [
+    (96, 256, (3, 3, 3), (0, 0, 0), (6, 20, 12)),      # N-split, unfolded widths
+    (40, 80, (1, 3, 3), (0, 1, 1), (5, 18, 12)),       # N-split + fold
+])
+def test_narrow_n_tiles(path, cin, cout, k, pad, sp):
+    """VXB_PATH_TC_N128/_N64 (deep levels): the fmaps are split over N tiles."""
+    import torch
+    D, K = _dev()
+    rng = np.random.default_rng(cout + path)
+    x = rng.uniform(-1, 1, (1, cin) + sp).astype(np.float32)
+    w = (rng.standard_normal((cout, cin) + k) * np.sqrt(2.0 / (cin * np.prod(k)))).astype(np.float32)
+    b = (rng.standard_normal(cout) * 0.1).astype(np.float32)
+    osp = tuple(s + 2 * p - kk + 1 for s, p, kk in zip(sp, pad, k))
+    pk = K.pack_conv(w, b, path=path)
+    assert pk.path == path
+    out = D.empty_blocked(1, cout, osp)
+    K.conv3d(D.to_device_blocked(x), pk, out, pad=pad, fused_act=("relu", 1.0))
+    torch.cuda.synchronize()
+    mx, l2 = R.normalized_error(D.to_host_standard(out), _ref_bf16(x, w, b, pad, "relu"))
+    assert mx < BF16_TOL and l2 < 3e-3, (mx, l2)
+
+
 def test_tc_conv_fp32_output_and_batch2():
     rng = np.random.default_rng(7)
     x = rng.uniform(-1, 1, (2, 16, 4, 18, 10)).astype(np.float32)

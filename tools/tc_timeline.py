@@ -56,6 +56,10 @@ for case in os.environ.get("CASES", "8:333,16:333,32:333").split(","):
         d = (rel[:, :, b] - rel[:, :, a])[used & (rel[:, :, b] >= 0)]
         print("  %-24s mean %7.2f us  p50 %7.2f  max %7.2f" % (nm, d.mean() / 1e3,
                                                               np.median(d) / 1e3, d.max() / 1e3))
+    if int(os.environ.get("VXB_TC_DBGMODE", "0")) & 1024:
+        g0 = (rel[:, :, 7] - rel[:, :, 1])[used & (rel[:, :, 7] >= 0)]
+        g1 = (rel[:, :, 2] - rel[:, :, 7])[used & (rel[:, :, 7] >= 0)]
+        print("  group0 %.2f us  group1 %.2f us" % (g0.mean() / 1e3, g1.mean() / 1e3))
     d = (rel[:, 1:, 1] - rel[:, :-1, 2])[used[:, 1:]]
     print("  MMA idle between tiles  mean %7.2f us" % (d.mean() / 1e3))
     last = np.array([rel[i, ntile[i] - 1, 4] for i in range(len(ctas))])
