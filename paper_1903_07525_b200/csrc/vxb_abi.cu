@@ -639,9 +639,11 @@ int vxb_conv_select_shape(int cin, int cout, const int k[3], const int stride[3]
   const int sms = std::max(1, device_sms_or(148));
   const long long sp = static_cast<long long>(ceil_div(out_xyz[0], 4)) *
                        ceil_div(out_xyz[1], TILE_Y) * ceil_div(out_xyz[2], TILE_Z);
-  if (sp * L.n_tiles >= sms || L.npad <= 64) return path;
+  // (fmap counts <= 128 keep their single N tile: there the CTA-pair MMA of
+  // the unsplit layer beats twice the tiles at half the width, measured)
+  if (sp * L.n_tiles >= sms || L.npad <= 128) return path;
   const TcLayout L128 = tc_layout(cin, 0, cout, k, true, 128);
-  if (sp * L128.n_tiles >= sms || L.npad <= 128) return VXB_PATH_TC_N128;
+  if (sp * L128.n_tiles >= sms) return VXB_PATH_TC_N128;
   return VXB_PATH_TC_N64;
 }
 

@@ -305,7 +305,8 @@ class PlanRunner:
                 if "segments" in info:
                     a, b, oa, ob = info["segments"]
                     pk = K.pack_conv(kern, w.tensor(st.name, ROLE_BIAS), stride=stride,
-                                     base_scale=scale, cin_split=a.dims[1], device=dev)
+                                     base_scale=scale, cin_split=a.dims[1],
+                                     out_shape=tuple(info["out"].dims[2:]), device=dev)
                     calls.append(lambda a=a.dt, b=b.dt, pk=pk, out=out, base=base, oa=oa, ob=ob,
                                  act=st.fused_act: K.conv3d(a, pk, out, base=base, fused_act=act,
                                                             x2=b, off=oa, off2=ob))
