@@ -597,7 +597,6 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
           mbar_wait(&a_full[a_st], a_ph);
           tc_fence_after();
           if (g == 0 && lane == 0) dbg_mark(p, it, 1);
-          if (g == 1 && lane == 0 && (p.dbg_mode & 1024)) dbg_mark(p, it, 7);
           const bool pair = gi.nch == 2;
           const int tz_n = pair ? p.kz : (p.kz + 1) >> 1;
           const uint32_t dz_step = pair ? 1u : 2u;
