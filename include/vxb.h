@@ -58,6 +58,8 @@ extern "C" {
 #define VXB_PATH_TC_UNFOLDED 3 /* tensor-core path without slice-axis tap folding */
 #define VXB_PATH_TC_N128 4     /* tensor-core path, output fmaps in N tiles of <= 128 */
 #define VXB_PATH_TC_N64 5      /* tensor-core path, output fmaps in N tiles of <= 64 */
+#define VXB_PATH_TC_N32 6      /* tensor-core path, output fmaps in N tiles of <= 32 */
+#define VXB_PATH_TC_N16 7      /* tensor-core path, output fmaps in N tiles of 16 */
 
 /* pooling modes: ops.py:63-86 */
 #define VXB_POOL_MAX 0

@@ -24,7 +24,9 @@ PATH_DIRECT = 2
 PATH_TC_UNFOLDED = 3
 PATH_TC_N128 = 4
 PATH_TC_N64 = 5
-TC_PATHS = (PATH_TC, PATH_TC_UNFOLDED, PATH_TC_N128, PATH_TC_N64)
+PATH_TC_N32 = 6
+PATH_TC_N16 = 7
+TC_PATHS = (PATH_TC, PATH_TC_UNFOLDED, PATH_TC_N128, PATH_TC_N64, PATH_TC_N32, PATH_TC_N16)
 POOL_CODE = {"max": 0, "avg": 1}
 ELT_CODE = {"add": 0, "mul": 1, "div": 2}
 

@@ -110,12 +110,18 @@ static int tc_fold_axis(int nt, const int k[3]) {
 }
 
 static bool is_tc(int path) {
-  return path == VXB_PATH_TC || path == VXB_PATH_TC_UNFOLDED || path == VXB_PATH_TC_N128 ||
-         path == VXB_PATH_TC_N64;
+  return path == VXB_PATH_TC || path == VXB_PATH_TC_UNFOLDED ||
+         (path >= VXB_PATH_TC_N128 && path <= VXB_PATH_TC_N16);
 }
 static bool path_folds(int path) { return path != VXB_PATH_TC_UNFOLDED; }
 static int path_nt_cap(int path) {
-  return path == VXB_PATH_TC_N64 ? 64 : path == VXB_PATH_TC_N128 ? 128 : 256;
+  switch (path) {
+    case VXB_PATH_TC_N128: return 128;
+    case VXB_PATH_TC_N64: return 64;
+    case VXB_PATH_TC_N32: return 32;
+    case VXB_PATH_TC_N16: return 16;
+    default: return 256;
+  }
 }
 
 static TcLayout tc_layout(int cin0, int cin1, int cout, const int k[3], bool allow_fold = true,
@@ -632,19 +638,41 @@ int vxb_conv_select_shape(int cin, int cout, const int k[3], const int stride[3]
   const TcLayout L = tc_layout(cin, 0, cout, k);
   if (L.fold == 2 && out_xyz[0] > 0 && ceil_div(out_xyz[0], TILE_Y) * TILE_Y * 4 > out_xyz[0] * 5)
     return VXB_PATH_TC_UNFOLDED;   // > 25% of the 16-row x tiles would be padding
-  // Too few output tiles for the SMs (deep levels: 9^3 .. 16^3 voxels with
-  // 256-512 fmaps)?  Narrower N tiles multiply the tile count; every N tile
-  // re-reads the (small, L2-resident) input.  Spatial tiles are estimated
-  // at 4 slices per tile.
+  // Too few output tiles for the SMs even at one slice per tile (deep U-net
+  // levels: 9^3 .. 24^3 voxels, or 18x12x12 in config 5)?  Narrower N tiles
+  // multiply the tile count and shorten each tile's MMAs; every N tile
+  // re-reads the (small, L2-resident) input.  Take the widest N tile that
+  // gives one tile per SM.
   const int sms = std::max(1, device_sms_or(148));
-  const long long sp = static_cast<long long>(ceil_div(out_xyz[0], 4)) *
-                       ceil_div(out_xyz[1], TILE_Y) * ceil_div(out_xyz[2], TILE_Z);
-  // (fmap counts <= 128 keep their single N tile: there the CTA-pair MMA of
-  // the unsplit layer beats twice the tiles at half the width, measured)
-  if (sp * L.n_tiles >= sms || L.npad <= 128) return path;
-  const TcLayout L128 = tc_layout(cin, 0, cout, k, true, 128);
-  if (sp * L128.n_tiles >= sms) return VXB_PATH_TC_N128;
-  return VXB_PATH_TC_N64;
+  const long long sp = static_cast<long long>(out_xyz[0]) * ceil_div(out_xyz[1], TILE_Y) *
+                       ceil_div(out_xyz[2], TILE_Z);
+  if (sp * L.n_tiles >= sms) return path;
+  if (L.npad > 128) {
+    // wide layers (CTA-pair MMAs when unsplit): the widest split that fills
+    // the SMs, else 64-wide tiles
+    const TcLayout L128 = tc_layout(cin, 0, cout, k, true, 128);
+    if (sp * L128.n_tiles >= sms) return VXB_PATH_TC_N128;
+    return VXB_PATH_TC_N64;
+  }
+  if (L.npad > 96) return path;   // 96-128 fmaps: one CTA-pair N tile beats two halves (measured)
+  // narrow (folded, single-CTA) layers: waves x per-MMA cycles of the N tile
+  // (SS-mode floor max(45.5, 32 + N/4), N = 3 nt when folded); the K work of
+  // a tile does not depend on the split
+  static const int kCaps[4] = {256, 64, 32, 16};
+  static const int kPaths[4] = {VXB_PATH_TC, VXB_PATH_TC_N64, VXB_PATH_TC_N32, VXB_PATH_TC_N16};
+  int best = path;
+  double best_cost = 1e30;
+  for (int i = 0; i < 4; ++i) {
+    const TcLayout Li = tc_layout(cin, 0, cout, k, true, kCaps[i]);
+    const long long waves = (sp * Li.n_tiles + sms - 1) / sms;
+    const int n = Li.fold ? 3 * Li.nt : Li.nt;
+    const double cost = static_cast<double>(waves) * std::max(45.5, 32.0 + n / 4.0);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = kPaths[i];
+    }
+  }
+  return best;
 }
 
 static size_t direct_bytes(int cin, int cout, const int k[3]) {
