@@ -434,6 +434,23 @@ class PlanRunner:
         cs.wait_stream(self.stream)
         return dict(self._out_std)
 
+    def run_on_stream(self, inputs):
+        """``run_device`` without ordering against the caller's current
+        stream: the input copies and the graph replay are enqueued on
+        ``self.stream`` only (the caller orders producers and consumers of
+        the tensors, e.g. several runners pipelining patches)."""
+        torch = _torch()
+        inputs = self._normalize(inputs)
+        if self._graph is None and self.use_graph:
+            self._replay()                   # first call: capture (synchronous once)
+            self.stream.synchronize()
+        with torch.cuda.stream(self.stream):
+            for name, t in inputs.items():
+                if t.data_ptr() != self._in_std[name].data_ptr():
+                    self._in_std[name].copy_(t, non_blocking=True)
+        self._replay()
+        return dict(self._out_std)
+
     def run(self, inputs, out=None) -> dict:
         """Reference-compatible forward (executor.py:168-198): host in, host out.
         Inputs go host -> pinned staging -> HBM and outputs the reverse, in

@@ -141,16 +141,25 @@ def partition(n_tiles: int, parts: int, rank: int) -> range:
 
 
 class DeviceTiler:
-    """Runs a block of tiles of one grid on one GPU, volume slab resident."""
+    """Runs a block of tiles of one grid on one GPU, volume slab resident.
 
-    def __init__(self, plan, grid: TileGrid, device, backend=None):
+    ``streams`` PlanRunners (each with its own graph, buffers and CUDA
+    stream) take the tiles round robin, so consecutive patches overlap: the
+    deep U-net levels of one patch leave most SMs idle (few output tiles),
+    and the next patch's large levels fill them.  Patches are independent,
+    so this changes no result."""
+
+    def __init__(self, plan, grid: TileGrid, device, backend=None, streams=None):
         import torch
         from .runner import PlanRunner
         self.torch = torch
         self.grid = grid
         self.device = torch.device(device)
+        n = int(streams if streams is not None else os.environ.get("VOXPLAN_STREAMS", "2"))
         with torch.cuda.device(self.device):
-            self.runner = PlanRunner(plan, backend=backend, device=self.device)
+            self.runners = [PlanRunner(plan, backend=backend, device=self.device)
+                            for _ in range(max(1, n))]
+        self.runner = self.runners[0]
         self.in_name = plan.inputs[0][0]
 
     def slab_bounds(self, tiles):
@@ -173,20 +182,31 @@ class DeviceTiler:
                                         dtype=torch.float32, device=self.device)
         self.lo, self.olo = lo, olo
 
+    @property
+    def launches_per_tile(self) -> int:
+        return self.runner.launches
+
     def run(self, tiles):
-        """Run the tiles from the resident slab into the resident output slab."""
+        """Run the tiles from the resident slab into the resident output slab
+        (enqueued; the current stream is made to wait for all of them)."""
         torch = self.torch
         pin = self.grid.patch_in
         with torch.cuda.device(self.device):
-            for t in tiles:
+            cur = torch.cuda.current_stream(self.device)
+            for r in self.runners:
+                r.stream.wait_stream(cur)       # slab / output slab are ready
+            for i, t in enumerate(tiles):
+                r = self.runners[i % len(self.runners)]
                 src = tuple(slice(a - l, a - l + p) for a, l, p in zip(t.in_lo, self.lo, pin))
-                outs = self.runner.run_device({self.in_name: self.slab[(slice(None), slice(None))
-                                                                       + src]})
-                res = next(iter(outs.values()))
                 dst = tuple(slice(o - l, o - l + (b - a))
                             for o, l, a, b in zip(t.out_lo, self.olo, t.keep_lo, t.keep_hi))
-                self.out_slab[(slice(None), slice(None)) + dst].copy_(
-                    res[(slice(None), slice(None)) + t.local_window])
+                res = next(iter(r.run_on_stream(
+                    {self.in_name: self.slab[(slice(None), slice(None)) + src]}).values()))
+                with torch.cuda.stream(r.stream):
+                    self.out_slab[(slice(None), slice(None)) + dst].copy_(
+                        res[(slice(None), slice(None)) + t.local_window])
+            for r in self.runners:
+                cur.wait_stream(r.stream)
 
     def download(self, out: np.ndarray, tiles):
         """Copy the output slab into the host volume (one D2H)."""
