@@ -167,6 +167,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ void dbg_mark(const TcParams &p, int it, int slot) {
   if (p.dbg && it < 64) p.dbg[(static_cast<size_t>(blockIdx.x) * 64 + it) * 8 + slot] = gtimer();
 }
+// SM clock counter next to a timestamp (effective clock = dclock / dns)
+__device__ __forceinline__ void dbg_clock(const TcParams &p, int it, int slot) {
+  if (p.dbg && it > 0 && it < 64)
+    p.dbg[(static_cast<size_t>(blockIdx.x) * 64 + it) * 8 + slot] = clock64();
+}
 
 constexpr int EPI_WARPS = 12;
 constexpr int TC_THREADS = 96 + 32 * EPI_WARPS;   // A-TMA, MMA, B-TMA + epilogue
@@ -596,7 +601,10 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
           GroupInfo gi = group_info(p, g);
           mbar_wait(&a_full[a_st], a_ph);
           tc_fence_after();
-          if (g == 0 && lane == 0) dbg_mark(p, it, 1);
+          if (g == 0 && lane == 0) {
+            dbg_mark(p, it, 1);
+            dbg_clock(p, it, 5);
+          }
           const bool pair = gi.nch == 2;
           const int tz_n = pair ? p.kz : (p.kz + 1) >> 1;
           const uint32_t dz_step = pair ? 1u : 2u;
@@ -644,7 +652,10 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
           umma_commit_pair_elect(&t_full[acc], pair_mask);
         else
           umma_commit_elect(&t_full[acc]);
-        if (lane == 0) dbg_mark(p, it, 2);
+        if (lane == 0) {
+          dbg_mark(p, it, 2);
+          dbg_clock(p, it, 6);
+        }
       }
     }
     __syncwarp();

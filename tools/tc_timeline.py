@@ -14,16 +14,20 @@ spatial = tuple(int(v) for v in os.environ.get("SPATIAL", "32,128,128").split(",
 _act = os.environ.get("ACT", "elu")
 FA = None if _act == "none" else (_act, 1.0)
 for case in os.environ.get("CASES", "8:333,16:333,32:333").split(","):
-    c, ks = case.split(":")
-    c = int(c)
+    parts = case.split(":")             # C:KKK or CIN:COUT:KKK
+    c = int(parts[0])
+    cout = int(parts[1]) if len(parts) == 3 else c
+    ks = parts[-1]
     k = tuple(int(v) for v in ks)
     x = D.empty_blocked(1, c, spatial)
     x.t.copy_(torch.randn(x.t.shape, device=dev).to(torch.bfloat16))
+    if os.environ.get("ZERO_INPUT"):
+        x.t.zero_()
     if os.environ.get("F32IN"):
         x = D.standard(torch.randn((1, c) + spatial, device=dev))
-    out = D.empty_blocked(1, c, spatial)
-    w = (np.random.default_rng(0).standard_normal((c, c) + k) * 0.05).astype(np.float32)
-    pk = K.pack_conv(w, np.zeros(c, np.float32))
+    out = D.empty_blocked(1, cout, spatial)
+    w = (np.random.default_rng(0).standard_normal((cout, c) + k) * 0.05).astype(np.float32)
+    pk = K.pack_conv(w, np.zeros(cout, np.float32))
     pad = tuple(v // 2 for v in k)
     for _ in range(3):
         K.conv3d(x, pk, out, pad=pad, fused_act=FA)
@@ -60,6 +64,11 @@ for case in os.environ.get("CASES", "8:333,16:333,32:333").split(","):
         g0 = (rel[:, :, 7] - rel[:, :, 1])[used & (rel[:, :, 7] >= 0)]
         g1 = (rel[:, :, 2] - rel[:, :, 7])[used & (rel[:, :, 7] >= 0)]
         print("  group0 %.2f us  group1 %.2f us" % (g0.mean() / 1e3, g1.mean() / 1e3))
+    ck = (t[:, 1:, 6] - t[:, 1:, 5]).astype(np.float64)
+    ns = (t[:, 1:, 2] - t[:, 1:, 1]).astype(np.float64)
+    ok = used[:, 1:] & (t[:, 1:, 5] > 0) & (t[:, 1:, 6] > 0) & (ns > 0)
+    if ok.any():
+        print("  SM clock during MMA issue: %.0f MHz" % (ck[ok].sum() / ns[ok].sum() * 1e3))
     d = (rel[:, 1:, 1] - rel[:, :-1, 2])[used[:, 1:]]
     print("  MMA idle between tiles  mean %7.2f us" % (d.mean() / 1e3))
     last = np.array([rel[i, ntile[i] - 1, 4] for i in range(len(ctas))])
