@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define VXB_ABI_VERSION 1
+#define VXB_ABI_VERSION 2
 
 /* element types */
 #define VXB_BF16 0
@@ -64,6 +64,11 @@ extern "C" {
 /* pooling modes: ops.py:63-86 */
 #define VXB_POOL_MAX 0
 #define VXB_POOL_AVG 1
+/* pooling fused into a conv epilogue (vxb_conv_desc.pool_mode): max over
+ * 1x2x2 windows with stride 1x2x2 of the stored (rounded) conv output, the
+ * following MaxPool step of the reference (ops.py:63-86) */
+#define VXB_POOL_FUSED_NONE 0
+#define VXB_POOL_FUSED_MAX122 1
 
 /* eltwise ops: ops.py:50-60 */
 #define VXB_ELT_ADD 0
@@ -114,7 +119,9 @@ typedef struct vxb_conv_desc {
   int32_t act;
   float alpha;
   int32_t path;            /* 0 = auto (vxb_conv_select) */
-  int32_t reserved[7];
+  int32_t pool_mode;       /* VXB_POOL_FUSED_*: also write the pooled output (ops.pool fused) */
+  int32_t reserved[6];
+  vxb_tensor pool_out;     /* pooled view, logical (n, cout, ox, oy/2, oz/2) */
 } vxb_conv_desc;
 
 /* Transposed convolution (kernels_py.deconv3d, kernels_py.py:162-196):

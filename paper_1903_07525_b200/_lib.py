@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 VXB_BF16 = 0
 VXB_F32 = 1
 ACT_CODE = {None: 0, "relu": 1, "elu": 2, "sigmoid": 3}   # kernels_cy.py:19
+ABI_VERSION = 2      # include/vxb.h VXB_ABI_VERSION
 PATH_TC = 1
 PATH_DIRECT = 2
 PATH_TC_UNFOLDED = 3
@@ -60,7 +61,9 @@ class VxbConvDesc(ctypes.Structure):
         ("act", c_int32),
         ("alpha", c_float),
         ("path", c_int32),
-        ("reserved", c_int32 * 7),
+        ("pool_mode", c_int32),
+        ("reserved", c_int32 * 6),
+        ("pool_out", VxbTensor),
     ]
 
 
@@ -134,6 +137,9 @@ def lib():
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
+        if handle.vxb_abi_version() != ABI_VERSION:
+            raise ExecutionError("%s has ABI %d, this package needs %d (rebuild it)"
+                                 % (LIB_PATH, handle.vxb_abi_version(), ABI_VERSION))
         _LIB = handle
     return _LIB
 

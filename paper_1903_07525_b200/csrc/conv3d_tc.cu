@@ -339,7 +339,7 @@ __device__ __forceinline__ void mma_group_fold(
   }
 }
 
-template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN>
+template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN, bool POOL = false>
 __global__ void __launch_bounds__(tc_threads(F32IN), 1)
     conv3d_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -798,7 +798,8 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
       auto finish = [&](int item, const uint32_t (&rv)[16], const float (&bv)[16]) {
         const int s = item / col_items, cc = (item % col_items) << 4;
         const int x = sc0 + s;
-        if (!(yz_ok && x < slim)) return;
+        const bool valid = yz_ok && x < slim;
+        if (!POOL && !valid) return;   // (fused pooling needs every lane at its shuffles)
         const long long obase = orow + x * ov.s[sl_dim];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -838,7 +839,39 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
             for (int i = 0; i < 8; ++i)
               if (i >= nvalid) r[i] = 0.f;
           }
-          if (FASTOUT) {
+          if (POOL) {
+            // bf16 blocked output with a fused MaxPool 1x2x2 / 1x2x2
+            // (ops.py:63-86) of the stored values: rows (y, z) (y, z+1)
+            // (y+1, z) (y+1, z+1) sit in lanes l, l+1, l+8, l+9; the max runs
+            // on the packed bf16 pairs (NaN-propagating, like np.maximum)
+            uint32_t w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(r[2 * i], r[2 * i + 1]);
+              w[i] = *reinterpret_cast<uint32_t *>(&h2);
+            }
+            if (valid)
+              *reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(ov.data) + obase +
+                                         (c0 >> 3) * ov.s[1]) = make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint32_t t1 = __shfl_down_sync(0xffffffffu, w[i], 1);
+              const uint32_t t2 = __shfl_down_sync(0xffffffffu, w[i], 8);
+              const uint32_t t3 = __shfl_down_sync(0xffffffffu, w[i], 9);
+              __nv_bfloat162 m = *reinterpret_cast<const __nv_bfloat162 *>(&w[i]);
+              m = __hmax2_nan(m, *reinterpret_cast<const __nv_bfloat162 *>(&t1));
+              m = __hmax2_nan(m, *reinterpret_cast<const __nv_bfloat162 *>(&t2));
+              m = __hmax2_nan(m, *reinterpret_cast<const __nv_bfloat162 *>(&t3));
+              w[i] = *reinterpret_cast<uint32_t *>(&m);
+            }
+            const int py = rc >> 1, pz = z >> 1;
+            if ((lane & 9) == 0 && x < slim && !tc.dummy && py < p.pool_oy && pz < p.pool_oz) {
+              const EpiView &pv = p.pool_out;
+              *reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(pv.data) + tc.b * pv.s[0] +
+                                         x * pv.s[2] + py * pv.s[3] + pz * pv.s[4] +
+                                         (c0 >> 3) * pv.s[1]) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          } else if (FASTOUT) {
             if (ov.blocked) {
               store8_bf16_blocked(ov, obase + (c0 >> 3) * ov.s[1], r);
             } else {
@@ -848,9 +881,10 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
               for (int i = 0; i < 8; ++i)
                 if (i < nvalid) op[i * ov.s[1]] = r[i];
             }
-          } else
+          } else {
             store8(ov, obase + (ov.blocked ? (c0 >> 3) * ov.s[1] : c0 * ov.s[1]), ov.blocked,
                    nvalid, r);
+          }
         }
       };
 
@@ -914,10 +948,10 @@ size_t tc_smem_bytes(const TcParams &p) {
          16;
 }
 
-template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN = false>
+template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN = false, bool POOL = false>
 static int launch_variant(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t stream,
                           size_t smem) {
-  auto kern = conv3d_tc_kernel<ACT, FASTOUT, BASE, PAIR, F32IN>;
+  auto kern = conv3d_tc_kernel<ACT, FASTOUT, BASE, PAIR, F32IN, POOL>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -968,6 +1002,14 @@ static int launch_act(const TcParams &p, const TcMaps &maps, int grid, cudaStrea
                       size_t smem) {
   const bool fast = (p.out.dtype == VXB_BF16 && p.out.blocked) ||
                     (p.out.dtype == VXB_F32 && !p.out.blocked);
+  if (p.pool) {
+    if (PAIR || p.f32in || p.out.dtype != VXB_BF16 || !p.out.blocked ||
+        p.pool_out.dtype != VXB_BF16 || !p.pool_out.blocked)
+      return set_error(VXB_EUNSUPPORTED,
+                       "fused pooling: bf16 blocked output and pool view, single-CTA tiles");
+    // activation at run time: two instances (with / without residual) only
+    return launch_variant<-1, true, BASE, false, false, true>(p, maps, grid, s, smem);
+  }
   if (p.f32in) {
     if (BASE || !fast)
       return set_error(VXB_EUNSUPPORTED,

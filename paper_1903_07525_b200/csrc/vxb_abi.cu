@@ -404,6 +404,8 @@ struct TcLaunch {
   float alpha;
   bool allow_fold;
   int nt_cap;
+  int pool;
+  EpiView pool_out;
 };
 
 static int run_tc(const TcLaunch &a, cudaStream_t stream) {
@@ -465,7 +467,7 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   // per-instruction cost (~48 cycles at N <= 32), so one M = 256 instruction
   // serving two SMs halves the MMA time per tile.
   const int pair_env = env_int("VXB_TC_PAIR", 1);
-  p.pair = (!p.fold && spatial >= 2 && L.nt % 16 == 0 && L.nt / 8 <= 256 &&
+  p.pair = (!p.fold && !a.pool && spatial >= 2 && L.nt % 16 == 0 && L.nt / 8 <= 256 &&
             ((a.out.dtype == VXB_BF16 && a.out.blocked) || (a.out.dtype == VXB_F32 && !a.out.blocked)) &&
             (pair_env == 1 || (pair_env == 2 && !c.resident))) ? 1 : 0;
   p.cluster = p.pair || (!c.resident && env_int("VXB_TC_CLUSTER", 1) == 2 && spatial >= 2) ? 2 : 1;
@@ -574,6 +576,14 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   p.out = a.out;
   p.base = a.base;
   p.has_base = a.has_base;
+  if (a.pool) {
+    // the epilogue pools over (y, z) row pairs of one 128-row slice
+    if (slice_y) return set_error(VXB_EUNSUPPORTED, "fused pooling needs x-sliced tiles");
+    p.pool = 1;
+    p.pool_out = a.pool_out;
+    p.pool_oy = a.oy / 2;
+    p.pool_oz = a.oz / 2;
+  }
   for (int r = 0; r < MAX_REPS; ++r) {
     p.out_rep_off[r] = a.out_rep_off[r];
     p.base_rep_off[r] = a.base_rep_off[r];
@@ -781,8 +791,21 @@ int vxb_conv3d(const vxb_conv_desc *d, void *stream) {
     a.scale = additive ? d->base_scale : nullptr;
     a.act = d->act;
     a.alpha = d->alpha;
+    if (d->pool_mode == VXB_POOL_FUSED_MAX122) {
+      if ((rc = check_view(&d->pool_out, "conv3d.pool_out"))) return rc;
+      const vxb_tensor &pv = d->pool_out;
+      if (pv.n != d->out.n || pv.c != d->cout || pv.x != d->out.x || pv.y != d->out.y / 2 ||
+          pv.z != d->out.z / 2)
+        return set_error(VXB_EINVAL, "conv3d.pool_out must be (n, cout, x, y/2, z/2)");
+      a.pool = 1;
+      a.pool_out = to_epi(pv);
+    } else if (d->pool_mode != VXB_POOL_FUSED_NONE) {
+      return set_error(VXB_EINVAL, "conv3d: bad pool_mode %d", d->pool_mode);
+    }
     return run_tc(a, s);
   }
+  if (d->pool_mode != VXB_POOL_FUSED_NONE)
+    return set_error(VXB_EUNSUPPORTED, "fused pooling needs the tensor-core conv path");
   if (two) return set_error(VXB_EUNSUPPORTED, "direct conv path takes a single input");
   DirectParams p;
   memset(&p, 0, sizeof(p));

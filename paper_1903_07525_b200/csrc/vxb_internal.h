@@ -71,6 +71,9 @@ struct TcParams {
   int cout, act;
   float alpha;
   int has_base;
+  // fused 1x2x2 max pool of the stored output (VXB_POOL_FUSED_MAX122)
+  int pool, pool_oy, pool_oz;
+  EpiView pool_out;
   unsigned long long *dbg;     // optional per-tile phase timestamps (VXB_TC_DEBUG)
   int dbg_mode;                // VXB_TC_DBGMODE (timing experiments, wrong results): 1 no
                                // epilogue, 2 no A loads, 4 no B loads, 8 no MMAs (resident B),

@@ -89,8 +89,10 @@ def pack_conv(kernel, bias, *, stride=(1, 1, 1), base_scale=None, cin_split=None
 
 def conv3d(x: DTensor, pk: PackedConv, out: DTensor, *, pad=(0, 0, 0), base: DTensor = None,
            fused_act=None, x2: DTensor = None, off=(0, 0, 0), off2=(0, 0, 0),
-           stream=None) -> None:
-    """Fused conv step (kernels_cy.conv3d -> _kernels.conv3d, _kernels.pyx:44-179)."""
+           pool_out: DTensor = None, stream=None) -> None:
+    """Fused conv step (kernels_cy.conv3d -> _kernels.conv3d, _kernels.pyx:44-179).
+    ``pool_out`` (n, cout, x, y/2, z/2): also write the 1x2x2 max pool of the
+    stored output (the following MaxPool step, ops.py:63-86, fused)."""
     L = _lib.lib()
     d = _lib.VxbConvDesc()
     d.in0 = x.vxb()
@@ -108,6 +110,9 @@ def conv3d(x: DTensor, pk: PackedConv, out: DTensor, *, pad=(0, 0, 0), base: DTe
     d.pad = _lib.i3(pad)
     d.act, d.alpha = _act(fused_act)
     d.path = pk.path
+    if pool_out is not None:
+        d.pool_mode = 1
+        d.pool_out = pool_out.vxb()
     _lib.check(L.vxb_conv3d(ctypes.byref(d), stream or current_stream_handle()), "vxb_conv3d")
 
 

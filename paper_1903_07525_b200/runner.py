@@ -68,7 +68,7 @@ class PlanRunner:
     """Executes one ExecutionPlan on one B200; reusable, deterministic."""
 
     def __init__(self, plan, backend=None, *, device=None, use_graph=True, fuse_concat=True,
-                 fuse_input=False):
+                 fuse_pool=False, fuse_input=False):
         torch = _torch()
         from .backend import resolve_device_backend
         self.backend = resolve_device_backend(backend)
@@ -80,6 +80,7 @@ class PlanRunner:
         self.use_graph = use_graph
         self.precision = self.backend.precision
         self.fuse_concat = fuse_concat and self.precision == "bf16"
+        self.fuse_pool = fuse_pool and self.precision == "bf16"
         self.fuse_input = fuse_input
         self._conv_path = _lib.PATH_DIRECT if self.precision == "fp32" else 0
         self.stream = torch.cuda.Stream(device=self.device)
@@ -153,6 +154,8 @@ class PlanRunner:
             self._out_values[name] = v
         if self.fuse_concat:
             self._fuse_mergecrop()
+        if self.fuse_pool:
+            self._fuse_maxpool()
 
     def _fuse_mergecrop(self):
         """Zero-copy MergeCrop: a conv whose only input is a MergeCrop of two
@@ -184,6 +187,41 @@ class PlanRunner:
         if drop:
             self._ops = [op for i, op in enumerate(self._ops) if i not in drop]
 
+    def _fuse_maxpool(self):
+        """MaxPool 1x2x2 / 1x2x2 (ops.py:63-86) folded into the epilogue of the
+        tensor-core conv that produces its input: the conv
+        writes its output and the pooled output; the pool step disappears.
+        Only x-sliced conv tiles (3-deep x kernels, 1x1x1) pool over their
+        (y, z) rows.  Opt-in (fuse_pool=True): measured on config 5 the extra
+        epilogue work (shuffles + second store) costs as much as the HBM-bound
+        pool kernel it replaces, and the pool kernel overlaps via PDL."""
+        producers = {id(info["out"]): i for i, (_, _, info) in enumerate(self._ops)}
+        drop = set()
+        for i, (kind, st, info) in enumerate(self._ops):
+            if kind is not LayerKind.POOLING:
+                continue
+            prm = st.params
+            if (prm.get("mode") != "max" or tuple(prm["window"]) != (1, 2, 2)
+                    or tuple(prm["stride"]) != (1, 2, 2)):
+                continue
+            src = info["ins"][0]
+            j = producers.get(id(src))
+            if j is None:
+                continue
+            ckind, cst, cinfo = self._ops[j]
+            if ckind is not LayerKind.CONVOLUTION or "pool_out" in cinfo:
+                continue
+            if tuple(cst.params.get("stride", (1, 1, 1))) != (1, 1, 1):
+                continue
+            k = tuple(int(v) for v in self.plan.weights.tensor(cst.name, ROLE_KERNEL).shape[2:])
+            if not (k[0] == 3 or k == (1, 1, 1)):
+                continue
+            cinfo["pool_out"] = info["out"]
+            src.readers -= 1
+            drop.add(i)
+        if drop:
+            self._ops = [op for i, op in enumerate(self._ops) if i not in drop]
+
     # ------------------------------------------------------------ storage
     def _reads(self, info):
         if "segments" in info:
@@ -206,6 +244,8 @@ class PlanRunner:
             for r in self._reads(info):
                 last[id(r)] = i
             last.setdefault(id(info["out"]), i)
+            if "pool_out" in info:
+                last.setdefault(id(info["pool_out"]), i)
         for v in self._out_values.values():
             last[id(v)] = len(self._ops)
         slots, free = [], []
@@ -230,6 +270,9 @@ class PlanRunner:
         for i, (_, _, info) in enumerate(self._ops):
             info["out"].slot = grab(info["out"])
             live.append(info["out"])
+            if "pool_out" in info:
+                info["pool_out"].slot = grab(info["pool_out"])
+                live.append(info["pool_out"])
             keep = []
             for v in live:
                 if last.get(id(v), -1) <= i:
@@ -307,9 +350,11 @@ class PlanRunner:
                     pk = K.pack_conv(kern, w.tensor(st.name, ROLE_BIAS), stride=stride,
                                      base_scale=scale, cin_split=a.dims[1],
                                      out_shape=tuple(info["out"].dims[2:]), device=dev)
+                    pool = info["pool_out"].dt if "pool_out" in info else None
                     calls.append(lambda a=a.dt, b=b.dt, pk=pk, out=out, base=base, oa=oa, ob=ob,
-                                 act=st.fused_act: K.conv3d(a, pk, out, base=base, fused_act=act,
-                                                            x2=b, off=oa, off2=ob))
+                                 act=st.fused_act, pool=pool:
+                                 K.conv3d(a, pk, out, base=base, fused_act=act, x2=b, off=oa,
+                                          off2=ob, pool_out=pool))
                 else:
                     pk = K.pack_conv(kern, w.tensor(st.name, ROLE_BIAS), stride=stride,
                                      base_scale=scale, path=self._conv_path,
@@ -317,9 +362,11 @@ class PlanRunner:
                     x = fused_in.get(id(info), info["x"].dt)
                     if id(info) in fused_in and pk.path not in _lib.TC_PATHS:
                         raise ExecutionError("fused fp32 input needs the tensor-core conv path")
+                    pool = info["pool_out"].dt if "pool_out" in info else None
                     calls.append(lambda x=x, pk=pk, out=out, base=base,
-                                 pad=info["pad"], act=st.fused_act:
-                                 K.conv3d(x, pk, out, pad=pad, base=base, fused_act=act))
+                                 pad=info["pad"], act=st.fused_act, pool=pool:
+                                 K.conv3d(x, pk, out, pad=pad, base=base, fused_act=act,
+                                          pool_out=pool))
             elif kind is LayerKind.DECONVOLUTION:
                 base = info["base"].dt if "base" in info else None
                 scale = st.base_scale if st.additive else None

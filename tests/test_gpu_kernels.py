@@ -222,6 +222,36 @@ def test_narrow_n_tiles(path, cin, cout, k, pad, sp):
     assert mx < BF16_TOL and l2 < 3e-3, (mx, l2)
 
 
+@pytest.mark.parametrize("cin,cout,k,pad,sp,base", [
+    (28, 28, (3, 3, 3), (1, 1, 1), (5, 24, 16), True),     # folded, residual
+    (13, 20, (3, 3, 3), (1, 1, 1), (4, 19, 13), False),    # odd y/z: floor, ragged chunk
+    (64, 80, (1, 1, 1), (0, 0, 0), (3, 16, 8), False),
+    (128, 128, (3, 3, 3), (1, 1, 1), (4, 16, 16), False),  # CTA pair
+])
+def test_fused_maxpool_bit_identical(cin, cout, k, pad, sp, base):
+    """Conv with its 1x2x2 MaxPool fused into the epilogue equals conv then
+    pool_kernel, bit for bit."""
+    import torch
+    D, K = _dev()
+    rng = np.random.default_rng(cin + cout)
+    x = rng.uniform(-1, 1, (1, cin) + sp).astype(np.float32)
+    w = (rng.standard_normal((cout, cin) + k) * 0.2).astype(np.float32)
+    b = (rng.standard_normal(cout) * 0.1).astype(np.float32)
+    osp = tuple(s + 2 * p - kk + 1 for s, p, kk in zip(sp, pad, k))
+    bd = D.to_device_blocked(rng.uniform(-1, 1, (1, cout) + osp).astype(np.float32)) if base else None
+    pk = K.pack_conv(w, b, base_scale=np.ones(cout, np.float32) if base else None)
+    xd = D.to_device_blocked(x)
+    out1, out2 = D.empty_blocked(1, cout, osp), D.empty_blocked(1, cout, osp)
+    psp = (osp[0], osp[1] // 2, osp[2] // 2)
+    p1, p2 = D.empty_blocked(1, cout, psp), D.empty_blocked(1, cout, psp)
+    K.conv3d(xd, pk, out1, pad=pad, base=bd, fused_act=("elu", 1.0), pool_out=p1)
+    K.conv3d(xd, pk, out2, pad=pad, base=bd, fused_act=("elu", 1.0))
+    K.pool3d(out2, p2, (1, 2, 2), (1, 2, 2), "max")
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(D.to_host_standard(out1), D.to_host_standard(out2))
+    assert torch.equal(p1.t, p2.t)
+
+
 def test_tc_conv_fp32_output_and_batch2():
     rng = np.random.default_rng(7)
     x = rng.uniform(-1, 1, (2, 16, 4, 18, 10)).astype(np.float32)

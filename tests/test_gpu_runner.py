@@ -142,6 +142,17 @@ def test_fused_input_pack_is_bit_identical(cfg):
     np.testing.assert_array_equal(a, plain.run(x)[n])
 
 
+def test_fused_maxpool_runner_bit_identical():
+    """Config 5's 1x2x2 pools fold into the preceding conv epilogues."""
+    spec, store = _small(5)
+    plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
+    x = C.make_input(spec, 4, 0.0, 1.0)
+    fused, plain = P.PlanRunner(plan, fuse_pool=True), P.PlanRunner(plan)
+    assert fused.launches < plain.launches
+    (n, a), = fused.run(x).items()
+    np.testing.assert_array_equal(a, plain.run(x)[n])
+
+
 def test_run_tiled_equals_manual_assembly():
     """test_acceptance.py:343-362 / test_tiling.py:111-142: tiled output equals
     the manual assembly of per-patch runs, exactly (each tile is a

@@ -13,7 +13,7 @@ cfg = int(os.environ.get("CFG", "4"))
 dev = torch.device("cuda", 0)
 spec, store = {1: C.config1, 3: C.config3, 4: C.config4, 5: C.config5}[cfg]()
 plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
-r = P.PlanRunner(plan, device=dev)
+r = P.PlanRunner(plan, device=dev, fuse_pool=os.environ.get("FUSEPOOL", "1") == "1")
 lo, hi = C.input_range(cfg)
 x = C.make_input(spec, 0, lo, hi)
 bufs = r.input_buffers()
