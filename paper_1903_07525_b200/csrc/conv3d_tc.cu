@@ -87,9 +87,24 @@ __device__ __forceinline__ TileCoord decode_tile(const TcParams &p, int t) {
 // Fast ELU for the tensor-core epilogue: alpha*(2^(v*log2 e) - 1), selected
 // branch-free (a data-dependent branch per value tripled the epilogue time).
 // Absolute error ~1e-7 near 0, far below the bf16 operand rounding.
+// 2^x in one MUFU.EX2 (ftz: inputs below -126 give 0, i.e. e^v - 1 = -1 for
+// v < -87, exact to fp32); __expf adds range-scaling FMULs around the MUFU
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float fast_elu(float v, float alpha) {
-  const float m = fmaf(alpha, __expf(v), -alpha);
+  const float m = fmaf(alpha, ex2_ftz(v * 1.4426950408889634f), -alpha);
   return v > 0.f ? v : m;
+}
+__device__ __forceinline__ float fast_sigmoid(float v) {
+  return rcp_ftz(1.f + ex2_ftz(v * -1.4426950408889634f));
 }
 __device__ __forceinline__ float apply_act(float v, int act, float alpha) {
   if (act == VXB_ACT_RELU) return v > 0.f ? v : 0.f;
@@ -729,6 +744,13 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
     const int ra = row >> 3, zz = row & 7;    // row-axis offset (y, or x with slice_y), z
     const int col_items = p.nt >> 4;
     const int items = p.bx * col_items;
+    // item -> (slice, column offset) without a division: items < 2^16, so
+    // a multiply-high by ceil(2^32 / col_items) is exact
+    const uint32_t cmagic = col_items > 1 ? 0xffffffffu / col_items + 1u : 0u;
+    auto split_item = [&](int item, int &s, int &cc) {
+      s = col_items > 1 ? static_cast<int>(__umulhi(static_cast<uint32_t>(item), cmagic)) : item;
+      cc = (item - s * col_items) << 4;
+    };
     const EpiView &ov = p.out;
     const EpiView &bvw = p.base;
     const int act = ACT >= 0 ? ACT : p.act;
@@ -748,14 +770,16 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * acc_cols;
 
       auto taddr_of = [&](int item) {
-        const int s = item / col_items, cc = (item % col_items) << 4;
+        int s, cc;
+        split_item(item, s, cc);
         return tbase + s * p.nt + cc;
       };
       // residual operand: bf16 blocked bases are prefetched raw two items
       // ahead (the first ones before the accumulator is even ready); other
       // layouts are read at use
       auto base_issue = [&](int item, uint4 (&d)[2]) {
-        const int s = item / col_items, cc = (item % col_items) << 4;
+        int s, cc;
+        split_item(item, s, cc);
         const int x = sc0 + s;
         const bool ok = yz_ok && x < slim;
         const __nv_bfloat16 *bp = static_cast<const __nv_bfloat16 *>(bvw.data) + brow +
@@ -781,7 +805,8 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
           }
           return;
         }
-        const int s = item / col_items, cc = (item % col_items) << 4;
+        int s, cc;
+        split_item(item, s, cc);
         const int x = sc0 + s;
         const bool ok = yz_ok && x < slim;
 #pragma unroll
@@ -796,10 +821,10 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
         }
       };
       auto finish = [&](int item, const uint32_t (&rv)[16], const float (&bv)[16]) {
-        const int s = item / col_items, cc = (item % col_items) << 4;
+        int s, cc;
+        split_item(item, s, cc);
         const int x = sc0 + s;
-        const bool valid = yz_ok && x < slim;
-        if (!POOL && !valid) return;   // (fused pooling needs every lane at its shuffles)
+        const bool valid = yz_ok && x < slim;   // stores only; all lanes run the math
         const long long obase = orow + x * ov.s[sl_dim];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -828,13 +853,17 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
               for (int i = 0; i < 8; ++i) r[i] = fast_elu(r[i], p.alpha);
             } else if (act == VXB_ACT_SIGMOID) {
 #pragma unroll
-              for (int i = 0; i < 8; ++i) r[i] = __fdividef(1.f, 1.f + __expf(-r[i]));
+              for (int i = 0; i < 8; ++i) r[i] = fast_sigmoid(r[i]);
             }
           } else {
 #pragma unroll
             for (int i = 0; i < 8; ++i) r[i] = apply_act(r[i], act, p.alpha);
           }
-          if (nvalid < 8) {
+          // tail lanes (ops.py:18-23 zero_tail): with zero-padded weights,
+          // bias 0 and zero base lanes they already hold act(0) = 0 for
+          // none / relu / elu; only sigmoid (and the runtime-act variant)
+          // must clear them
+          if ((ACT < 0 || ACT == VXB_ACT_SIGMOID || !FASTOUT) && nvalid < 8) {
 #pragma unroll
             for (int i = 0; i < 8; ++i)
               if (i >= nvalid) r[i] = 0.f;
@@ -873,15 +902,15 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
             }
           } else if (FASTOUT) {
             if (ov.blocked) {
-              store8_bf16_blocked(ov, obase + (c0 >> 3) * ov.s[1], r);
+              if (valid) store8_bf16_blocked(ov, obase + (c0 >> 3) * ov.s[1], r);
             } else {
               // fused unpack: fp32 NCDHW network output written directly
               float *op = static_cast<float *>(ov.data) + obase + c0 * ov.s[1];
 #pragma unroll
               for (int i = 0; i < 8; ++i)
-                if (i < nvalid) op[i * ov.s[1]] = r[i];
+                if (valid && i < nvalid) op[i * ov.s[1]] = r[i];
             }
-          } else {
+          } else if (valid) {
             store8(ov, obase + (ov.blocked ? (c0 >> 3) * ov.s[1] : c0 * ov.s[1]), ov.blocked,
                    nvalid, r);
           }
