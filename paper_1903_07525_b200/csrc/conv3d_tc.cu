@@ -903,12 +903,16 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
           } else if (FASTOUT) {
             if (ov.blocked) {
               if (valid) store8_bf16_blocked(ov, obase + (c0 >> 3) * ov.s[1], r);
-            } else {
+            } else if (valid) {
               // fused unpack: fp32 NCDHW network output written directly
+              // (one pointer walked across the channel planes)
               float *op = static_cast<float *>(ov.data) + obase + c0 * ov.s[1];
+              const long long cs = ov.s[1];
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                if (valid && i < nvalid) op[i * ov.s[1]] = r[i];
+              for (int i = 0; i < 8; ++i) {
+                if (i < nvalid) *op = r[i];
+                op += cs;
+              }
             }
           } else if (valid) {
             store8(ov, obase + (ov.blocked ? (c0 >> 3) * ov.s[1] : c0 * ov.s[1]), ov.blocked,
