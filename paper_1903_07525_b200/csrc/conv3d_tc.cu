@@ -306,45 +306,52 @@ __device__ __forceinline__ void mma_group_fold(
     }
     tc_fence_after();
     uint32_t b_lo = desc_lo(b_base0 + b_st * b_stage_bytes, 128u);
-    for (int i = 0; i < n; ++i) {
-      const uint32_t a_lo = a_lo0 + off;
-      if (first) {
-#pragma unroll
-        for (int x = 0; x < BX; ++x)
-          umma_bf16_lohi_elect(d_base + x * nt, a_lo + x * slice_inc, a_hi, b_lo + 2 * blk_inc,
-                               b_hi, id1, 0u);
-#pragma unroll
-        for (int j = 1; j < BX + 2; ++j) {
-          const int dlo = j - BX + 1 > 1 ? j - BX + 1 : 1, dhi = j < 2 ? j : 2;
-          const uint32_t idn = dhi - dlo == 0 ? id1 : id2;
-          umma_bf16_lohi_elect(d_base + (j - dhi) * nt, a_lo + j * slice_inc, a_hi,
-                               b_lo + (2 - dhi) * blk_inc, b_hi, idn, 1u);
-        }
-        first = 0;
-      } else {
-        // interior input slices first: they share B (all 3 blocks) and the
-        // instruction descriptor, so consecutive MMAs only move A and D
-#pragma unroll
-        for (int j = 2; j < BX; ++j)
-          umma_bf16_lohi_elect(d_base + (j - 2) * nt, a_lo + j * slice_inc, a_hi, b_lo, b_hi, id3,
-                               1u);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int j = e < 2 ? e : BX + e - 2;
-          if (j >= 2 && j < BX) continue;   // BX < 2: the edges are everything
-          if (e >= 2 && j < 2) continue;
-          const int dlo = j - BX + 1 > 0 ? j - BX + 1 : 0, dhi = j < 2 ? j : 2;
-          const uint32_t idn = dhi - dlo == 0 ? id1 : (dhi - dlo == 1 ? id2 : id3);
-          umma_bf16_lohi_elect(d_base + (j - dhi) * nt, a_lo + j * slice_inc, a_hi,
-                               b_lo + (2 - dhi) * blk_inc, b_hi, idn, 1u);
-        }
-      }
+    auto advance = [&]() {
       b_lo += slab_inc;
       off += dz_step;
       if (++tz == tz_n) {
         tz = 0;
         off += a_wrap;
       }
+    };
+    int i = 0;
+    if (first) {
+      // the tile's first K step (peeled so the steady loop has no branch)
+      const uint32_t a_lo = a_lo0 + off;
+#pragma unroll
+      for (int x = 0; x < BX; ++x)
+        umma_bf16_lohi_elect(d_base + x * nt, a_lo + x * slice_inc, a_hi, b_lo + 2 * blk_inc,
+                             b_hi, id1, 0u);
+#pragma unroll
+      for (int j = 1; j < BX + 2; ++j) {
+        const int dlo = j - BX + 1 > 1 ? j - BX + 1 : 1, dhi = j < 2 ? j : 2;
+        const uint32_t idn = dhi - dlo == 0 ? id1 : id2;
+        umma_bf16_lohi_elect(d_base + (j - dhi) * nt, a_lo + j * slice_inc, a_hi,
+                             b_lo + (2 - dhi) * blk_inc, b_hi, idn, 1u);
+      }
+      first = 0;
+      advance();
+      i = 1;
+    }
+    for (; i < n; ++i) {
+      const uint32_t a_lo = a_lo0 + off;
+      // interior input slices first: they share B (all 3 blocks) and the
+      // instruction descriptor, so consecutive MMAs only move A and D
+#pragma unroll
+      for (int j = 2; j < BX; ++j)
+        umma_bf16_lohi_elect(d_base + (j - 2) * nt, a_lo + j * slice_inc, a_hi, b_lo, b_hi, id3,
+                             1u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = e < 2 ? e : BX + e - 2;
+        if (j >= 2 && j < BX) continue;   // BX < 2: the edges are everything
+        if (e >= 2 && j < 2) continue;
+        const int dlo = j - BX + 1 > 0 ? j - BX + 1 : 0, dhi = j < 2 ? j : 2;
+        const uint32_t idn = dhi - dlo == 0 ? id1 : (dhi - dlo == 1 ? id2 : id3);
+        umma_bf16_lohi_elect(d_base + (j - dhi) * nt, a_lo + j * slice_inc, a_hi,
+                             b_lo + (2 - dhi) * blk_inc, b_hi, idn, 1u);
+      }
+      advance();
     }
     if (!cx.resident) umma_commit_elect(&cx.b_empty[b_st]);
     if (++b_st == cx.nb_stages) {
