@@ -318,16 +318,17 @@ __device__ __forceinline__ void mma_group_fold(
     if (first) {
       // the tile's first K step (peeled so the steady loop has no branch)
       const uint32_t a_lo = a_lo0 + off;
+      if constexpr (BX >= 2) {
+        umma_fold_first<BX>(d_base, a_lo, a_hi, b_lo, b_hi, id1, id2, id3, nt, slice_inc, blk_inc);
+      } else {
+        umma_bf16_lohi_elect(d_base, a_lo, a_hi, b_lo + 2 * blk_inc, b_hi, id1, 0u);
 #pragma unroll
-      for (int x = 0; x < BX; ++x)
-        umma_bf16_lohi_elect(d_base + x * nt, a_lo + x * slice_inc, a_hi, b_lo + 2 * blk_inc,
-                             b_hi, id1, 0u);
-#pragma unroll
-      for (int j = 1; j < BX + 2; ++j) {
-        const int dlo = j - BX + 1 > 1 ? j - BX + 1 : 1, dhi = j < 2 ? j : 2;
-        const uint32_t idn = dhi - dlo == 0 ? id1 : id2;
-        umma_bf16_lohi_elect(d_base + (j - dhi) * nt, a_lo + j * slice_inc, a_hi,
-                             b_lo + (2 - dhi) * blk_inc, b_hi, idn, 1u);
+        for (int j = 1; j < BX + 2; ++j) {
+          const int dlo = j - BX + 1 > 1 ? j - BX + 1 : 1, dhi = j < 2 ? j : 2;
+          const uint32_t idn = dhi - dlo == 0 ? id1 : id2;
+          umma_bf16_lohi_elect(d_base + (j - dhi) * nt, a_lo + j * slice_inc, a_hi,
+                               b_lo + (2 - dhi) * blk_inc, b_hi, idn, 1u);
+        }
       }
       first = 0;
       advance();
@@ -335,25 +336,88 @@ __device__ __forceinline__ void mma_group_fold(
     }
     for (; i < n; ++i) {
       const uint32_t a_lo = a_lo0 + off;
-      // interior input slices first: they share B (all 3 blocks) and the
-      // instruction descriptor, so consecutive MMAs only move A and D
+      if constexpr (BX >= 2) {
+        // one asm block per step: interior slices (shared B, N = 3nt), then
+        // the tail and head slices
+        umma_fold_step<BX>(d_base, a_lo, a_hi, b_lo, b_hi, id1, id2, id3, nt, slice_inc, blk_inc);
+      } else {
+        // BX = 1: input slices 0..2 each feed the single output slice
 #pragma unroll
-      for (int j = 2; j < BX; ++j)
-        umma_bf16_lohi_elect(d_base + (j - 2) * nt, a_lo + j * slice_inc, a_hi, b_lo, b_hi, id3,
-                             1u);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int j = e < 2 ? e : BX + e - 2;
-        if (j >= 2 && j < BX) continue;   // BX < 2: the edges are everything
-        if (e >= 2 && j < 2) continue;
-        const int dlo = j - BX + 1 > 0 ? j - BX + 1 : 0, dhi = j < 2 ? j : 2;
-        const uint32_t idn = dhi - dlo == 0 ? id1 : (dhi - dlo == 1 ? id2 : id3);
-        umma_bf16_lohi_elect(d_base + (j - dhi) * nt, a_lo + j * slice_inc, a_hi,
-                             b_lo + (2 - dhi) * blk_inc, b_hi, idn, 1u);
+        for (int j = 0; j < 3; ++j)
+          umma_bf16_lohi_elect(d_base, a_lo + j * slice_inc, a_hi, b_lo + (2 - j) * blk_inc, b_hi,
+                               id1, 1u);
       }
       advance();
     }
     if (!cx.resident) umma_commit_elect(&cx.b_empty[b_st]);
+    if (++b_st == cx.nb_stages) {
+      b_st = 0;
+      b_ph ^= 1;
+    }
+  }
+}
+
+// Folded CTA-pair variant (cta_group::2, M = 256: each MMA covers the same
+// slice of both CTAs' tiles, B split by rows between the pair).  Every MMA
+// runs at N = 3nt from the start of the slab, so the split is the same for
+// all of them: input slice j writes slices j-2..j (D = d_base + j*nt, where
+// d_base is the column of slice -2) and the edge slices' extra terms land in
+// the scratch columns around the tile.  At N <= 96 an M = 256 instruction
+// costs what an M = 128 one does (~45-50 cycles, tools/umma_align.cu), so the
+// pair halves the MMA time per tile of the low-fmap convs.  The first step of
+// a tile writes input slices j = 0, 3, 6, .. with accumulate off (their
+// 3-slice ranges tile the accumulator without overlap), then j = 1 mod 3 and
+// j = 2 mod 3 accumulate on top.
+template <int BX>
+__device__ __forceinline__ void mma_group_fold_pair(
+    const uint32_t a_lo0, const uint32_t a_hi, const uint32_t b_base0, const uint32_t b_stage_bytes,
+    const uint32_t b_hi, const uint32_t slab_inc, const uint32_t slice_inc, const uint32_t d_base,
+    const uint32_t nt, const uint32_t id3, const int steps, const int tz_n, const uint32_t dz_step,
+    const uint32_t a_wrap, const MmaCtx &cx, int &b_st, int &b_ph, uint32_t &first) {
+  constexpr int C = BX + 2;
+  int tz = 0;
+  uint32_t off = 0;
+  for (int s0 = 0; s0 < steps; s0 += cx.bsteps) {
+    const int n = min(cx.bsteps, steps - s0);
+    if (cx.resident) {
+      if (cx.first_tile_iter) mbar_wait(&cx.b_full[b_st], 0);
+    } else {
+      mbar_wait(&cx.b_full[b_st], b_ph);
+    }
+    tc_fence_after();
+    uint32_t b_lo = desc_lo(b_base0 + b_st * b_stage_bytes, 128u);
+    auto advance = [&]() {
+      b_lo += slab_inc;
+      off += dz_step;
+      if (++tz == tz_n) {
+        tz = 0;
+        off += a_wrap;
+      }
+    };
+    int i = 0;
+    if (first) {
+      const uint32_t a_lo = a_lo0 + off;
+      umma_pair_run<(C + 2) / 3>(d_base, a_lo, a_hi, b_lo, b_hi, id3, 0u, 3 * nt, 3 * slice_inc);
+      umma_pair_run<(C + 1) / 3>(d_base + nt, a_lo + slice_inc, a_hi, b_lo, b_hi, id3, 1u, 3 * nt,
+                                 3 * slice_inc);
+      umma_pair_run<C / 3>(d_base + 2 * nt, a_lo + 2 * slice_inc, a_hi, b_lo, b_hi, id3, 1u,
+                           3 * nt, 3 * slice_inc);
+      first = 0;
+      advance();
+      i = 1;
+    }
+    for (; i < n; ++i) {
+      // j = 0, 3, .. then 1, 4, .. then 2, 5, ..: consecutive MMAs never
+      // touch the same accumulator slices (no read-after-write stalls)
+      const uint32_t a_lo = a_lo0 + off;
+      umma_pair_run<(C + 2) / 3>(d_base, a_lo, a_hi, b_lo, b_hi, id3, 1u, 3 * nt, 3 * slice_inc);
+      umma_pair_run<(C + 1) / 3>(d_base + nt, a_lo + slice_inc, a_hi, b_lo, b_hi, id3, 1u, 3 * nt,
+                                 3 * slice_inc);
+      umma_pair_run<C / 3>(d_base + 2 * nt, a_lo + 2 * slice_inc, a_hi, b_lo, b_hi, id3, 1u,
+                           3 * nt, 3 * slice_inc);
+      advance();
+    }
+    if (!cx.resident) umma_commit_pair_elect(&cx.b_empty[b_st], 0x3);
     if (++b_st == cx.nb_stages) {
       b_st = 0;
       b_ph ^= 1;
@@ -393,9 +457,8 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
   const int first_tile = (blockIdx.x / p.cluster) * p.cluster + crank;
   const int tile_step = gridDim.x;
   const uint16_t pair_mask = 0x3;
-  const int acc_cols = p.bx * p.nt;
-  uint32_t tmem_cols = 32;
-  while (tmem_cols < static_cast<uint32_t>(acc_cols * p.acc_stages)) tmem_cols <<= 1;
+  const int acc_stride = p.acc_stride;
+  const uint32_t tmem_cols = static_cast<uint32_t>(p.tmem_cols);
 
   // one-time setup by all threads: guard bytes behind every chunk array
   // (read with zero weight by odd-chunk z-pair steps) and the per-fmap
@@ -591,6 +654,7 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
       const uint32_t a_hi = desc_hi(p.a_sbo);
       const uint32_t blk_inc = (p.nt * SLAB_ROW_BYTES) >> 4;
       // (debug mode 16: every folded MMA at N = nt, to time the issue loop)
+      const uint32_t idp = idesc_bf16(256, p.fold ? 3 * p.nt : p.nt);   // folded pairs
       const uint32_t id1 = idesc_bf16(128, p.nt),
                      id2 = (p.dbg_mode & 16) ? id1 : idesc_bf16(128, 2 * p.nt),
                      id3 = (p.dbg_mode & 16) ? id1 : idesc_bf16(128, p.fold ? 3 * p.nt : p.nt);
@@ -615,7 +679,7 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
         const int acc = it % p.acc_stages;
         mbar_wait(&t_empty[acc], ((it / p.acc_stages) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d_base = tmem_base + acc * acc_cols;
+        const uint32_t d_base = tmem_base + acc * acc_stride;
         uint32_t accumulate = 0, first = 1;
         if (p.resident) b_st = 0;
         cx.first_tile_iter = it == 0;
@@ -639,6 +703,20 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
                        b_ph, accumulate)
           if ((p.dbg_mode & 8) && p.resident) {
             // debug: no MMAs (epilogue-only timing; resident weights only)
+          } else if (PAIR && p.fold) {
+            const uint32_t a_wrap = fold_stride - tz_n * dz_step;
+#define VXB_FOLDP(BXV)                                                                       \
+  mma_group_fold_pair<BXV>(a_lo0, a_hi, b_base0, p.b_stage_bytes, b_hi, b_inc, slice_inc, d_base, \
+                           p.nt, idp, gi.steps, tz_n, dz_step, a_wrap, cx, b_st, b_ph, first)
+            switch (p.bx) {
+              case 1: VXB_FOLDP(1); break;
+              case 2: VXB_FOLDP(2); break;
+              case 3: VXB_FOLDP(3); break;
+              case 4: VXB_FOLDP(4); break;
+              case 6: VXB_FOLDP(6); break;
+              default: VXB_FOLDP(8); break;
+            }
+#undef VXB_FOLDP
           } else if (!PAIR && p.fold) {
             const uint32_t a_wrap = fold_stride - tz_n * dz_step;
 #define VXB_FOLD(BXV)                                                                           \
@@ -774,7 +852,8 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
           p.out_rep_off[tc.rep] + tc.b * ov.s[0] + rc * ov.s[ra_dim] + z * ov.s[4];
       const long long brow =
           p.base_rep_off[tc.rep] + tc.b * bvw.s[0] + rc * bvw.s[ra_dim] + z * bvw.s[4];
-      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * acc_cols;
+      const uint32_t tbase =
+          tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * acc_stride + p.slice0_col;
 
       auto taddr_of = [&](int item) {
         int s, cc;

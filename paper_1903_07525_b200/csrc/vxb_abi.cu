@@ -229,14 +229,23 @@ static void tc_pack(const TcLayout &L, int cin0, int cin1, int cout, const int k
 struct TcConfig {
   int bx, acc, na, nb, bsteps, resident, chunk_bytes, chunk_stride, chunk_slots, a_stage,
       b_stage;
+  int pair;   // cta_group::2 tiles (each CTA holds half of every B stage)
   size_t smem;
 };
 
 // other_tiles: tiles over the non-slice axes x batch x N tiles x reps.
 static const int kTileOverhead = 3;
 
+// TMEM columns of the accumulator stages (see TcParams::acc_stride)
+static int tc_tmem_cols(int bx, int nt, int acc, bool fold_pair) {
+  return fold_pair ? acc * (bx + 2) * nt + 2 * nt : acc * bx * nt;
+}
+
+// can_pair: the conv may run as CTA pairs (pair_mode 1: always, 2: only with
+// streamed weights); fold_pair: it is a folded conv that pairs (TMEM layout)
 static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, long long other_tiles,
-                        int sms, int reps, int reserved, TcConfig &c) {
+                        int sms, int reps, int reserved, bool can_pair, int pair_mode,
+                        bool fold_pair, TcConfig &c) {
   // room for bias/scale/barriers, plus the fp32-input staging ring if any
   const int budget = 227 * 1024 - 6144 - reserved;
   c.acc = env_int("VXB_TC_ACC", 2);
@@ -252,17 +261,21 @@ static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, lon
   c.bx = 1;
   long long best = -1;
   for (int cand : {8, 6, 4, 3, 2, 1}) {
-    if (cand > bx_cap || cand * L.nt * c.acc > 512) continue;
+    if (cand > bx_cap || tc_tmem_cols(cand, L.nt, c.acc, fold_pair) > 512) continue;
     if (!L.fold && (cand & (cand - 1))) continue;   // unfolded tiles: 1, 2, 4, 8
-    const long long tiles = static_cast<long long>(ceil_div(slice_extent, cand)) * other_tiles;
+    long long tiles = static_cast<long long>(ceil_div(slice_extent, cand)) * other_tiles;
+    if (fold_pair) tiles = (tiles + 1) / 2 * 2;
     const long long waves = (tiles + sms - 1) / sms;
-    const long long cost = waves * ((L.fold ? cand + 2 : cand) + kTileOverhead);
+    // a folded pair issues bx + 2 MMAs per step for two tiles (one per SM)
+    const long long cost = fold_pair ? waves * ((cand + 2) + 2 * kTileOverhead)
+                                     : waves * 2 * ((L.fold ? cand + 2 : cand) + kTileOverhead);
     if (best < 0 || cost < best) {
       best = cost;
       c.bx = cand;
     }
   }
-  if (c.bx * L.nt * c.acc > 512) return set_error(VXB_EUNSUPPORTED, "TMEM overflow");
+  if (tc_tmem_cols(c.bx, L.nt, c.acc, fold_pair) > 512)
+    return set_error(VXB_EUNSUPPORTED, "TMEM overflow");
   bool any_pair = false;
   int max_steps = 1;
   for (const TcGroup &g : L.groups) {
@@ -293,16 +306,34 @@ static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, lon
         c.nb = nbs;
       }
     }
+    c.pair = can_pair && (pair_mode == 1 || !c.resident);
+    if (c.resident) c.b_stage = c.b_stage / (c.pair ? 2 : 1);
     if (!c.resident) {
-      c.bsteps = std::max(1, std::min(max_steps, 32768 / slab));
-      c.b_stage = c.bsteps * slab;
-      int room = (budget - c.na * c.a_stage) / c.b_stage;
-      c.nb = std::min(4, room);
+      // Streamed weights: as few B stages per K group as fit (ring >= 2).
+      // Every stage boundary costs the MMA warp a b_full wait + commit round
+      // trip (~300 cycles measured: C128 1x3x3 stages of 8+1 steps 147 us,
+      // one 9-step stage 127 us; C64 3x3x3 one 9-step stage 88.6 us, 5+4
+      // steps 92.4 us; deeper rings of smaller stages measured no better).
+      const int half = c.pair ? 2 : 1;
+      const int env_bs = env_int("VXB_TC_BSTEPS", 0);
+      const int avail = budget - c.na * c.a_stage;
+      const int min_ring = env_int("VXB_TC_BRING", 2);
+      c.bsteps = 0;
+      for (int parts = 1; parts <= max_steps && !env_bs; ++parts) {
+        const int bs = ceil_div(max_steps, parts);
+        const int stage = bs * slab / half;
+        if (stage <= 64 * 1024 && avail / stage >= min_ring) {
+          c.bsteps = bs;
+          break;
+        }
+      }
+      if (!c.bsteps) c.bsteps = std::max(1, std::min(max_steps, env_bs ? env_bs : 32768 / slab));
+      c.b_stage = c.bsteps * slab / half;
+      c.nb = std::min(c.pair ? 6 : 4, avail / c.b_stage);
       while (c.nb < 2 && c.bsteps > 1) {
         c.bsteps = (c.bsteps + 1) / 2;
-        c.b_stage = c.bsteps * slab;
-        room = (budget - c.na * c.a_stage) / c.b_stage;
-        c.nb = std::min(4, room);
+        c.b_stage = c.bsteps * slab / half;
+        c.nb = std::min(c.pair ? 6 : 4, avail / c.b_stage);
       }
     }
     if (c.nb >= 1 && (c.resident || c.nb >= 2)) break;
@@ -438,7 +469,31 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
     hzb = round_up(zshift + TILE_Z + a.k[2] - 1, 4);
     stg_bytes = kStgBudget;
   }
-  int rc = tc_configure(L, a.k, slice_y ? a.oy : a.ox, other_tiles, sms, a.reps, stg_bytes, c);
+  // folded low-fmap convs run as CTA pairs when N = 3nt <= 96: an M = 256
+  // MMA then costs what an M = 128 one does (tools/umma_align.cu)
+  const int pair_env = env_int("VXB_TC_PAIR", 1);
+  const bool out_ok = (a.out.dtype == VXB_BF16 && a.out.blocked) ||
+                      (a.out.dtype == VXB_F32 && !a.out.blocked);
+  // Measured (config-2 shapes, 128x256x256): 3x3x3 at nt = 16 gains 14 %;
+  // 1x3x3 and nt = 32 lose (their tiles are bound by the A-halo stream, and
+  // the pair couples two CTAs' loads), so only that case pairs by default.
+  const int fp_env = env_int("VXB_TC_FOLDPAIR", 1);
+  const bool fold_pair = L.fold && L.nt <= 32 && pair_env == 1 && fp_env &&
+                         (fp_env == 2 || (L.fold == 1 && L.nt == 16)) && !a.pool && !f32in &&
+                         out_ok;
+  // weight-streaming convs run as CTA pairs sharing one B stream
+  // (cta_group::2: M = 256 per MMA, each CTA ingests and reads only half of
+  // every weight slab, halving the smem traffic that bounds high-fmap
+  // convs); resident-weight unfolded convs pair too (one M = 256 instruction
+  // serves two SMs at the per-instruction floor).  A pair needs >= 2 tiles:
+  // checked at the widest tile, so any tile width chosen below has them.
+  const long long spatial_min =
+      static_cast<long long>(ceil_div(slice_y ? a.oy : a.ox, 8)) *
+      ceil_div(slice_y ? a.ox : a.oy, TILE_Y) * ceil_div(a.oz, TILE_Z) * a.nb;
+  const bool can_pair = (!L.fold || fold_pair) && !a.pool && spatial_min >= 2 && L.nt % 16 == 0 &&
+                        L.nt / 8 <= 256 && out_ok && (pair_env == 1 || pair_env == 2);
+  int rc = tc_configure(L, a.k, slice_y ? a.oy : a.ox, other_tiles, sms, a.reps, stg_bytes,
+                        can_pair, pair_env, fold_pair, c);
   if (rc) return rc;
   TcParams p;
   memset(&p, 0, sizeof(p));
@@ -460,24 +515,8 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   p.n_tiles = L.n_tiles;
   p.reps = a.reps;
   const long long spatial = static_cast<long long>(p.tiles_x) * p.tiles_y * p.tiles_z * p.nb;
-  // weight-streaming convs run as CTA pairs sharing one multicast B stream
-  // cta_group::2 pairs: M = 256 per MMA, each CTA ingests and reads only half
-  // of every weight slab (halves the smem traffic that bounds high-fmap convs)
-  // Resident-weight (low-fmap) convs pair up too: their MMAs are bound by a
-  // per-instruction cost (~48 cycles at N <= 32), so one M = 256 instruction
-  // serving two SMs halves the MMA time per tile.
-  const int pair_env = env_int("VXB_TC_PAIR", 1);
-  p.pair = (!p.fold && !a.pool && spatial >= 2 && L.nt % 16 == 0 && L.nt / 8 <= 256 &&
-            ((a.out.dtype == VXB_BF16 && a.out.blocked) || (a.out.dtype == VXB_F32 && !a.out.blocked)) &&
-            (pair_env == 1 || (pair_env == 2 && !c.resident))) ? 1 : 0;
+  p.pair = c.pair;
   p.cluster = p.pair || (!c.resident && env_int("VXB_TC_CLUSTER", 1) == 2 && spatial >= 2) ? 2 : 1;
-  if (p.pair) {
-    c.b_stage /= 2;
-    if (!c.resident) {
-      const int budget = 227 * 1024 - 6144;
-      c.nb = std::max(2, std::min(6, (budget - c.na * c.a_stage) / c.b_stage));
-    }
-  }
   const long long spatial_pad = (spatial + p.cluster - 1) / p.cluster * p.cluster;
   long long total = spatial_pad * p.n_tiles * p.reps;
   if (total > 0x7fffffffLL) return set_error(VXB_EUNSUPPORTED, "too many tiles");
@@ -557,11 +596,13 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   if (p.pair) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return set_error(VXB_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    const cuuint64_t slab = static_cast<cuuint64_t>(L.nt) * SLAB_ROW_BYTES;
-    cuuint64_t dims[4] = {128, static_cast<cuuint64_t>(L.nt / 8), 2,
-                          static_cast<cuuint64_t>(a.reps) * L.n_tiles * L.steps};
+    const cuuint64_t slab = static_cast<cuuint64_t>(L.slab);
+    // a slab is R rows (nt, or 3nt folded) x 32 B; each CTA takes R/2 rows =
+    // R/8 units of 128 B
+    const cuuint64_t units = static_cast<cuuint64_t>(L.slab) / SLAB_ROW_BYTES / 8;
+    cuuint64_t dims[4] = {128, units, 2, static_cast<cuuint64_t>(a.reps) * L.n_tiles * L.steps};
     cuuint64_t strides[3] = {128, slab / 2, slab};
-    cuuint32_t box[4] = {128, static_cast<cuuint32_t>(L.nt / 8), 1,
+    cuuint32_t box[4] = {128, static_cast<cuuint32_t>(units), 1,
                          static_cast<cuuint32_t>(c.bsteps)};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = enc(&maps.w, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(a.w), dims,
@@ -600,12 +641,26 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
     cudaMemsetAsync(g_dbg, 0, kDbgBytes, stream);
     p.dbg = static_cast<unsigned long long *>(g_dbg);
   }
+  const bool fp = p.pair && p.fold;
+  p.acc_stride = (fp ? p.bx + 2 : p.bx) * p.nt;
+  p.slice0_col = fp ? 2 * p.nt : 0;
+  const int cols = tc_tmem_cols(p.bx, p.nt, p.acc_stages, fp);
+  p.tmem_cols = 32;
+  while (p.tmem_cols < cols) p.tmem_cols <<= 1;
+  if (p.tmem_cols > 512) return set_error(VXB_EUNSUPPORTED, "TMEM overflow (%d columns)", cols);
   c.smem = tc_smem_bytes(p);
   if (c.smem > 227 * 1024) return set_error(VXB_EUNSUPPORTED, "conv needs %zu B smem", c.smem);
   // persistent: one CTA per SM (480 threads x ~100 registers leaves no room
   // for a second one, and the smem ring is sized for the whole SM)
   int grid = static_cast<int>(std::min<long long>(total, static_cast<long long>(sms)));
   grid = std::max(p.cluster, grid / p.cluster * p.cluster);
+  if (env_int("VXB_PRINT", 0))
+    fprintf(stderr,
+            "conv3d_tc cin %d+%d cout %d k %d%d%d out %dx%dx%d: nt %d ntiles %d fold %d pair %d "
+            "bx %d acc %d na %d nb %d bsteps %d resident %d tiles %d grid %d smem %zu tmem %d\n",
+            a.cin0, a.cin1, a.cout, a.k[0], a.k[1], a.k[2], a.ox, a.oy, a.oz, p.nt, p.n_tiles,
+            L.fold, p.pair, p.bx, p.acc_stages, p.na, p.nb_stages, p.bsteps, p.resident,
+            p.total_tiles, grid, c.smem, p.tmem_cols);
   return launch_conv3d_tc(p, maps, grid, stream);
 }
 

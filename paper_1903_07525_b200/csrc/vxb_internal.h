@@ -47,6 +47,12 @@ struct TcParams {
   int f32in_zshift;            // box z start is rounded down to 16 B: rows start this far in
   int f32in_xb;                // halo x-slices per staging box
   int acc_stages;              // TMEM accumulator stages
+  // TMEM columns between accumulator stages, and from a stage's base to its
+  // slice 0.  Folded CTA-pair tiles (fold && pair) issue every MMA at N = 3nt,
+  // so input slices 0 and bx+1 also write the two slices before / after the
+  // tile: stage s spans slices -2..bx+1 and neighbouring stages share their
+  // 2nt-column scratch band (stride (bx+2)nt, slice 0 at +2nt).
+  int acc_stride, slice0_col, tmem_cols;
   int kx, ky, kz;
   int hx, hy, hz;              // halo tile extents
   int pad[3];

@@ -377,6 +377,119 @@ __device__ __forceinline__ void umma_bf16_pair_lohi_elect(uint32_t d, uint32_t a
       "r"(a_inc)                                                                          \
       : "memory"
 
+// Folded K step (slice-axis taps stacked in N, see mma_group_fold) as ONE asm
+// block: a single elect, every descriptor derived in-block from the step's
+// base words.  Operands: %0 d_base, %1 a_lo, %2 a_hi, %3 b_lo, %4 b_hi,
+// %5..%7 idesc for N = nt / 2nt / 3nt, %8 nt (TMEM columns), %9 slice_inc
+// (A lo-word step between input slices), %10 blk_inc (B lo-word step between
+// the stacked tap blocks).  BX >= 2.
+//
+// Input slice j writes accumulator slices [j - min(j,2), j - max(j-BX+1,0)],
+// so MMAs of neighbouring j overlap in TMEM.  Issued in j order they form a
+// read-after-write chain through the accumulator and the tensor pipe
+// serialises them (~64 instead of ~46 cycles per MMA); the orders below
+// (found by search, tools/fold_order.py) keep MMAs that touch the same
+// slices at least two issues apart.  VXB_FM(D, A, B, ID, P): accumulator
+// slice D, input slice A, B tap block B, instruction descriptor ID,
+// accumulate predicate P (q = overwrite, for the tile's first step).
+#define VXB_FM(D, A, B, ID, P)                                                               \
+  "mad.lo.u32 dd, %8, " #D ", %0;\n\tmad.lo.u32 al, %9, " #A ", %1;\n\t"                    \
+  "mad.lo.u32 bl, %10, " #B ", %3;\n\tmov.b64 ad, {al, %2};\n\tmov.b64 bd, {bl, %4};\n\t"  \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [dd], ad, bd, " ID ", " P ";\n\t"
+#define VXB_FOLD_ASM(SEQ)                                                                   \
+  "{\n\t.reg .pred e, p, q;\n\t.reg .b64 ad, bd;\n\t.reg .b32 al, dd, bl;\n\t"           \
+  "elect.sync _|e, 0xffffffff;\n\tsetp.eq.u32 p, %8, %8;\n\tsetp.ne.u32 q, %8, %8;\n\t" SEQ "}"
+#define VXB_FOLD_OPS                                                                        \
+  ::"r"(d), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(id1), "r"(id2), "r"(id3), "r"(nt), \
+      "r"(slice_inc), "r"(blk_inc)                                                          \
+      : "memory"
+#define VXB_FOLD_STEADY_2 VXB_FM(1, 3, 0, "%5", "p") VXB_FM(0, 0, 2, "%5", "p") VXB_FM(0, 2, 0, "%6", "p") VXB_FM(0, 1, 1, "%6", "p")
+#define VXB_FOLD_FIRST_2 VXB_FM(0, 0, 2, "%5", "q") VXB_FM(1, 1, 2, "%5", "q") VXB_FM(0, 1, 1, "%5", "p") VXB_FM(1, 3, 0, "%5", "p") VXB_FM(0, 2, 0, "%6", "p")
+#define VXB_FOLD_STEADY_3 VXB_FM(0, 1, 1, "%6", "p") VXB_FM(0, 2, 0, "%7", "p") VXB_FM(1, 3, 0, "%6", "p") VXB_FM(0, 0, 2, "%5", "p") VXB_FM(2, 4, 0, "%5", "p")
+#define VXB_FOLD_FIRST_3 VXB_FM(2, 2, 2, "%5", "q") VXB_FM(1, 1, 2, "%5", "q") VXB_FM(0, 0, 2, "%5", "q") VXB_FM(1, 3, 0, "%6", "p") VXB_FM(0, 1, 1, "%5", "p") VXB_FM(2, 4, 0, "%5", "p") VXB_FM(0, 2, 0, "%6", "p")
+#define VXB_FOLD_STEADY_4 VXB_FM(3, 5, 0, "%5", "p") VXB_FM(0, 2, 0, "%7", "p") VXB_FM(1, 3, 0, "%7", "p") VXB_FM(0, 0, 2, "%5", "p") VXB_FM(2, 4, 0, "%6", "p") VXB_FM(0, 1, 1, "%6", "p")
+#define VXB_FOLD_FIRST_4 VXB_FM(3, 3, 2, "%5", "q") VXB_FM(1, 1, 2, "%5", "q") VXB_FM(2, 2, 2, "%5", "q") VXB_FM(0, 0, 2, "%5", "q") VXB_FM(3, 5, 0, "%5", "p") VXB_FM(1, 3, 0, "%6", "p") VXB_FM(0, 1, 1, "%5", "p") VXB_FM(2, 4, 0, "%6", "p") VXB_FM(0, 2, 0, "%6", "p")
+#define VXB_FOLD_STEADY_6 VXB_FM(0, 0, 2, "%5", "p") VXB_FM(1, 3, 0, "%7", "p") VXB_FM(4, 6, 0, "%6", "p") VXB_FM(0, 2, 0, "%7", "p") VXB_FM(3, 5, 0, "%7", "p") VXB_FM(0, 1, 1, "%6", "p") VXB_FM(2, 4, 0, "%7", "p") VXB_FM(5, 7, 0, "%5", "p")
+#define VXB_FOLD_FIRST_6 VXB_FM(3, 3, 2, "%5", "q") VXB_FM(0, 0, 2, "%5", "q") VXB_FM(1, 1, 2, "%5", "q") VXB_FM(4, 4, 2, "%5", "q") VXB_FM(2, 2, 2, "%5", "q") VXB_FM(0, 1, 1, "%5", "p") VXB_FM(5, 5, 2, "%5", "q") VXB_FM(1, 3, 0, "%6", "p") VXB_FM(3, 5, 0, "%6", "p") VXB_FM(5, 7, 0, "%5", "p") VXB_FM(0, 2, 0, "%6", "p") VXB_FM(2, 4, 0, "%6", "p") VXB_FM(4, 6, 0, "%6", "p")
+#define VXB_FOLD_STEADY_8 VXB_FM(1, 3, 0, "%7", "p") VXB_FM(4, 6, 0, "%7", "p") VXB_FM(7, 9, 0, "%5", "p") VXB_FM(0, 2, 0, "%7", "p") VXB_FM(3, 5, 0, "%7", "p") VXB_FM(6, 8, 0, "%6", "p") VXB_FM(0, 1, 1, "%6", "p") VXB_FM(2, 4, 0, "%7", "p") VXB_FM(5, 7, 0, "%7", "p") VXB_FM(0, 0, 2, "%5", "p")
+#define VXB_FOLD_FIRST_8 VXB_FM(4, 4, 2, "%5", "q") VXB_FM(0, 0, 2, "%5", "q") VXB_FM(5, 5, 2, "%5", "q") VXB_FM(6, 6, 2, "%5", "q") VXB_FM(2, 2, 2, "%5", "q") VXB_FM(7, 7, 2, "%5", "q") VXB_FM(5, 7, 0, "%6", "p") VXB_FM(0, 1, 1, "%5", "p") VXB_FM(1, 1, 2, "%5", "q") VXB_FM(3, 3, 2, "%5", "q") VXB_FM(6, 8, 0, "%6", "p") VXB_FM(1, 3, 0, "%6", "p") VXB_FM(7, 9, 0, "%5", "p") VXB_FM(3, 5, 0, "%6", "p") VXB_FM(0, 2, 0, "%6", "p") VXB_FM(2, 4, 0, "%6", "p") VXB_FM(4, 6, 0, "%6", "p")
+
+#define VXB_R1(x) x
+#define VXB_R2(x) x x
+#define VXB_R3(x) x x x
+#define VXB_R4(x) x x x x
+#define VXB_R5(x) x x x x x
+#define VXB_R6(x) x x x x x x
+#define VXB_R7(x) x x x x x x x
+#define VXB_R8(x) x x x x x x x x
+template <int BX>
+__device__ __forceinline__ void umma_fold_step(uint32_t d, uint32_t a_lo, uint32_t a_hi,
+                                               uint32_t b_lo, uint32_t b_hi, uint32_t id1,
+                                               uint32_t id2, uint32_t id3, uint32_t nt,
+                                               uint32_t slice_inc, uint32_t blk_inc) {
+  static_assert(BX == 2 || BX == 3 || BX == 4 || BX == 6 || BX == 8, "folded step width");
+  if (BX == 2) asm volatile(VXB_FOLD_ASM(VXB_FOLD_STEADY_2) VXB_FOLD_OPS);
+  if (BX == 3) asm volatile(VXB_FOLD_ASM(VXB_FOLD_STEADY_3) VXB_FOLD_OPS);
+  if (BX == 4) asm volatile(VXB_FOLD_ASM(VXB_FOLD_STEADY_4) VXB_FOLD_OPS);
+  if (BX == 6) asm volatile(VXB_FOLD_ASM(VXB_FOLD_STEADY_6) VXB_FOLD_OPS);
+  if (BX == 8) asm volatile(VXB_FOLD_ASM(VXB_FOLD_STEADY_8) VXB_FOLD_OPS);
+}
+// first K step of a tile: the d = 0 terms overwrite (accumulate off) before
+// any accumulating MMA touches their slice
+template <int BX>
+__device__ __forceinline__ void umma_fold_first(uint32_t d, uint32_t a_lo, uint32_t a_hi,
+                                                uint32_t b_lo, uint32_t b_hi, uint32_t id1,
+                                                uint32_t id2, uint32_t id3, uint32_t nt,
+                                                uint32_t slice_inc, uint32_t blk_inc) {
+  static_assert(BX == 2 || BX == 3 || BX == 4 || BX == 6 || BX == 8, "folded step width");
+  if (BX == 2) asm volatile(VXB_FOLD_ASM(VXB_FOLD_FIRST_2) VXB_FOLD_OPS);
+  if (BX == 3) asm volatile(VXB_FOLD_ASM(VXB_FOLD_FIRST_3) VXB_FOLD_OPS);
+  if (BX == 4) asm volatile(VXB_FOLD_ASM(VXB_FOLD_FIRST_4) VXB_FOLD_OPS);
+  if (BX == 6) asm volatile(VXB_FOLD_ASM(VXB_FOLD_FIRST_6) VXB_FOLD_OPS);
+  if (BX == 8) asm volatile(VXB_FOLD_ASM(VXB_FOLD_FIRST_8) VXB_FOLD_OPS);
+}
+#undef VXB_FM
+#undef VXB_FOLD_ASM
+#undef VXB_FOLD_OPS
+
+// CNT cta_group::2 MMAs in one asm block: D and the A lo word advance by
+// d_inc / a_inc, B and the instruction descriptor are shared (the folded
+// CTA-pair walk, mma_group_fold_pair).
+#define VXB_PRUN_HEAD                                                        \
+  "{\n\t.reg .pred e, p;\n\t.reg .b64 ad, bd;\n\t.reg .b32 al, dd;\n\t"     \
+  "elect.sync _|e, 0xffffffff;\n\t"                                          \
+  "setp.ne.b32 p, %6, 0;\n\t"                                                \
+  "mov.b32 al, %1;\n\tmov.b32 dd, %0;\n\t"                                   \
+  "mov.b64 bd, {%3, %4};\n\t"
+#define VXB_PRUN_MMA                                                                        \
+  "mov.b64 ad, {al, %2};\n\t@e tcgen05.mma.cta_group::2.kind::f16 [dd], ad, bd, %5, p;\n\t" \
+  "add.u32 al, al, %8;\n\tadd.u32 dd, dd, %7;\n\t"
+#define VXB_PRUN_OPS                                                                      \
+  ::"r"(d), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate), "r"(d_inc), \
+      "r"(a_inc)                                                                          \
+      : "memory"
+template <int CNT>
+__device__ __forceinline__ void umma_pair_run(uint32_t d, uint32_t a_lo, uint32_t a_hi,
+                                              uint32_t b_lo, uint32_t b_hi, uint32_t idesc,
+                                              uint32_t accumulate, uint32_t d_inc,
+                                              uint32_t a_inc) {
+  static_assert(CNT >= 1 && CNT <= 10, "run length");
+  if (CNT == 1) asm volatile(VXB_PRUN_HEAD VXB_R1(VXB_PRUN_MMA) "}" VXB_PRUN_OPS);
+  if (CNT == 2) asm volatile(VXB_PRUN_HEAD VXB_R2(VXB_PRUN_MMA) "}" VXB_PRUN_OPS);
+  if (CNT == 3) asm volatile(VXB_PRUN_HEAD VXB_R3(VXB_PRUN_MMA) "}" VXB_PRUN_OPS);
+  if (CNT == 4) asm volatile(VXB_PRUN_HEAD VXB_R4(VXB_PRUN_MMA) "}" VXB_PRUN_OPS);
+  if (CNT == 5) asm volatile(VXB_PRUN_HEAD VXB_R5(VXB_PRUN_MMA) "}" VXB_PRUN_OPS);
+  if (CNT == 6) asm volatile(VXB_PRUN_HEAD VXB_R6(VXB_PRUN_MMA) "}" VXB_PRUN_OPS);
+  if (CNT == 7) asm volatile(VXB_PRUN_HEAD VXB_R7(VXB_PRUN_MMA) "}" VXB_PRUN_OPS);
+  if (CNT == 8) asm volatile(VXB_PRUN_HEAD VXB_R8(VXB_PRUN_MMA) "}" VXB_PRUN_OPS);
+  if (CNT == 9) asm volatile(VXB_PRUN_HEAD VXB_R8(VXB_PRUN_MMA) VXB_PRUN_MMA "}" VXB_PRUN_OPS);
+  if (CNT == 10)
+    asm volatile(VXB_PRUN_HEAD VXB_R8(VXB_PRUN_MMA) VXB_R2(VXB_PRUN_MMA) "}" VXB_PRUN_OPS);
+}
+#undef VXB_PRUN_HEAD
+#undef VXB_PRUN_MMA
+#undef VXB_PRUN_OPS
+
 template <int BX, bool PAIR>
 __device__ __forceinline__ void umma_step_elect(uint32_t d, uint32_t a_lo, uint32_t a_hi,
                                                 uint32_t b_lo, uint32_t b_hi, uint32_t idesc,

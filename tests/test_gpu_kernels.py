@@ -32,11 +32,17 @@ def _conv_bf16(x, w, b, pad, act=None, base=None, scale=None, out_dtype="bf16"):
     D, K = _dev()
     xd = D.to_device_blocked(x)
     osp = tuple(s + 2 * p - k + 1 for s, p, k in zip(x.shape[2:], pad, w.shape[2:]))
-    out = D.empty_blocked(x.shape[0], w.shape[0], osp, out_dtype)
+    if out_dtype == "f32std":   # fp32 NCDHW output written by the conv epilogue
+        out = D.standard(torch.empty((x.shape[0], w.shape[0]) + osp, dtype=torch.float32,
+                                     device=xd.t.device))
+    else:
+        out = D.empty_blocked(x.shape[0], w.shape[0], osp, out_dtype)
     bd = D.to_device_blocked(base) if base is not None else None
     pk = K.pack_conv(w, b, base_scale=scale)
     K.conv3d(xd, pk, out, pad=pad, base=bd, fused_act=(act, 1.0) if act else None)
     torch.cuda.synchronize()
+    if out_dtype == "f32std":
+        return out.t.cpu().numpy(), pk.path
     return D.to_host_standard(out), pk.path
 
 
@@ -100,6 +106,34 @@ def test_tap_fold_matches_unfolded(k, pad, monkeypatch):
     plain, _ = _conv_bf16(x, w, b, pad, "elu", out_dtype="fp32")
     mx, _ = R.normalized_error(folded, plain)
     assert mx < 1e-5, mx
+
+
+@pytest.mark.parametrize("bx", ["1", "2", "3", "4", "6", "8"])
+@pytest.mark.parametrize("c,n,sp", [(8, 1, (18, 20, 12)), (16, 2, (9, 21, 10)),
+                                    (28, 1, (18, 33, 12)), (32, 1, (7, 16, 17))])
+@pytest.mark.parametrize("k,pad", [((3, 3, 3), (1, 1, 1)), ((1, 3, 3), (0, 1, 1))])
+def test_fold_pair_matches_single_cta(bx, c, n, sp, k, pad, monkeypatch):
+    """Folded convs with N = 3nt <= 96 run as CTA pairs (cta_group::2, every
+    MMA at N = 3nt with scratch slices around the tile); the result differs
+    from the single-CTA folded walk only in fp32 summation order.  Covers odd
+    tile counts (the pair's padding tile), batch 2, residual operands and all
+    tile widths."""
+    monkeypatch.setenv("VXB_TC_BX", bx)
+    monkeypatch.setenv("VXB_TC_FOLDPAIR", "2")   # every eligible fold pairs
+    rng = np.random.default_rng(int(bx) * 100 + c)
+    x = rng.uniform(-1, 1, (n, c) + sp).astype(np.float32)
+    w = (rng.standard_normal((c, c) + k) * 0.1).astype(np.float32)
+    b = rng.standard_normal(c).astype(np.float32)
+    base = rng.uniform(-1, 1, (n, c) + sp).astype(np.float32)
+    scale = rng.uniform(0.5, 1.5, c).astype(np.float32)
+    paired, _ = _conv_bf16(x, w, b, pad, "elu", base, scale, out_dtype="f32std")
+    monkeypatch.setenv("VXB_TC_FOLDPAIR", "0")
+    single, _ = _conv_bf16(x, w, b, pad, "elu", base, scale, out_dtype="f32std")
+    mx, _ = R.normalized_error(paired, single)
+    assert mx < 1e-5, mx
+    want = _ref_bf16(x, w, b, pad, "elu", base, scale)
+    mx, l2 = R.normalized_error(paired, want)
+    assert mx < BF16_TOL and l2 < 3e-3, (mx, l2)
 
 
 @pytest.mark.parametrize("bx", ["3", "6", "8"])

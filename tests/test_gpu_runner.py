@@ -126,10 +126,13 @@ def test_runner_graph_replay_deterministic_and_validates():
 
 
 @pytest.mark.parametrize("cfg", [1, 4])
-def test_fused_input_pack_is_bit_identical(cfg):
+def test_fused_input_pack_is_bit_identical(cfg, monkeypatch):
     """fuse_input=True hands the fp32 network input straight to the first
     conv (in-kernel conversion); the bf16 operands and hence the outputs are
-    identical to packing first."""
+    identical to packing first.  (Both sides use the single-CTA MMA walk: the
+    fp32-input conv does not run as a CTA pair, whose folded walk sums in
+    another order.)"""
+    monkeypatch.setenv("VXB_TC_FOLDPAIR", "0")
     spec, store = _small(cfg)
     plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
     lo, hi = C.input_range(cfg)
@@ -142,8 +145,10 @@ def test_fused_input_pack_is_bit_identical(cfg):
     np.testing.assert_array_equal(a, plain.run(x)[n])
 
 
-def test_fused_maxpool_runner_bit_identical():
-    """Config 5's 1x2x2 pools fold into the preceding conv epilogues."""
+def test_fused_maxpool_runner_bit_identical(monkeypatch):
+    """Config 5's 1x2x2 pools fold into the preceding conv epilogues (same
+    single-CTA MMA walk on both sides, see above)."""
+    monkeypatch.setenv("VXB_TC_FOLDPAIR", "0")
     spec, store = _small(5)
     plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
     x = C.make_input(spec, 4, 0.0, 1.0)
