@@ -429,7 +429,9 @@ template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN, bool POOL = f
 __global__ void __launch_bounds__(tc_threads(F32IN), 1)
     conv3d_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int warp = threadIdx.x >> 5;
+  // warp index broadcast from lane 0 so ptxas treats each role's code as
+  // warp-uniform (as CUTLASS's canonical_warp_idx_sync does)
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   const SmemMap sm = smem_map(p);
   pdl_trigger();
@@ -453,7 +455,11 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
 
   // CTA pairs (cluster 2) walk pairs of tiles in lockstep so they can share
   // one B (weight) stream through TMA multicast
-  const int crank = p.cluster == 2 ? static_cast<int>(cluster_rank()) : 0;
+  // (broadcast so ptxas knows it is warp-uniform: an opaque asm result would
+  // make everything under `crank == 0` look divergent, and the MMA issue loop
+  // then routes every descriptor through R2UR / VOTEU / BRA.DIV sequences)
+  const int crank =
+      p.cluster == 2 ? __shfl_sync(0xffffffffu, static_cast<int>(cluster_rank()), 0) : 0;
   const int first_tile = (blockIdx.x / p.cluster) * p.cluster + crank;
   const int tile_step = gridDim.x;
   const uint16_t pair_mask = 0x3;
