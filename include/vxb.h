@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define VXB_ABI_VERSION 2
+#define VXB_ABI_VERSION 3
 
 /* element types */
 #define VXB_BF16 0
@@ -216,6 +216,14 @@ int vxb_pad_copy(const vxb_tensor *in, const vxb_tensor *out, const int pads[3],
  * generic strided copy between any two views of the same logical shape,
  * converting dtype; tail lanes of a blocked destination are zeroed. */
 int vxb_copy(const vxb_tensor *src, const vxb_tensor *dst, void *stream);
+/* vxb_copy with flags.  VXB_COPY_INDEPENDENT: the copy reads nothing the
+ * previous kernel in the stream writes and writes nothing it touches (a
+ * network-input pack), so it may start beside that kernel instead of after
+ * it (programmatic launch without a grid-dependency wait).  Used by
+ * PlanBatch to overlap one network's input pack with the previous network's
+ * convolution (runner.py). */
+#define VXB_COPY_INDEPENDENT 1
+int vxb_copy_ex(const vxb_tensor *src, const vxb_tensor *dst, int flags, void *stream);
 /* fill a whole view (all lanes) with zeros */
 int vxb_zero(const vxb_tensor *t, void *stream);
 

@@ -26,7 +26,7 @@ from .tiling import TileGrid, grid_for, plan_tiles
 
 def __getattr__(name):
     # device-side entry points import torch lazily
-    if name in ("PlanRunner", "execute"):
+    if name in ("PlanRunner", "PlanBatch", "execute"):
         from . import runner
         return getattr(runner, name)
     if name == "run_tiled":
@@ -44,7 +44,7 @@ __all__ = [
     "BACKEND_ENV", "Backend", "ConvInvocation", "CycleError", "DanglingReferenceError",
     "DEFAULT_PATCH_EXTENT", "DEFAULT_SIMD_WIDTH", "DuplicateTopError", "ExecutionError",
     "ExecutionPlan", "FormatError", "LayerKind", "LayerSpec", "LayoutError", "ModelError",
-    "NetworkSpec", "ParseError", "PassReport", "PlanError", "PlanRunner", "ShapeError",
+    "NetworkSpec", "ParseError", "PassReport", "PlanBatch", "PlanError", "PlanRunner", "ShapeError",
     "SubImageTask", "TileError", "TileGrid", "UnknownLayerError", "VoxplanError", "WeightStore",
     "available_backends", "build_ir", "compile_network", "compiled_available", "dump_plan",
     "execute", "get_backend", "grid_for", "optimize", "parse_network", "parse_plan",

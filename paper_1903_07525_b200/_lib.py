@@ -19,7 +19,8 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 VXB_BF16 = 0
 VXB_F32 = 1
 ACT_CODE = {None: 0, "relu": 1, "elu": 2, "sigmoid": 3}   # kernels_cy.py:19
-ABI_VERSION = 2      # include/vxb.h VXB_ABI_VERSION
+ABI_VERSION = 3      # include/vxb.h VXB_ABI_VERSION
+COPY_INDEPENDENT = 1  # VXB_COPY_INDEPENDENT
 PATH_TC = 1
 PATH_DIRECT = 2
 PATH_TC_UNFOLDED = 3
@@ -114,6 +115,7 @@ SIGNATURES = [
     ("vxb_mergecrop", c_int, [TP, TP, TP, c_void_p]),
     ("vxb_pad_copy", c_int, [TP, TP, I3, c_void_p]),
     ("vxb_copy", c_int, [TP, TP, c_void_p]),
+    ("vxb_copy_ex", c_int, [TP, TP, c_int, c_void_p]),
     ("vxb_zero", c_int, [TP, c_void_p]),
 ]
 

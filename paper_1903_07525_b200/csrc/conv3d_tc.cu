@@ -190,7 +190,7 @@ __device__ __forceinline__ void dbg_clock(const TcParams &p, int it, int slot) {
 
 constexpr int EPI_WARPS = 12;
 constexpr int TC_THREADS = 96 + 32 * EPI_WARPS;   // A-TMA, MMA, B-TMA + epilogue
-constexpr int CVT_WARPS = 2;                      // fp32-input converters (F32IN)
+constexpr int CVT_WARPS = 4;                      // fp32-input converters (F32IN)
 __host__ __device__ constexpr int tc_threads(bool f32in) {
   return TC_THREADS + (f32in ? 32 * CVT_WARPS : 0);
 }
@@ -767,13 +767,22 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
     __syncwarp();
   } else if (F32IN && warp >= 3 + EPI_WARPS) {
     // ===================== fp32 -> bf16 chunk converters (F32IN) ============
-    // Staging slot = (8 c, xb, hy, hzb) fp32 of xb halo x-slices; every row
-    // (x, y, z < hz) becomes one 16-byte bf16x8 row of the A stage's chunk array.
+    // Staging slot = (8 c, xb, hy, hzb) fp32 of xb halo x-slices.  A work item
+    // is one z-pair of a staging row: 8 float2 loads (one per channel plane)
+    // give two voxels' 8 channels, written as two 16-byte bf16x8 rows of the
+    // A stage's chunk array.  Pairs start at even staging positions (8-byte
+    // loads), so with an odd z shift the first / last pair of a row holds one
+    // voxel outside the halo, which is not stored.
     const int ct = threadIdx.x - 32 * (3 + EPI_WARPS);   // 0 .. 32*CVT_WARPS-1
     constexpr int NT = 32 * CVT_WARPS;
     const int rows = p.hy * p.hz;
-    const int ddy = NT / p.hz, ddz = NT % p.hz;
+    const int zs = p.f32in_zshift;
+    const int p0 = zs >> 1;                              // first pair (staging position 2*p0)
+    const int np = ((zs + p.hz + 1) >> 1) - p0;          // pairs per row
+    const int per_x = p.hy * np;
     const int cstride = p.f32in_xb * p.hy * p.hzb;       // fp32 elements per channel plane
+    // this thread's first item and the stride, split into (x, y, pair)
+    const int s_x = NT / per_x, s_y = (NT % per_x) / np, s_p = NT % np;
     int a_st = 0, s_st = 0, s_ph = 0;
     for (int tile = first_tile; tile < p.total_tiles; tile += tile_step) {
       for (int g = 0; g < p.n_groups; ++g) {
@@ -784,25 +793,39 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
             mbar_wait(&stg_full[s_st], s_ph);
             const float *src0 = reinterpret_cast<const float *>(stg_buf + s_st * p.stg_bytes);
             const int nxs = min(p.f32in_xb, p.hx - xs0);
-            for (int xi = 0; xi < nxs; ++xi) {
-            const float *src = src0 + xi * p.hy * p.hzb;
-            uint4 *dst = reinterpret_cast<uint4 *>(abase + ci * p.chunk_stride) + (xs0 + xi) * rows;
-            int y = ct / p.hz, z = ct % p.hz;
-            for (int r = (p.dbg_mode & 64) ? rows : ct; r < rows; r += NT) {
-              const float *q = src + y * p.hzb + z + p.f32in_zshift;
-              uint4 u;
-              __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&u);
+            uint4 *dst0 = reinterpret_cast<uint4 *>(abase + ci * p.chunk_stride) + xs0 * rows;
+            int xi = ct / per_x, y = (ct % per_x) / np, pp = ct % np;
+            if (p.dbg_mode & 64) xi = nxs;
+            while (xi < nxs) {
+              const int zp = 2 * (pp + p0);                // staging position of the pair
+              const float *q = src0 + (xi * p.hy + y) * p.hzb + zp;
+              float2 v[8];
 #pragma unroll
-              for (int i = 0; i < 4; ++i)
-                h[i] = __floats2bfloat162_rn(q[(2 * i) * cstride], q[(2 * i + 1) * cstride]);
-              dst[r] = u;
-              y += ddy;
-              z += ddz;
-              if (z >= p.hz) {
-                z -= p.hz;
+              for (int c = 0; c < 8; ++c) v[c] = *reinterpret_cast<const float2 *>(q + c * cstride);
+              uint4 lo, hi;
+              __nv_bfloat162 *hl = reinterpret_cast<__nv_bfloat162 *>(&lo);
+              __nv_bfloat162 *hh = reinterpret_cast<__nv_bfloat162 *>(&hi);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                hl[i] = __floats2bfloat162_rn(v[2 * i].x, v[2 * i + 1].x);
+                hh[i] = __floats2bfloat162_rn(v[2 * i].y, v[2 * i + 1].y);
+              }
+              const int z = zp - zs;                       // halo z of the pair's first voxel
+              uint4 *d = dst0 + xi * rows + y * p.hz + z;
+              if (z >= 0) d[0] = lo;
+              if (z + 1 < p.hz) d[1] = hi;
+              // advance by NT items: (x, y, pair) with carries
+              pp += s_p;
+              y += s_y;
+              xi += s_x;
+              if (pp >= np) {
+                pp -= np;
                 ++y;
               }
-            }
+              if (y >= p.hy) {
+                y -= p.hy;
+                ++xi;
+              }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&stg_empty[s_st]);

@@ -466,8 +466,14 @@ static dim3 grid3(const DView &v, int threads) {
 // Network-boundary pack: fp32 NCDHW (z contiguous) -> bf16 blocked.  Each
 // thread converts 4 consecutive z of one 8-fmap chunk: 8 float4 loads (one
 // per fmap plane, 512 B per warp instruction) and 4 16-byte stores.
+// INDEP: the pack reads only a network input and writes a buffer no kernel
+// before it in the stream touches, so it skips griddepcontrol.wait and may
+// run beside its predecessor (e.g. the previous network's persistent conv,
+// whose one CTA per SM leaves room for one pack CTA); it triggers its own
+// dependents only by completing.
+template <bool INDEP>
 __global__ void pack_std_f32_kernel(DView src, DView dst) {
-  pdl_begin();
+  if (!INDEP) pdl_begin();
   const int zq = dst.z >> 2;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= dst.y * zq) return;
@@ -539,10 +545,12 @@ static bool std_f32_vec4(const DView &t) {
 }
 static bool blocked_bf16(const DView &t) { return t.blocked && t.dtype == VXB_BF16; }
 
-int launch_copy(const DView &src, const DView &dst, cudaStream_t s) {
+int launch_copy(const DView &src, const DView &dst, cudaStream_t s, bool independent) {
   if (std_f32_vec4(src) && blocked_bf16(dst)) {
     dim3 g((dst.y * (dst.z >> 2) + 127) / 128, dst.x, dst.n * ((dst.c + 7) / 8));
-    return check_cuda(launch_pdl(pack_std_f32_kernel, g, dim3(128), 0, s, src, dst),
+    return check_cuda(independent
+                          ? launch_pdl(pack_std_f32_kernel<true>, g, dim3(128), 0, s, src, dst)
+                          : launch_pdl(pack_std_f32_kernel<false>, g, dim3(128), 0, s, src, dst),
                       "pack_std_f32_kernel");
   }
   if (blocked_bf16(src) && std_f32_vec4(dst)) {

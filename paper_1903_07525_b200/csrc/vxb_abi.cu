@@ -1129,6 +1129,15 @@ int vxb_copy(const vxb_tensor *src, const vxb_tensor *dst, void *stream) {
   return launch_copy(to_dview(*src), to_dview(*dst), as_stream(stream));
 }
 
+int vxb_copy_ex(const vxb_tensor *src, const vxb_tensor *dst, int flags, void *stream) {
+  int rc;
+  if ((rc = check_view(src, "copy.src")) || (rc = check_view(dst, "copy.dst"))) return rc;
+  if ((rc = same_shape(src, dst, "copy"))) return rc;
+  if (flags & ~VXB_COPY_INDEPENDENT) return set_error(VXB_EINVAL, "copy: unknown flags %d", flags);
+  return launch_copy(to_dview(*src), to_dview(*dst), as_stream(stream),
+                     (flags & VXB_COPY_INDEPENDENT) != 0);
+}
+
 int vxb_zero(const vxb_tensor *t, void *stream) {
   int rc;
   if ((rc = check_view(t, "zero"))) return rc;

@@ -125,7 +125,7 @@ struct GatherDeconvParams {
   float alpha;
 };
 
-int launch_copy(const DView &src, const DView &dst, cudaStream_t s);
+int launch_copy(const DView &src, const DView &dst, cudaStream_t s, bool independent = false);
 int launch_zero(const DView &dst, cudaStream_t s);
 int launch_pool(const DView &in, const DView &out, const int *w, const int *st, int mode,
                 cudaStream_t s);

@@ -110,11 +110,18 @@ def null_tensor() -> _lib.VxbTensor:
     return _lib.VxbTensor()
 
 
-def copy(src: DTensor, dst: DTensor, stream=None) -> None:
+def copy(src: DTensor, dst: DTensor, stream=None, independent=False) -> None:
+    """vxb_copy; ``independent`` (vxb_copy_ex VXB_COPY_INDEPENDENT): the copy
+    touches nothing the previous kernel in the stream does, so it may run
+    beside that kernel (a network-input pack)."""
     L = _lib.lib()
     s, d = src.vxb(), dst.vxb()
-    _lib.check(L.vxb_copy(ctypes.byref(s), ctypes.byref(d), stream or current_stream_handle()),
-               "vxb_copy")
+    h = stream or current_stream_handle()
+    if independent:
+        _lib.check(L.vxb_copy_ex(ctypes.byref(s), ctypes.byref(d), _lib.COPY_INDEPENDENT, h),
+                   "vxb_copy_ex")
+    else:
+        _lib.check(L.vxb_copy(ctypes.byref(s), ctypes.byref(d), h), "vxb_copy")
 
 
 def zero(t: DTensor, stream=None) -> None:

@@ -324,7 +324,10 @@ class PlanRunner:
                 fused_in[id(rs[0][1])] = standard(self._in_std[name])
                 continue
             src = standard(self._in_std[name])
-            calls.append(lambda s=src, d=v.dt: _copy(s, d))
+            # the pack reads a network input and writes a buffer only this
+            # network's later steps read: independent of the kernel before it
+            # (in a PlanBatch, the previous network's last conv)
+            calls.append(lambda s=src, d=v.dt: _copy(s, d, independent=True))
         n_in = len(calls)
         self.fused_inputs = len(fused_in)
         # fused unpack: a conv/deconv whose result is only a network output
@@ -577,9 +580,62 @@ class PendingRun:
         return self.outputs
 
 
-def _copy(src: DTensor, dst: DTensor):
+def _copy(src: DTensor, dst: DTensor, independent=False):
     from .device import copy
-    copy(src, dst)
+    copy(src, dst, independent=independent)
+
+
+class PlanBatch:
+    """Several independent networks (PlanRunners on one device, inputs in
+    their static input buffers) replayed back to back as ONE CUDA graph.
+
+    A serving loop over many small volumes, or the config-2 featuremap
+    sweep, runs networks whose inputs are all resident: the fp32 -> bf16
+    input pack of network i+1 then has no dependency on network i.  Packs are
+    launched with VXB_COPY_INDEPENDENT, so inside the graph each one starts as
+    soon as the previous network's persistent conv is resident and runs in
+    the one CTA slot per SM that conv leaves free (HBM-bound pack beside a
+    tensor-bound conv); the next conv still waits for its pack.  Results are
+    bit-identical to running the networks one by one."""
+
+    def __init__(self, runners):
+        torch = _torch()
+        if not runners:
+            raise ExecutionError("PlanBatch needs at least one runner")
+        dev = runners[0].device
+        if any(r.device != dev for r in runners):
+            raise ExecutionError("PlanBatch runners must share one device")
+        self.runners = list(runners)
+        self.device = dev
+        self.stream = torch.cuda.Stream(device=dev)
+        self.launches = sum(r.launches for r in runners)
+        self._graph = None
+
+    def replay(self):
+        """Enqueue every network once on ``self.stream`` (captured on first use)."""
+        torch = _torch()
+        if self._graph is None:
+            with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+                for r in self.runners:
+                    r._launch_all()          # warm-up: first launches configure kernels
+            self.stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.device(self.device), torch.cuda.graph(g, stream=self.stream):
+                for r in self.runners:
+                    r._launch_all()
+            self._graph = g
+        with torch.cuda.stream(self.stream):
+            self._graph.replay()
+
+    def run_device(self):
+        """Replay ordered after the caller's current stream; returns each
+        runner's static output buffers."""
+        torch = _torch()
+        cs = torch.cuda.current_stream(self.device)
+        self.stream.wait_stream(cs)
+        self.replay()
+        cs.wait_stream(self.stream)
+        return [dict(r._out_std) for r in self.runners]
 
 
 def execute(plan, inputs, backend=None) -> dict:

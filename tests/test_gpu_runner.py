@@ -174,3 +174,29 @@ def test_run_tiled_equals_manual_assembly():
         want[(slice(None), slice(None)) + t.out_window] = res[(slice(None), slice(None))
                                                               + t.local_window]
     np.testing.assert_array_equal(got, want)
+
+
+def test_plan_batch_bit_identical_to_sequential_runs():
+    """PlanBatch replays several independent networks as one graph with each
+    input pack launched independently (it may run beside the previous
+    network's conv); every output equals the network run on its own."""
+    nets = []
+    for c, k in ((8, (3, 3, 3)), (32, (1, 3, 3)), (16, (3, 3, 3)), (64, (3, 3, 3))):
+        spec, store = C.config2(c, k)
+        plan, _ = P.compile_network(spec, store, fixpoint=True)
+        nets.append(plan)
+    runners = [P.PlanRunner(p) for p in nets]
+    for i, r in enumerate(runners):
+        for name, t in r.input_buffers().items():
+            t.copy_(torch.rand(t.shape, generator=torch.Generator().manual_seed(i)) * 2 - 1)
+    alone = []
+    for r in runners:
+        outs = r.run_device(r.input_buffers())
+        alone.append({n: t.clone() for n, t in outs.items()})
+    batch = P.PlanBatch(runners)
+    for _ in range(2):
+        got = batch.run_device()
+        torch.cuda.synchronize()
+        for a, g in zip(alone, got):
+            for n in a:
+                assert torch.equal(a[n], g[n]), n
