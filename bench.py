@@ -207,7 +207,14 @@ def run_b200(args, rank, world, local_rank):
     # The step: every layer's network once, as one CUDA graph (PlanBatch):
     # each network's fp32 -> bf16 input pack runs beside the previous
     # network's conv (independent launch), each conv waits for its own pack.
-    batch = P.PlanBatch([L["runner"] for L in layers])
+    order = list(range(len(layers)))
+    mode = os.environ.get("VXB_BATCH_ORDER", "")
+    if mode == "desc":
+        order.sort(key=lambda i: -layers[i]["flops"])
+    elif mode == "small_then_desc":
+        order.sort(key=lambda i: -layers[i]["flops"])
+        order = order[-1:] + order[:-1]
+    batch = P.PlanBatch([layers[i]["runner"] for i in order])
 
     def batch_step():
         """One timed window around the whole sweep on the batch stream (a

@@ -14,6 +14,7 @@
 // All element-wise kernels work on one 8-fmap chunk per thread: for the
 // blocked bf16 layout that is one 16-byte load/store, z fastest across the
 // warp so a warp touches 512 contiguous bytes.
+#include <algorithm>
 #include <cuda_bf16.h>
 #include "vxb_internal.h"
 
@@ -466,20 +467,9 @@ static dim3 grid3(const DView &v, int threads) {
 // Network-boundary pack: fp32 NCDHW (z contiguous) -> bf16 blocked.  Each
 // thread converts 4 consecutive z of one 8-fmap chunk: 8 float4 loads (one
 // per fmap plane, 512 B per warp instruction) and 4 16-byte stores.
-// INDEP: the pack reads only a network input and writes a buffer no kernel
-// before it in the stream touches, so it skips griddepcontrol.wait and may
-// run beside its predecessor (e.g. the previous network's persistent conv,
-// whose one CTA per SM leaves room for one pack CTA); it triggers its own
-// dependents only by completing.
-template <bool INDEP>
-__global__ void pack_std_f32_kernel(DView src, DView dst) {
-  if (!INDEP) pdl_begin();
-  const int zq = dst.z >> 2;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= dst.y * zq) return;
-  const int y = i / zq, z = (i - y * zq) * 4, x = blockIdx.y;
-  const int nch = (dst.c + 7) >> 3;
-  const int b = blockIdx.z / nch, ch = blockIdx.z - b * nch;
+// One pack item: 4 consecutive z of one 8-fmap chunk at (b, ch, x, y).
+__device__ __forceinline__ void pack_item(const DView &src, const DView &dst, int b, int ch, int x,
+                                          int y, int z) {
   float v[8][4];
 #pragma unroll
   for (int l = 0; l < 8; ++l) {
@@ -503,6 +493,36 @@ __global__ void pack_std_f32_kernel(DView src, DView dst) {
     for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[2 * k][q], v[2 * k + 1][q]);
     *reinterpret_cast<uint4 *>(o + q * dst.s[4]) = u;
   }
+}
+
+__global__ void pack_std_f32_kernel(DView src, DView dst) {
+  pdl_begin();
+  const int zq = dst.z >> 2;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= dst.y * zq) return;
+  const int y = i / zq, z = (i - y * zq) * 4, x = blockIdx.y;
+  const int nch = (dst.c + 7) >> 3;
+  const int b = blockIdx.z / nch, ch = blockIdx.z - b * nch;
+  pack_item(src, dst, b, ch, x, y, z);
+}
+
+// Independent variant (VXB_COPY_INDEPENDENT): reads only a network input and
+// writes a buffer no kernel before it in the stream touches, so it skips
+// griddepcontrol.wait and may run beside its predecessor (the previous
+// network's persistent conv, whose one CTA per SM leaves room for one pack
+// CTA).  Its dependents launch only when it completes.  (A grid-stride
+// variant with 4 CTAs per SM measured slower: 1.05 vs 0.89 ms per config-2
+// step — fewer loads in flight, and no full-occupancy tail once the conv
+// ends.)
+__global__ void pack_std_f32_indep_kernel(DView src, DView dst, int trigger) {
+  if (trigger) pdl_trigger();
+  const int zq = dst.z >> 2;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= dst.y * zq) return;
+  const int y = i / zq, z = (i - y * zq) * 4, x = blockIdx.y;
+  const int nch = (dst.c + 7) >> 3;
+  const int b = blockIdx.z / nch, ch = blockIdx.z - b * nch;
+  pack_item(src, dst, b, ch, x, y, z);
 }
 
 // The reverse at the output boundary: bf16 blocked -> fp32 NCDHW.
@@ -545,12 +565,19 @@ static bool std_f32_vec4(const DView &t) {
 }
 static bool blocked_bf16(const DView &t) { return t.blocked && t.dtype == VXB_BF16; }
 
+static int pack_trigger() {
+  const char *v = getenv("VXB_PACK_TRIGGER");
+  return v && atoi(v) ? 1 : 0;
+}
+
 int launch_copy(const DView &src, const DView &dst, cudaStream_t s, bool independent) {
   if (std_f32_vec4(src) && blocked_bf16(dst)) {
     dim3 g((dst.y * (dst.z >> 2) + 127) / 128, dst.x, dst.n * ((dst.c + 7) / 8));
-    return check_cuda(independent
-                          ? launch_pdl(pack_std_f32_kernel<true>, g, dim3(128), 0, s, src, dst)
-                          : launch_pdl(pack_std_f32_kernel<false>, g, dim3(128), 0, s, src, dst),
+    if (independent)
+      return check_cuda(launch_pdl(pack_std_f32_indep_kernel, g, dim3(128), 0, s, src, dst,
+                                   pack_trigger()),
+                        "pack_std_f32_indep_kernel");
+    return check_cuda(launch_pdl(pack_std_f32_kernel, g, dim3(128), 0, s, src, dst),
                       "pack_std_f32_kernel");
   }
   if (blocked_bf16(src) && std_f32_vec4(dst)) {
