@@ -596,9 +596,16 @@ class PlanBatch:
     soon as the previous network's persistent conv is resident and runs in
     the one CTA slot per SM that conv leaves free (HBM-bound pack beside a
     tensor-bound conv); the next conv still waits for its pack.  Results are
-    bit-identical to running the networks one by one."""
+    bit-identical to running the networks one by one.
 
-    def __init__(self, runners):
+    ``reorder`` (default) runs the networks largest-first by conv FLOPs so
+    that each input pack hides behind a conv at least as large as its own
+    network's, except that the smallest network goes first (its pack is the
+    one nothing hides): config-2 sweep 0.878 ms in listed order, 0.844
+    largest-first, 0.842 smallest + largest-first.  Outputs are returned in
+    the caller's order."""
+
+    def __init__(self, runners, reorder=True):
         torch = _torch()
         if not runners:
             raise ExecutionError("PlanBatch needs at least one runner")
@@ -606,6 +613,12 @@ class PlanBatch:
         if any(r.device != dev for r in runners):
             raise ExecutionError("PlanBatch runners must share one device")
         self.runners = list(runners)
+        order = list(range(len(self.runners)))
+        if reorder and len(order) > 2:
+            work = [_conv_flops(r.plan) for r in self.runners]
+            order.sort(key=lambda i: -work[i])
+            order = order[-1:] + order[:-1]
+        self.order = order
         self.device = dev
         self.stream = torch.cuda.Stream(device=dev)
         self.launches = sum(r.launches for r in runners)
@@ -616,13 +629,13 @@ class PlanBatch:
         torch = _torch()
         if self._graph is None:
             with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
-                for r in self.runners:
-                    r._launch_all()          # warm-up: first launches configure kernels
+                for i in self.order:
+                    self.runners[i]._launch_all()   # warm-up: first launches configure kernels
             self.stream.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.device(self.device), torch.cuda.graph(g, stream=self.stream):
-                for r in self.runners:
-                    r._launch_all()
+                for i in self.order:
+                    self.runners[i]._launch_all()
             self._graph = g
         with torch.cuda.stream(self.stream):
             self._graph.replay()
@@ -636,6 +649,16 @@ class PlanBatch:
         self.replay()
         cs.wait_stream(self.stream)
         return [dict(r._out_std) for r in self.runners]
+
+
+def _conv_flops(plan) -> float:
+    """Multiply-add work of a plan's convolutions (PlanBatch ordering)."""
+    f = 0.0
+    for st in plan.steps:
+        if st.kind is LayerKind.CONVOLUTION:
+            k = plan.weights.tensor(st.name, ROLE_KERNEL).shape
+            f += 2.0 * float(np.prod(k)) * float(np.prod(st.output.dims[2:])) * st.output.dims[0]
+    return f
 
 
 def execute(plan, inputs, backend=None) -> dict:
