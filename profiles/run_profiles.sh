@@ -11,13 +11,13 @@ timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > "$
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file "$OUT/launches_config2.csv" python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
   --no-e2e > /dev/null 2>&1; echo "launches rc=$?"
-# 3. full capture of the dominant kernel: c128_k333, the 9th conv launch (each runner
-#    runs its layer once eagerly, then from its CUDA graph)
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:conv3d_tc -s 8 -c 1 \
+# 3. full capture of the dominant kernel: c128_k333, the 2nd conv launch (PlanBatch warm-up
+#    order: smallest network first, then largest-first by FLOPs; c16_k333 is the 8th)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:conv3d_tc -s 1 -c 1 \
   -o "$OUT/ncu_c128_k333" -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e \
   > /dev/null 2>&1; echo "full rc=$?"
-# 4. one low-fmap conv (c16_k333, 3rd conv launch) and the config-5 patch launch list
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:conv3d_tc -s 2 -c 1 \
+# 4. one low-fmap conv (c16_k333) and the config-5 patch launch list
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:conv3d_tc -s 7 -c 1 \
   -o "$OUT/ncu_c16_k333" -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e \
   > /dev/null 2>&1; echo "full16 rc=$?"
 timeout 300 python tools/cfg5_patch.py > "$OUT/cfg5_ops.txt" 2>&1
