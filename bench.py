@@ -573,9 +573,10 @@ def run_tiled_volume(args, rank, world, dev, dist, peaks, flush):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic", "config": {"workload": workload_name(5), "tiles": len(grid.tiles),
+                                        "patches_per_launch": dt.batch,
                                         "parallelism": "tiles/%d ranks" % world},
         "tflops": flops_patch * len(grid.tiles) / (ms * 1e-3) / 1e12,
-        "gpu_launches": dt.runner.launches * len(mine) * args.steps,
+        "gpu_launches": dt.launches_for(len(mine)) * args.steps,
         "clocks": clk.summary(),
     }
 

@@ -445,8 +445,12 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   const int slice_y = L.fold == 2;
   int sms = device_sms();
   if (sms <= 0) return set_error(VXB_ECUDA, "no CUDA device");
+  // The tile shape (and with it the MMA order, hence the fp32 summation
+  // order) is chosen from ONE batch entry's tile count, so a batch of
+  // volumes (rebatched plans: several patches per launch) computes every
+  // entry bit-identically to a batch-1 run.
   const long long other_tiles = static_cast<long long>(ceil_div(slice_y ? a.ox : a.oy, TILE_Y)) *
-                                ceil_div(a.oz, TILE_Z) * a.nb * L.n_tiles * a.reps;
+                                ceil_div(a.oz, TILE_Z) * L.n_tiles * a.reps;
   // fp32 NCDHW input (the network's own input tensor): converted in-kernel
   const vxb_tensor &x0 = *a.in[0];
   const bool f32in = x0.dtype == VXB_F32 && !x0.blocked;
@@ -489,7 +493,7 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   // checked at the widest tile, so any tile width chosen below has them.
   const long long spatial_min =
       static_cast<long long>(ceil_div(slice_y ? a.oy : a.ox, 8)) *
-      ceil_div(slice_y ? a.ox : a.oy, TILE_Y) * ceil_div(a.oz, TILE_Z) * a.nb;
+      ceil_div(slice_y ? a.ox : a.oy, TILE_Y) * ceil_div(a.oz, TILE_Z);
   const bool can_pair = (!L.fold || fold_pair) && !a.pool && spatial_min >= 2 && L.nt % 16 == 0 &&
                         L.nt / 8 <= 256 && out_ok && (pair_env == 1 || pair_env == 2);
   int rc = tc_configure(L, a.k, slice_y ? a.oy : a.ox, other_tiles, sms, a.reps, stg_bytes,

@@ -200,3 +200,34 @@ def test_plan_batch_bit_identical_to_sequential_runs():
         for a, g in zip(alone, got):
             for n in a:
                 assert torch.equal(a[n], g[n]), n
+
+
+@pytest.mark.parametrize("batch", ["2", "3"])
+def test_patch_batching_bit_identical(batch, monkeypatch):
+    """DeviceTiler runs `batch` patches per launch (plan.rebatch): the deep
+    levels of several patches share kernels; each patch's output is exactly
+    the single-patch result (a short last group repeats its last patch)."""
+    spec, store = C.config5(patch=(4, 32, 32), feats=(8, 12, 16))
+    plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
+    vol = np.random.default_rng(1).uniform(0, 1, (1, 1, 7, 80, 70)).astype(np.float32)
+    grid = P.grid_for(plan, vol.shape[2:], overlap=0)
+    monkeypatch.setenv("VOXPLAN_PATCH_BATCH", "1")
+    want = P.run_tiled(plan, vol, grid=grid)
+    monkeypatch.setenv("VOXPLAN_PATCH_BATCH", batch)
+    got = P.run_tiled(plan, vol, grid=grid)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_rebatched_plan_equals_per_volume_runs():
+    """plan.rebatch on a U-net with pooling, deconv, crop + concat: entry b
+    of the batched run equals the batch-1 run on volume b, bit for bit."""
+    from paper_1903_07525_b200.plan import rebatch
+    spec, store = _small(4)
+    plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
+    xs = [C.make_input(spec, s, 0.0, 1.0) for s in (0, 1)]
+    one = P.PlanRunner(plan)
+    want = [next(iter(one.run(x).values())) for x in xs]
+    two = P.PlanRunner(rebatch(plan, 2))
+    got = next(iter(two.run(np.concatenate(xs, axis=0)).values()))
+    for b in range(2):
+        np.testing.assert_array_equal(got[b:b + 1], want[b])

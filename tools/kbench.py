@@ -14,6 +14,9 @@ torch.cuda.set_device(dev)
 res = {}
 only = os.environ.get("ONLY")
 REPS = int(os.environ.get("REPS", "1"))
+_act = os.environ.get("ACT", "elu")
+FA = None if _act == "none" else (_act, 1.0)
+F32OUT = os.environ.get("F32OUT") == "1"   # fp32 NCDHW output (the network-output epilogue)
 spatial = tuple(int(v) for v in os.environ.get("SPATIAL", "32,128,128").split(","))
 for k in ((3, 3, 3), (1, 3, 3)):
     for c in (8, 16, 32, 64, 128):
@@ -24,17 +27,18 @@ for k in ((3, 3, 3), (1, 3, 3)):
         x = D.empty_blocked(1, c, spatial)
         x.t.copy_(torch.randn(x.t.shape, device=dev).to(torch.bfloat16))
         x.t[..., (c % 8 or 8):] = 0 if c % 8 else x.t[..., 8:]
-        out = D.empty_blocked(1, c, spatial)
+        out = (D.standard(torch.empty((1, c) + spatial, device=dev)) if F32OUT
+               else D.empty_blocked(1, c, spatial))
         w = (rng.standard_normal((c, c) + k) * 0.05).astype(np.float32)
         pk = K.pack_conv(w, np.zeros(c, np.float32))
         pad = tuple(v // 2 for v in k)
         s = torch.cuda.Stream()
         with torch.cuda.stream(s):
-            K.conv3d(x, pk, out, pad=pad, fused_act=("elu", 1.0))
+            K.conv3d(x, pk, out, pad=pad, fused_act=FA)
         s.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
-            K.conv3d(x, pk, out, pad=pad, fused_act=("elu", 1.0))
+            K.conv3d(x, pk, out, pad=pad, fused_act=FA)
         flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
         times = []
         for it in range(12):
