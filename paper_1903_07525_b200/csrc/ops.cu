@@ -185,6 +185,53 @@ __global__ void pool_kernel(DView in, DView out, int kx, int ky, int kz, int sx,
   }
 }
 
+// Max pool fast path: bf16 blocked in/out, window (KX, 2, 2) = stride (the
+// U-net pools: 2x2x2 in config 4, 1x2x2 in config 5).  All 4*KX 16-byte
+// window loads are issued before the reduction (the generic kernel's runtime
+// window loop exposes each load's latency), then the same seeded
+// (dx, dy, dz)-order comparison as pool_kernel / ops.pool (NaN-propagating).
+template <int KX>
+__global__ void pool_max_bf16_kernel(DView in, DView out) {
+  pdl_begin();
+  ChunkIdx k;
+  const int nch = (out.c + 7) >> 3;
+  if (!chunk_index3(nch, out.y, out.z, k)) return;
+  const __nv_bfloat16 *base = static_cast<const __nv_bfloat16 *>(in.data) + k.b * in.s[0] +
+                              k.ch * in.s[1] + (k.x * KX) * in.s[2] + (2 * k.y) * in.s[3] +
+                              (2 * k.z) * in.s[4];
+  uint4 v[KX * 4];
+#pragma unroll
+  for (int dx = 0; dx < KX; ++dx)
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+      for (int dz = 0; dz < 2; ++dz)
+        v[(dx * 2 + dy) * 2 + dz] = __ldg(reinterpret_cast<const uint4 *>(
+            base + dx * in.s[2] + dy * in.s[3] + dz * in.s[4]));
+  float r[8];
+  {
+    const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v[0]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(h[i]);
+      r[2 * i] = f.x;
+      r[2 * i + 1] = f.y;
+    }
+  }
+#pragma unroll
+  for (int w = 1; w < KX * 4; ++w) {
+    const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v[w]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(h[i]);
+      r[2 * i] = (f.x > r[2 * i] || f.x != f.x) ? f.x : r[2 * i];
+      r[2 * i + 1] = (f.y > r[2 * i + 1] || f.y != f.y) ? f.y : r[2 * i + 1];
+    }
+  }
+  zero_tail_lanes(r, k.ch, out.c);
+  st_chunk(out, k.b, k.ch, k.x, k.y, k.z, r);
+}
+
 // ------------------------------------------------------------------ eltwise
 __global__ void eltwise_kernel(DView a, DView b, DView out, int op) {
   pdl_begin();
@@ -593,6 +640,15 @@ int launch_zero(const DView &dst, cudaStream_t s) {
 }
 int launch_pool(const DView &in, const DView &out, const int *w, const int *st, int mode,
                 cudaStream_t s) {
+  const bool fast = mode == VXB_POOL_MAX && blocked_bf16(in) && blocked_bf16(out) &&
+                    (w[0] == 1 || w[0] == 2) && w[1] == 2 && w[2] == 2 && st[0] == w[0] &&
+                    st[1] == 2 && st[2] == 2 && in.s[4] == 8 && out.s[4] == 8;
+  if (fast)
+    return check_cuda(w[0] == 2 ? launch_pdl(pool_max_bf16_kernel<2>, grid3(out, 256), dim3(256),
+                                             0, s, in, out)
+                                : launch_pdl(pool_max_bf16_kernel<1>, grid3(out, 256), dim3(256),
+                                             0, s, in, out),
+                      "pool_max_bf16_kernel");
   return check_cuda(launch_pdl(pool_kernel, grid3(out, 256), dim3(256), 0, s, in, out, w[0], w[1],
                                w[2], st[0], st[1], st[2], mode),
                     "pool_kernel");
