@@ -1017,7 +1017,7 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
             }
           } else if (FASTOUT) {
             if (ov.blocked) {
-              if (valid) store8_bf16_blocked(ov, obase + (c0 >> 3) * ov.s[1], r);
+              if (valid && !(p.dbg_mode & 512)) store8_bf16_blocked(ov, obase + (c0 >> 3) * ov.s[1], r);
             } else if (valid) {
               // fused unpack: fp32 NCDHW network output written directly
               // (one pointer walked across the channel planes)
@@ -1054,14 +1054,14 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
         if (warp == 3 && lane == 0 && item == sub) dbg_mark(p, it, 7);
         if (nxt < items) tmem_ld16_issue(taddr_of(nxt), rb);
         if (BASE) base_get(item, qa, bv);
-        finish(item, ra, bv);
+        if (!(p.dbg_mode & 256)) finish(item, ra, bv);
         if (braw && item + 2 * NSUB < items) base_issue(item + 2 * NSUB, qa);
         if (nxt >= items) break;
         const int nn = nxt + NSUB;
         tmem_wait_ld16(rb);
         if (nn < items) tmem_ld16_issue(taddr_of(nn), ra);
         if (BASE) base_get(nxt, qb, bv);
-        finish(nxt, rb, bv);
+        if (!(p.dbg_mode & 256)) finish(nxt, rb, bv);
         if (braw && nxt + 2 * NSUB < items) base_issue(nxt + 2 * NSUB, qb);
         item = nn;
       }

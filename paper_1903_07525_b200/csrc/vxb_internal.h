@@ -83,7 +83,8 @@ struct TcParams {
   unsigned long long *dbg;     // optional per-tile phase timestamps (VXB_TC_DEBUG)
   int dbg_mode;                // VXB_TC_DBGMODE (timing experiments, wrong results): 1 no
                                // epilogue, 2 no A loads, 4 no B loads, 8 no MMAs (resident B),
-                               // 16 folded MMAs at N = nt, 64 no fp32 conversion, 128 no fp32 TMA
+                               // 16 folded MMAs at N = nt, 64 no fp32 conversion, 128 no fp32
+                               // TMA, 256 epilogue TMEM loads only, 512 no bf16 output stores
 };
 
 struct TcMaps {
