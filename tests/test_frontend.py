@@ -174,3 +174,30 @@ def test_full_size_config_shapes():
     shapes = P.validate_shapes(*C.config5())
     assert shapes["prob"] == (1, 3, 18, 192, 192)
     assert abs(C.conv_flops(C.config5()[0]) / 663552 - 322e3) / 322e3 < 0.05
+
+
+def test_rebatch_scales_every_batch_dim():
+    """plan.rebatch (tiled executor: several patches per launch) sets dims[0]
+    of every step input/output/base, plan input and output to the batch,
+    scales the buffer table, and keeps everything else (weights, params,
+    fused flags) identical; only batch-1 plans are accepted."""
+    from paper_1903_07525_b200 import configs as C
+    from paper_1903_07525_b200.errors import PlanError
+    from paper_1903_07525_b200.plan import rebatch
+    spec, store = C.config5(patch=(6, 48, 48), feats=(8, 12, 16, 20))
+    plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
+    b = rebatch(plan, 3)
+    assert [d[2] for d in b.inputs] == [(3,) + tuple(d[2][1:]) for d in plan.inputs]
+    assert [d[2] for d in b.outputs] == [(3,) + tuple(d[2][1:]) for d in plan.outputs]
+    for s0, s1 in zip(plan.steps, b.steps):
+        assert s1.output.dims == (3,) + tuple(s0.output.dims[1:])
+        assert [x.dims for x in s1.inputs] == [(3,) + tuple(x.dims[1:]) for x in s0.inputs]
+        assert (s1.base is None) == (s0.base is None)
+        if s1.base is not None:
+            assert s1.base.dims == (3,) + tuple(s0.base.dims[1:])
+        assert (s1.kind, s1.name, s1.params, s1.fused_act, s1.additive, s1.base_scale) == \
+            (s0.kind, s0.name, s0.params, s0.fused_act, s0.additive, s0.base_scale)
+    assert b.arena_elements == 3 * plan.arena_elements
+    assert b.weights is plan.weights
+    with pytest.raises(PlanError):
+        rebatch(b, 2)
