@@ -1112,13 +1112,16 @@ static int launch_variant(const TcParams &p, const TcMaps &maps, int grid, cudaS
   cfg.blockDim = dim3(tc_threads(F32IN));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   int na = 0;
   if (pdl_enabled()) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
+  attr[na].id = cudaLaunchAttributePriority;
+  attr[na].val.priority = launch_priority(false);
+  ++na;
   if (p.cluster > 1) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
     attr[na].val.clusterDim.x = p.cluster;

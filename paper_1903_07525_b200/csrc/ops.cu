@@ -621,8 +621,8 @@ int launch_copy(const DView &src, const DView &dst, cudaStream_t s, bool indepen
   if (std_f32_vec4(src) && blocked_bf16(dst)) {
     dim3 g((dst.y * (dst.z >> 2) + 127) / 128, dst.x, dst.n * ((dst.c + 7) / 8));
     if (independent)
-      return check_cuda(launch_pdl(pack_std_f32_indep_kernel, g, dim3(128), 0, s, src, dst,
-                                   pack_trigger()),
+      return check_cuda(launch_pdl_prio(pack_std_f32_indep_kernel, g, dim3(128), 0, s, true, src,
+                                        dst, pack_trigger()),
                         "pack_std_f32_indep_kernel");
     return check_cuda(launch_pdl(pack_std_f32_kernel, g, dim3(128), 0, s, src, dst),
                       "pack_std_f32_kernel");

@@ -39,6 +39,15 @@ static int env_int(const char *name, int dflt) {
 }
 
 bool pdl_enabled() { return env_int("VXB_PDL", 1) != 0; }
+int launch_priority(bool background) {
+  static int lo = 0, hi = 0, init = 0;
+  if (!init) {
+    if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) lo = hi = 0;
+    if (!env_int("VXB_PRIORITIES", 1)) lo = hi = 0;
+    init = 1;
+  }
+  return background ? lo : hi;
+}
 
 static DView to_dview(const vxb_tensor &t) {
   DView v;
