@@ -293,7 +293,8 @@ static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, lon
   }
   const int slab = L.slab;
   // fp32-input convs buffer their input in the staging ring: two A stages
-  int na_cap = reserved ? 2 : std::max(2, std::min(6, env_int("VXB_TC_NA", 3)));
+  int na_cap = reserved ? std::max(2, std::min(4, env_int("VXB_TC_F32IN_NA", 2)))
+                        : std::max(2, std::min(6, env_int("VXB_TC_NA", 3)));
   for (;;) {
     const int sx = L.fold == 2 ? TILE_Y : c.bx, sy = L.fold == 2 ? c.bx : TILE_Y;
     const int hx = sx + k[0] - 1, hy = sy + k[1] - 1, hz = TILE_Z + k[2] - 1;
@@ -465,7 +466,7 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
   const bool f32in = x0.dtype == VXB_F32 && !x0.blocked;
   // staging ring: ~80 KB of fp32 boxes in flight covers the TMA latency at
   // the input rate of the low-fmap convs (each box <= 16 KB: xb x-slices)
-  const int kStgBudget = 80 * 1024;
+  const int kStgBudget = env_int("VXB_TC_STG_KB", 80) * 1024;
   int stg_bytes = 0, hzb = 0, zshift = 0;
   if (f32in) {
     if (a.in[1] || a.has_base)
