@@ -476,8 +476,9 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
     }
   const int cpad = p.n_tiles * p.nt;
   for (int c = threadIdx.x; c < cpad; c += blockDim.x) {
-    s_bias[c] = c < p.cout ? p.bias[c] : 0.f;
-    s_scale[c] = (c < p.cout && p.scale) ? p.scale[c] : 1.f;
+    const int cr = p.rep_n ? c % p.rep_n : c;   // taps in N: column -> channel of its tap
+    s_bias[c] = cr < p.cout ? p.bias[cr] : 0.f;
+    s_scale[c] = (cr < p.cout && p.scale) ? p.scale[cr] : 1.f;
   }
   fence_proxy_async_smem();
 
@@ -877,10 +878,20 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
       const int sc0 = p.slice_y ? tc.y0 : tc.x0, slim = p.slice_y ? p.oy : p.ox;
       const bool yz_ok = rc < (p.slice_y ? p.ox : p.oy) && z < p.oz && !tc.dummy;
       const int ra_dim = p.slice_y ? 2 : 3, sl_dim = p.slice_y ? 3 : 2;
-      const long long orow =
-          p.out_rep_off[tc.rep] + tc.b * ov.s[0] + rc * ov.s[ra_dim] + z * ov.s[4];
-      const long long brow =
-          p.base_rep_off[tc.rep] + tc.b * bvw.s[0] + rc * bvw.s[ra_dim] + z * bvw.s[4];
+      // (replica offsets are added per item: with taps in N (rep_n) every
+      // 16-column item belongs to one tap)
+      const long long orow = tc.b * ov.s[0] + rc * ov.s[ra_dim] + z * ov.s[4];
+      const long long brow = tc.b * bvw.s[0] + rc * bvw.s[ra_dim] + z * bvw.s[4];
+      // item column -> (replica, first channel of the item)
+      auto item_rep = [&](int cc, int &rep, int &ch) {
+        if (p.rep_n) {
+          rep = cc / p.rep_n;
+          ch = cc - rep * p.rep_n;
+        } else {
+          rep = tc.rep;
+          ch = tc.nt * p.nt + cc;
+        }
+      };
       const uint32_t tbase =
           tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * acc_stride + p.slice0_col;
 
@@ -893,15 +904,16 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
       // ahead (the first ones before the accumulator is even ready); other
       // layouts are read at use
       auto base_issue = [&](int item, uint4 (&d)[2]) {
-        int s, cc;
+        int s, cc, rep, ch;
         split_item(item, s, cc);
+        item_rep(cc, rep, ch);
         const int x = sc0 + s;
         const bool ok = yz_ok && x < slim;
         const __nv_bfloat16 *bp = static_cast<const __nv_bfloat16 *>(bvw.data) + brow +
-                                  x * bvw.s[sl_dim];
+                                  p.base_rep_off[rep] + x * bvw.s[sl_dim];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int c0 = tc.nt * p.nt + cc + h * 8;
+          const int c0 = ch + h * 8;
           d[h] = make_uint4(0u, 0u, 0u, 0u);
           if (ok && c0 < p.cout) d[h] = __ldg(reinterpret_cast<const uint4 *>(bp + (c0 >> 3) * bvw.s[1]));
         }
@@ -920,41 +932,45 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
           }
           return;
         }
-        int s, cc;
+        int s, cc, rep, ch;
         split_item(item, s, cc);
+        item_rep(cc, rep, ch);
         const int x = sc0 + s;
         const bool ok = yz_ok && x < slim;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           float t8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          const int c0 = tc.nt * p.nt + cc + h * 8;
+          const int c0 = ch + h * 8;
           if (ok && c0 < p.cout)
-            load8(bvw, brow + x * bvw.s[sl_dim] + (bvw.blocked ? (c0 >> 3) * bvw.s[1] : c0 * bvw.s[1]),
+            load8(bvw, brow + p.base_rep_off[rep] + x * bvw.s[sl_dim] +
+                           (bvw.blocked ? (c0 >> 3) * bvw.s[1] : c0 * bvw.s[1]),
                   bvw.blocked, t8);
 #pragma unroll
           for (int i = 0; i < 8; ++i) bv[h * 8 + i] = t8[i];
         }
       };
       auto finish = [&](int item, const uint32_t (&rv)[16], const float (&bv)[16]) {
-        int s, cc;
+        int s, cc, rep, ch;
         split_item(item, s, cc);
+        item_rep(cc, rep, ch);
         const int x = sc0 + s;
         const bool valid = yz_ok && x < slim;   // stores only; all lanes run the math
-        const long long obase = orow + x * ov.s[sl_dim];
+        const long long obase = orow + p.out_rep_off[rep] + x * ov.s[sl_dim];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int c0 = tc.nt * p.nt + cc + h * 8;
+          const int c0 = ch + h * 8;                       // output channel
+          const int col = tc.nt * p.nt + cc + h * 8;       // bias / scale column
           if (c0 >= p.cout) break;
           const int nvalid = min(8, p.cout - c0);
-          const float4 b0 = *reinterpret_cast<const float4 *>(s_bias + c0);
-          const float4 b1 = *reinterpret_cast<const float4 *>(s_bias + c0 + 4);
+          const float4 b0 = *reinterpret_cast<const float4 *>(s_bias + col);
+          const float4 b1 = *reinterpret_cast<const float4 *>(s_bias + col + 4);
           const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
           float r[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) r[i] = __uint_as_float(rv[h * 8 + i]) + bb[i];
           if (BASE) {
-            const float4 s0 = *reinterpret_cast<const float4 *>(s_scale + c0);
-            const float4 s1 = *reinterpret_cast<const float4 *>(s_scale + c0 + 4);
+            const float4 s0 = *reinterpret_cast<const float4 *>(s_scale + col);
+            const float4 s1 = *reinterpret_cast<const float4 *>(s_scale + col + 4);
             const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
             for (int i = 0; i < 8; ++i) r[i] = fmaf(sc[i], bv[h * 8 + i], r[i]);

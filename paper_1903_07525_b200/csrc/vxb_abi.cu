@@ -436,6 +436,7 @@ struct TcLaunch {
   int k[3], pad[3];
   int ox, oy, oz, nb;
   int reps;
+  int rep_n;        // > 0: the reps ride in N (rep_n columns each), one tile computes all
   long long out_rep_off[MAX_REPS], base_rep_off[MAX_REPS];
   EpiView out, base;
   int has_base;
@@ -449,8 +450,12 @@ struct TcLaunch {
   EpiView pool_out;
 };
 
-static int run_tc(const TcLaunch &a, cudaStream_t stream) {
-  TcLayout L = tc_layout(a.cin0, a.cin1, a.cout, a.k, a.allow_fold, a.nt_cap > 0 ? a.nt_cap : 256);
+static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
+  TcLaunch a = a_in;
+  const int n_cols = a.rep_n ? a.reps * a.rep_n : a.cout;   // GEMM N over all taps in N
+  const int rep_offsets = a.reps;
+  if (a.rep_n) a.reps = 1;                                   // one tile covers every tap
+  TcLayout L = tc_layout(a.cin0, a.cin1, n_cols, a.k, a.allow_fold, a.nt_cap > 0 ? a.nt_cap : 256);
   TcConfig c;
   const int slice_y = L.fold == 2;
   int sms = device_sms();
@@ -643,6 +648,8 @@ static int run_tc(const TcLaunch &a, cudaStream_t stream) {
     p.out_rep_off[r] = a.out_rep_off[r];
     p.base_rep_off[r] = a.base_rep_off[r];
   }
+  p.rep_n = a.rep_n;
+  (void)rep_offsets;
   p.cout = a.cout;
   p.act = a.act;
   p.alpha = a.alpha;
@@ -953,8 +960,26 @@ static bool deconv_tc(const int k[3], const int stride[3], int path) {
   return path != VXB_PATH_DIRECT && deconv_tc_ok(k, stride);
 }
 
+// Taps in N: with k == stride every output voxel takes exactly one tap, so a
+// k-tap deconv is one 1x1x1 GEMM with N = taps x round_up(cout, 16): the
+// input tile is read once for all taps and the epilogue sends each 16-column
+// item to its tap's (strided) output voxels.  Used when N fits one MMA
+// (config 5's 1x2x2 deconvs: 4 x 32..64); otherwise every tap is a tile
+// replica (config 4's 2x2x2 deconvs at 128-512 fmaps).
+static int deconv_rep_n(int cout, const int k[3], const int stride[3], int path) {
+  if (!deconv_tc(k, stride, path)) return 0;
+  const int reps = k[0] * k[1] * k[2];
+  const int ntr = round_up(cout, 16);
+  if (reps < 2 || reps * ntr > 256 || !env_int("VXB_DECONV_REPN", 1)) return 0;
+  return ntr;
+}
+
 size_t vxb_deconv_weights_bytes(int cin, int cout, const int k[3], const int stride[3],
                                 int path) {
+  if (const int rn = deconv_rep_n(cout, k, stride, path)) {
+    int one[3] = {1, 1, 1};
+    return tc_bytes_per_rep(tc_layout(cin, 0, k[0] * k[1] * k[2] * rn, one));
+  }
   if (deconv_tc(k, stride, path)) {
     int one[3] = {1, 1, 1};
     return static_cast<size_t>(k[0] * k[1] * k[2]) * tc_bytes_per_rep(tc_layout(cin, 0, cout, one));
@@ -974,6 +999,19 @@ int vxb_deconv_pack_weights(const float *w, int cin, int cout, const int k[3], c
     return VXB_OK;
   }
   int one[3] = {1, 1, 1};
+  if (const int rn = deconv_rep_n(cout, k, stride, path)) {
+    // column co' = tap * rn + co, taps in (dx, dy, dz) order
+    const int reps = k[0] * k[1] * k[2];
+    TcLayout L = tc_layout(cin, 0, reps * rn, one);
+    auto wtap = [&](int cop, int ci, int, int, int) {
+      const int r = cop / rn, co = cop - r * rn;
+      if (co >= cout) return 0.f;
+      const int dz = r % k[2], dy = (r / k[2]) % k[1], dx = r / (k[2] * k[1]);
+      return w[((((static_cast<size_t>(co) * cin) + ci) * k[0] + dx) * k[1] + dy) * k[2] + dz];
+    };
+    tc_pack(L, cin, 0, reps * rn, one, wtap, static_cast<uint8_t *>(dst));
+    return VXB_OK;
+  }
   TcLayout L = tc_layout(cin, 0, cout, one);
   size_t per = tc_bytes_per_rep(L);
   int r = 0;
@@ -1019,6 +1057,7 @@ int vxb_deconv3d(const vxb_deconv_desc *d, void *stream) {
     a.oz = d->in.z;
     a.nb = d->in.n;
     a.reps = d->k[0] * d->k[1] * d->k[2];
+    a.rep_n = deconv_rep_n(d->cout, d->k, d->stride, d->path);
     a.out = to_epi(d->out);
     for (int i = 0; i < 3; ++i) a.out.s[2 + i] = d->out.s[2 + i] * d->stride[i];
     a.has_base = additive;

@@ -74,6 +74,7 @@ struct TcParams {
   const float *bias, *scale;
   EpiView out, base;
   long long out_rep_off[MAX_REPS], base_rep_off[MAX_REPS];
+  int rep_n;                   // deconv taps in N: columns per tap (0 = taps are tile replicas)
   int cout, act;
   float alpha;
   int has_base;

@@ -497,3 +497,42 @@ def test_deconv_golden(golden_ops, i):
         torch.cuda.synchronize()
         want = R.deconv3d(R.bf16_round(x), R.bf16_round(w), b, tuple(s))
         assert R.normalized_error(D.to_host_standard(out), want)[0] < BF16_TOL
+
+
+@pytest.mark.parametrize("k", [(1, 2, 2), (2, 2, 2)])
+@pytest.mark.parametrize("cin,cout", [(36, 28), (80, 64), (12, 20)])
+def test_deconv_taps_in_n_matches_replicas(k, cin, cout, monkeypatch):
+    """k == stride deconvs with taps x round_up(cout,16) <= 256 run as ONE
+    1x1x1 GEMM with every tap in N (the epilogue routes each 16-column item
+    to its tap's strided output voxels); the sums are the same MMAs as the
+    one-replica-per-tap walk, so results are bit-identical, with and without
+    the fused skip add + activation."""
+    import torch
+    D, K = _dev()
+    rng = np.random.default_rng(cin + cout + k[0])
+    x = rng.uniform(-1, 1, (2, cin, 3, 9, 10)).astype(np.float32)
+    w = (rng.standard_normal((cout, cin) + k) * 0.2).astype(np.float32)
+    b = rng.standard_normal(cout).astype(np.float32)
+    osp = tuple(s * kk for s, kk in zip(x.shape[2:], k))
+    base = rng.uniform(-1, 1, (2, cout) + osp).astype(np.float32)
+    scale = rng.uniform(0.5, 1.5, cout).astype(np.float32)
+
+    def run(with_base):
+        pk = K.pack_deconv(w, b, stride=k, base_scale=scale if with_base else None)
+        out = D.empty_blocked(2, cout, osp)
+        K.deconv3d(D.to_device_blocked(x), pk, out,
+                   base=D.to_device_blocked(base) if with_base else None,
+                   fused_act=("elu", 1.0) if with_base else None)
+        torch.cuda.synchronize()
+        return D.to_host_standard(out)
+
+    for with_base in (False, True):
+        monkeypatch.setenv("VXB_DECONV_REPN", "1")
+        fused = run(with_base)
+        monkeypatch.setenv("VXB_DECONV_REPN", "0")
+        plain = run(with_base)
+        np.testing.assert_array_equal(fused, plain)
+        want = R.deconv3d(R.bf16_round(x), R.bf16_round(w), b, k)
+        if with_base:
+            want = R.activation(want + scale.reshape(1, -1, 1, 1, 1) * R.bf16_round(base), "elu")
+        assert R.normalized_error(fused, want)[0] < BF16_TOL

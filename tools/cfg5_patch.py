@@ -1,4 +1,5 @@
-"""One config-5 patch through PlanRunner.run_device (graph), for launch lists."""
+"""One config-5 patch (BATCH patches per launch) through PlanRunner.run_device
+(graph), for launch lists."""
 import os, sys
 import numpy as np
 import torch
@@ -9,8 +10,12 @@ from paper_1903_07525_b200 import configs as C
 dev = torch.device("cuda", 0)
 spec, store = C.config5()
 plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
+B = int(os.environ.get("BATCH", "1"))          # patches per launch (plan.rebatch)
+if B > 1:
+    from paper_1903_07525_b200.plan import rebatch
+    plan = rebatch(plan, B)
 r = P.PlanRunner(plan, device=dev)
-x = C.make_input(spec, 0, 0.0, 1.0)
+x = np.concatenate([C.make_input(spec, i, 0.0, 1.0) for i in range(B)], axis=0)
 bufs = r.input_buffers()
 bufs[plan.inputs[0][0]].copy_(torch.from_numpy(x))
 for _ in range(int(os.environ.get("ITERS", "3"))):
