@@ -314,11 +314,29 @@ def kernel_roofline(L, dev, peaks):
     graph K times between events on the graph's stream."""
     import torch
     from paper_1903_07525_b200.netspec import LayerKind
+    from paper_1903_07525_b200.formats import ROLE_KERNEL
     runner = L["runner"]
-    # the conv call is the op between the input pack and output unpack
-    conv_calls = [c for c, (kind, st, info) in zip(runner.op_calls, runner._ops)
-                  if kind is LayerKind.CONVOLUTION]
-    call = conv_calls[0]
+    plan = L["plan"]
+    # the network's largest conv (by FLOPs): its own algorithmic FLOPs and
+    # bytes (bf16 blocked input, output bf16 or the fused fp32 network output,
+    # residual operand if any; weights negligible)
+    out_vals = {id(v): name for name, v in runner._out_values.items()}
+    best = None
+    for c, (kind, st, info) in zip(runner.op_calls, runner._ops):
+        if kind is not LayerKind.CONVOLUTION:
+            continue
+        kshape = plan.weights.tensor(st.name, ROLE_KERNEL).shape
+        n, cout, ox, oy, oz = st.output.dims
+        f = 2.0 * float(np.prod(kshape)) * n * ox * oy * oz
+        # input tensors read (a fused concat reads both segments)
+        ins = list(info["segments"][:2]) if "segments" in info else [info["x"]]
+        in_b = 2.0 * sum(v.dims[1] * float(np.prod(v.dims[2:])) * v.dims[0] for v in ins)
+        fused = out_vals.get(id(info["out"])) in runner._fused_outputs
+        out_b = (4.0 if fused else 2.0) * cout * n * ox * oy * oz
+        base_b = 2.0 * cout * n * ox * oy * oz if st.additive else 0.0
+        if best is None or f > best[1]:
+            best = (c, f, in_b + out_b + base_b, st.name)
+    call, flops, alg_bytes, conv_name = best
     s = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(s):
         call()
@@ -338,14 +356,6 @@ def kernel_roofline(L, dev, peaks):
         e1.record(s)
     s.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    flops = L["flops"]
-    n, c, x, y, z = L["plan"].inputs[0][2]
-    cout = L["plan"].steps[-1].output.dims[1]
-    # bf16 blocked input (packed by the preceding kernel); the output is the
-    # network's fp32 NCDHW tensor when the runner fused the unpack into the
-    # conv epilogue, else bf16 blocked; weights negligible
-    out_b = 4 if runner._fused_outputs else 2
-    alg_bytes = (c * 2 + cout * out_b) * x * y * z
     ai = flops / alg_bytes
     ridge = peaks["bf16"] * 1e12 / (peaks["hbm"] * 1e9)
     if ai >= ridge:
@@ -356,7 +366,9 @@ def kernel_roofline(L, dev, peaks):
         achieved = alg_bytes / (ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm"]}
-    roof.update({"kernel": "conv3d_tc_kernel (%s)" % L["name"], "ms_per_launch": ms,
+    label = L["name"] if conv_name == "conv" or len(runner._ops) <= 2 else \
+        "%s/%s" % (L["name"], conv_name)
+    roof.update({"kernel": "conv3d_tc_kernel (%s)" % label, "ms_per_launch": ms,
                  "alg_flops": flops, "alg_bytes": alg_bytes, "peak_source": peaks["source"],
                  "traffic": ncu_traffic(L["name"])})
     return roof
