@@ -629,7 +629,8 @@ class PlanBatch:
         if reorder and len(order) > 2:
             work = [_conv_flops(r.plan) for r in self.runners]
             order.sort(key=lambda i: -work[i])
-            order = order[-1:] + order[:-1]
+            if os.environ.get("VXB_BATCH_ORDER", "small_first") == "small_first":
+                order = order[-1:] + order[:-1]
         self.order = order
         self.device = dev
         self.stream = torch.cuda.Stream(device=dev)
