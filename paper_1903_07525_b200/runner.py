@@ -91,6 +91,7 @@ class PlanRunner:
             self._allocate()
             self._bind()
         self._graph = None
+        self._indep_inputs = False       # set by PlanBatch while it captures
         self.launches = len(self._calls)
 
     # ------------------------------------------------------------ lowering
@@ -326,13 +327,15 @@ class PlanRunner:
                 fused_in[id(rs[0][1])] = standard(self._in_std[name])
                 continue
             src = standard(self._in_std[name])
-            # the pack reads a network input and writes a buffer only this
-            # network's later steps read: independent of the kernel before it
-            # (in a PlanBatch, the previous network's last conv)
+            # The pack reads a network input and writes a buffer only this
+            # network's later steps read.  Inside a PlanBatch graph the kernel
+            # before it is another network's, so it is launched independent
+            # (no grid-dependency wait, may run beside that kernel); alone it
+            # keeps the ordinary wait, since the input may have just been
+            # written by a kernel (a strided torch copy) it must not overtake.
             if os.environ.get("VXB_DEBUG_SKIP_INPUT_PACK") == "1":
                 continue        # timing experiments only: inputs never reach the network
-            indep = os.environ.get("VXB_DEBUG_PACK_DEPENDENT") != "1"
-            calls.append(lambda s=src, d=v.dt, i=indep: _copy(s, d, independent=i))
+            calls.append(lambda s=src, d=v.dt: _copy(s, d, independent=self._indep_inputs))
         n_in = len(calls)
         self._n_in_calls = n_in          # the input packs come first (PlanBatch side stream)
         self.fused_inputs = len(fused_in)
@@ -670,13 +673,20 @@ class PlanBatch:
                 for i in self.order:
                     self.runners[i]._launch_all()   # warm-up: first launches configure kernels
             self.stream.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.device(self.device), torch.cuda.graph(g, stream=self.stream):
-                if two:
-                    self._capture_two_streams()
-                else:
-                    for i in self.order:
-                        self.runners[i]._launch_all()
+            indep = os.environ.get("VXB_DEBUG_PACK_DEPENDENT") != "1"
+            for r in self.runners:
+                r._indep_inputs = indep
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.device(self.device), torch.cuda.graph(g, stream=self.stream):
+                    if two:
+                        self._capture_two_streams()
+                    else:
+                        for i in self.order:
+                            self.runners[i]._launch_all()
+            finally:
+                for r in self.runners:
+                    r._indep_inputs = False
             self._graph = g
         with torch.cuda.stream(self.stream):
             self._graph.replay()
