@@ -224,6 +224,15 @@ int vxb_copy(const vxb_tensor *src, const vxb_tensor *dst, void *stream);
  * convolution (runner.py). */
 #define VXB_COPY_INDEPENDENT 1
 int vxb_copy_ex(const vxb_tensor *src, const vxb_tensor *dst, int flags, void *stream);
+/* z-window pack of a 1-channel fp32 network input for a conv with kz z-taps
+ * and z padding pz (the first layer of both U-nets; blocked.to_blocked,
+ * blocked.py:209-231, followed by the conv's own z taps): lane l of dst voxel
+ * (x, y, z) = src(x, y, z + l - pz) (zero outside), lanes >= kz zero, so the
+ * conv runs as a (kx, ky, 1) kernel over kz lanes with
+ * w'(co, l, dx, dy, 0) = w(co, 0, dx, dy, l).  dst: bf16 blocked, c == kz,
+ * z == src z + 2 pz - kz + 1.  flags: VXB_COPY_INDEPENDENT as for vxb_copy_ex. */
+int vxb_pack_zwin(const vxb_tensor *src, const vxb_tensor *dst, int kz, int pz, int flags,
+                  void *stream);
 /* fill a whole view (all lanes) with zeros */
 int vxb_zero(const vxb_tensor *t, void *stream);
 

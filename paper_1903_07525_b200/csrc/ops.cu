@@ -572,6 +572,43 @@ __global__ void pack_std_f32_indep_kernel(DView src, DView dst, int trigger) {
   pack_item(src, dst, b, ch, x, y, z);
 }
 
+// z-window pack of a single-channel network input for a conv with kz z-taps
+// (pad pz): lane l of output voxel (x, y, z) holds in(x, y, z + l - pz), lanes
+// >= kz and out-of-range taps zero.  The conv then runs as a (kx, ky, 1)
+// kernel over kz "channels" (w'(co, l, dx, dy, 0) = w(co, 0, dx, dy, l)):
+// half the K steps of the 1-channel conv, whose 8-lane chunks were 7/8
+// padding.  Each thread writes 4 consecutive z (4 x 16-byte chunks).
+template <bool INDEP>
+__global__ void pack_zwin_kernel(DView src, DView dst, int kz, int pz, int trigger) {
+  if (!INDEP) pdl_begin();
+  else if (trigger) pdl_trigger();
+  const int zq = (dst.z + 3) >> 2;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= dst.y * zq) return;
+  const int y = i / zq, z0 = (i - y * zq) * 4, x = blockIdx.y, b = blockIdx.z;
+  const float *row = static_cast<const float *>(src.data) + b * src.s[0] + x * src.s[2] +
+                     y * src.s[3];
+  float v[4 + 8 - 1];
+#pragma unroll
+  for (int j = 0; j < 11; ++j) {
+    const int zz = z0 + j - pz;
+    v[j] = (j < 3 + kz && zz >= 0 && zz < src.z) ? row[zz * src.s[4]] : 0.f;
+  }
+  __nv_bfloat16 *o = static_cast<__nv_bfloat16 *>(dst.data) + b * dst.s[0] + x * dst.s[2] +
+                     y * dst.s[3];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (z0 + q >= dst.z) break;
+    uint4 u;
+    __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      h[k] = __floats2bfloat162_rn(2 * k < kz ? v[q + 2 * k] : 0.f,
+                                   2 * k + 1 < kz ? v[q + 2 * k + 1] : 0.f);
+    *reinterpret_cast<uint4 *>(o + (z0 + q) * dst.s[4]) = u;
+  }
+}
+
 // The reverse at the output boundary: bf16 blocked -> fp32 NCDHW.
 __global__ void unpack_std_f32_kernel(DView src, DView dst) {
   pdl_begin();
@@ -634,6 +671,16 @@ int launch_copy(const DView &src, const DView &dst, cudaStream_t s, bool indepen
   }
   return check_cuda(launch_pdl(copy_kernel, grid3(dst, 256), dim3(256), 0, s, src, dst),
                     "copy_kernel");
+}
+int launch_pack_zwin(const DView &src, const DView &dst, int kz, int pz, cudaStream_t s,
+                     bool independent) {
+  dim3 g((dst.y * ((dst.z + 3) >> 2) + 127) / 128, dst.x, dst.n);
+  if (independent)
+    return check_cuda(launch_pdl_prio(pack_zwin_kernel<true>, g, dim3(128), 0, s, true, src, dst,
+                                      kz, pz, pack_trigger()),
+                      "pack_zwin_kernel");
+  return check_cuda(launch_pdl(pack_zwin_kernel<false>, g, dim3(128), 0, s, src, dst, kz, pz, 0),
+                    "pack_zwin_kernel");
 }
 int launch_zero(const DView &dst, cudaStream_t s) {
   return check_cuda(launch_pdl(zero_kernel, grid3(dst, 256), dim3(256), 0, s, dst), "zero_kernel");

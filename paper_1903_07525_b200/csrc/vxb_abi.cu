@@ -1191,6 +1191,23 @@ int vxb_copy_ex(const vxb_tensor *src, const vxb_tensor *dst, int flags, void *s
                      (flags & VXB_COPY_INDEPENDENT) != 0);
 }
 
+int vxb_pack_zwin(const vxb_tensor *src, const vxb_tensor *dst, int kz, int pz, int flags,
+                  void *stream) {
+  int rc;
+  if ((rc = check_view(src, "pack_zwin.src")) || (rc = check_view(dst, "pack_zwin.dst")))
+    return rc;
+  if (src->blocked || src->dtype != VXB_F32 || src->c != 1)
+    return set_error(VXB_EINVAL, "pack_zwin: source must be a 1-channel fp32 standard view");
+  if (!dst->blocked || dst->dtype != VXB_BF16 || dst->c != kz || kz < 1 || kz > 8)
+    return set_error(VXB_EINVAL, "pack_zwin: destination must be bf16 blocked with c == kz <= 8");
+  if (pz < 0 || dst->n != src->n || dst->x != src->x || dst->y != src->y ||
+      dst->z != src->z + 2 * pz - kz + 1)
+    return set_error(VXB_EINVAL, "pack_zwin: shape mismatch (dst z = src z + 2 pz - kz + 1)");
+  if (flags & ~VXB_COPY_INDEPENDENT) return set_error(VXB_EINVAL, "pack_zwin: unknown flags");
+  return launch_pack_zwin(to_dview(*src), to_dview(*dst), kz, pz, as_stream(stream),
+                          (flags & VXB_COPY_INDEPENDENT) != 0);
+}
+
 int vxb_zero(const vxb_tensor *t, void *stream) {
   int rc;
   if ((rc = check_view(t, "zero"))) return rc;

@@ -128,6 +128,8 @@ struct GatherDeconvParams {
 };
 
 int launch_copy(const DView &src, const DView &dst, cudaStream_t s, bool independent = false);
+int launch_pack_zwin(const DView &src, const DView &dst, int kz, int pz, cudaStream_t s,
+                     bool independent);
 int launch_zero(const DView &dst, cudaStream_t s);
 int launch_pool(const DView &in, const DView &out, const int *w, const int *st, int mode,
                 cudaStream_t s);

@@ -124,6 +124,16 @@ def copy(src: DTensor, dst: DTensor, stream=None, independent=False) -> None:
         _lib.check(L.vxb_copy(ctypes.byref(s), ctypes.byref(d), h), "vxb_copy")
 
 
+def pack_zwin(src: DTensor, dst: DTensor, kz: int, pz: int, stream=None,
+              independent=False) -> None:
+    """vxb_pack_zwin: z-window pack of a 1-channel fp32 input (lane l = z tap l)."""
+    L = _lib.lib()
+    s, d = src.vxb(), dst.vxb()
+    flags = _lib.COPY_INDEPENDENT if independent else 0
+    _lib.check(L.vxb_pack_zwin(ctypes.byref(s), ctypes.byref(d), int(kz), int(pz), flags,
+                               stream or current_stream_handle()), "vxb_pack_zwin")
+
+
 def zero(t: DTensor, stream=None) -> None:
     L = _lib.lib()
     v = t.vxb()

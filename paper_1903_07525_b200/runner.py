@@ -321,12 +321,21 @@ class PlanRunner:
             if kind is LayerKind.CONVOLUTION and info.get("x") is not None:
                 readers.setdefault(id(info["x"]), []).append((st, info))
         fused_in = {}
+        self._zwin = {}       # id(conv info) -> (z-window input tensor, kz, pz)
         for name, v in self._in_values.items():
             rs = readers.get(id(v), [])
             if v.readers == 1 and len(rs) == 1 and self._f32in_ok(name, *rs[0]):
                 fused_in[id(rs[0][1])] = standard(self._in_std[name])
                 continue
             src = standard(self._in_std[name])
+            zw = self._zwin_plan(v, rs)
+            if zw is not None:
+                # single-channel input: z taps packed into the chunk lanes
+                xz, kz, pz = zw
+                self._zwin[id(rs[0][1])] = zw
+                calls.append(lambda s=src, d=xz, kz=kz, pz=pz:
+                             _pack_zwin(s, d, kz, pz, independent=self._indep_inputs))
+                continue
             # The pack reads a network input and writes a buffer only this
             # network's later steps read.  Inside a PlanBatch graph the kernel
             # before it is another network's, so it is launched independent
@@ -367,6 +376,20 @@ class PlanRunner:
                                  act=st.fused_act, pool=pool:
                                  K.conv3d(a, pk, out, base=base, fused_act=act, x2=b, off=oa,
                                           off2=ob, pool_out=pool))
+                elif id(info) in self._zwin:
+                    xz, kz, pz = self._zwin[id(info)]
+                    # w'(co, l, dx, dy, 0) = w(co, 0, dx, dy, l)
+                    kz_w = np.ascontiguousarray(
+                        np.transpose(np.asarray(kern, np.float32)[:, 0], (0, 3, 1, 2))[..., None])
+                    pk = K.pack_conv(kz_w, w.tensor(st.name, ROLE_BIAS), stride=stride,
+                                     base_scale=scale, out_shape=tuple(info["out"].dims[2:]),
+                                     device=dev)
+                    pool = info["pool_out"].dt if "pool_out" in info else None
+                    calls.append(lambda x=xz, pk=pk, out=out, base=base,
+                                 pad=(info["pad"][0], info["pad"][1], 0), act=st.fused_act,
+                                 pool=pool:
+                                 K.conv3d(x, pk, out, pad=pad, base=base, fused_act=act,
+                                          pool_out=pool))
                 else:
                     pk = K.pack_conv(kern, w.tensor(st.name, ROLE_BIAS), stride=stride,
                                      base_scale=scale, path=self._conv_path,
@@ -422,6 +445,32 @@ class PlanRunner:
             dst = standard(self._out_std[name])
             calls.append(lambda s=v.dt, d=dst: _copy(s, d))
         self._calls = calls
+
+    def _zwin_plan(self, v, rs):
+        """z-window pack for a 1-channel network input read only by one
+        stride-1 tensor-core conv with <= 8 z taps (the U-nets' first layer:
+        its 8-lane chunks would otherwise be 7/8 padding).  Returns the
+        packed input tensor (n, kz, x, y, oz), kz and the z pad, or None."""
+        if self.precision != "bf16" or os.environ.get("VXB_ZWIN", "1") != "1":
+            return None
+        if v.dims[1] != 1 or v.readers != 1 or len(rs) != 1:
+            return None
+        st, info = rs[0]
+        if "segments" in info or tuple(st.params.get("stride", (1, 1, 1))) != (1, 1, 1):
+            return None
+        kern = self.plan.weights.tensor(st.name, ROLE_KERNEL)
+        k = tuple(int(t) for t in kern.shape[2:])
+        pz = int(info["pad"][2])
+        if not 1 <= k[2] <= 8 or pz > k[2] - 1:
+            return None
+        L = _lib.lib()
+        if L.vxb_conv_select(k[2], st.output.dims[1], _lib.i3((k[0], k[1], 1)),
+                             _lib.i3((1, 1, 1))) != _lib.PATH_TC:
+            return None
+        n, _, x, y, z = v.dims
+        oz = z + 2 * pz - k[2] + 1
+        from .device import empty_blocked
+        return empty_blocked(n, k[2], (x, y, oz), "bf16", self.device, zero=True), k[2], pz
 
     def _f32in_ok(self, name, st, info) -> bool:
         """Can this conv read network input `name` as fp32 NCDHW directly
@@ -587,6 +636,11 @@ class PendingRun:
     def wait(self) -> dict:
         self._event.synchronize()
         return self.outputs
+
+
+def _pack_zwin(src: DTensor, dst: DTensor, kz: int, pz: int, independent=False):
+    from .device import pack_zwin
+    pack_zwin(src, dst, kz, pz, independent=independent)
 
 
 def _copy(src: DTensor, dst: DTensor, independent=False):

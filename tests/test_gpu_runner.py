@@ -231,3 +231,50 @@ def test_rebatched_plan_equals_per_volume_runs():
     got = next(iter(two.run(np.concatenate(xs, axis=0)).values()))
     for b in range(2):
         np.testing.assert_array_equal(got[b:b + 1], want[b])
+
+
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_zwin_first_layer_matches_plain_pack(cfg, monkeypatch):
+    """The U-nets' 1-channel input is packed with its z taps in the chunk
+    lanes (vxb_pack_zwin) and the first conv runs as a (kx, ky, 1) kernel:
+    the same products summed in another order, so the network output agrees
+    with the plain 8-lane pack to fp32-reordering precision."""
+    spec, store = _small(cfg)
+    plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
+    lo, hi = C.input_range(cfg)
+    x = C.make_input(spec, 5, lo, hi)
+    zw = P.PlanRunner(plan)
+    assert zw._zwin, "first conv should take the z-window pack"
+    (n, a), = zw.run(x).items()
+    monkeypatch.setenv("VXB_ZWIN", "0")
+    plain = P.PlanRunner(plan)
+    assert not plain._zwin
+    b = plain.run(x)[n]
+    mx, l2 = R.normalized_error(a, b)
+    assert mx < 2e-2 and l2 < 5e-3, (mx, l2)
+    emu = R.run_plan(plan, x, storage="bf16")[n]
+    mx, l2 = R.normalized_error(a, emu)
+    # config 5's chain of unnormalised He-init convs amplifies single bf16
+    # rounding flips (DESIGN.md §4: same bound as test_config_networks)
+    tol = (0.5, 5e-2) if cfg == 5 else (2e-2, 1e-2)
+    assert mx < tol[0] and l2 < tol[1], (mx, l2)
+
+
+def test_pack_zwin_lanes_exact():
+    """vxb_pack_zwin lane l of voxel z = bf16(src[z + l - pz]), zeros outside
+    the volume and in lanes >= kz (checked against numpy, bit for bit)."""
+    from paper_1903_07525_b200 import device as D
+    rng = np.random.default_rng(3)
+    src = rng.standard_normal((2, 1, 3, 5, 21)).astype(np.float32)
+    for kz, pz in ((3, 1), (3, 0), (5, 2), (1, 0)):
+        oz = src.shape[4] + 2 * pz - kz + 1
+        dst = D.empty_blocked(2, kz, (3, 5, oz))
+        D.pack_zwin(D.standard(torch.from_numpy(src).cuda()), dst, kz, pz)
+        torch.cuda.synchronize()
+        got = dst.t.float().cpu().numpy()            # (n, 1, x, y, z, 8)
+        padded = np.pad(src[:, 0], ((0, 0), (0, 0), (0, 0), (pz, pz + 8)))
+        want = np.zeros_like(got)
+        for l in range(kz):
+            want[:, 0, :, :, :, l] = padded[:, :, :, l:l + oz]
+        want = R.bf16_round(want)
+        np.testing.assert_array_equal(got, want)
