@@ -278,3 +278,49 @@ def test_pack_zwin_lanes_exact():
             want[:, 0, :, :, :, l] = padded[:, :, :, l:l + oz]
         want = R.bf16_round(want)
         np.testing.assert_array_equal(got, want)
+
+
+def _all_ops_net():
+    """Every layer kind and parameter the reference executes (cf. the
+    reference's test_executor.py:85-101 all-ops network): strided conv,
+    1x1x1 conv, standalone BN / Scale / ReLU / Sigmoid, avg + max pooling,
+    a k != stride deconv (gather path), eltwise sum / product / division,
+    crop + concat, with odd fmap counts."""
+    from paper_1903_07525_b200.configs import _Net
+    from paper_1903_07525_b200.netspec import LayerKind as LK
+    n = _Net("all_ops", 42)
+    x = n.input((1, 3, 12, 14, 13))
+    c1 = n.conv("c1", x, 3, 10, (3, 3, 3), pad=(1, 1, 1))
+    s1 = n.bn_scale("b1", c1, 10)
+    r1 = n.act("r1", s1, LK.RELU)
+    c2 = n.conv("c2", r1, 10, 12, (3, 3, 3), stride=(2, 2, 2))            # 5 x 6 x 6
+    p1 = n._add("p1", LK.POOLING, (r1,), {"mode": "avg", "window": (2, 2, 2),
+                                          "stride": (2, 2, 2)})          # 6 x 7 x 6
+    c3 = n.conv("c3", p1, 10, 12, (2, 2, 2))                              # 5 x 6 x 5
+    m = n.merge("m", c2, c3)                                              # crop + concat, 24
+    c4 = n.conv("c4", m, 24, 12, (1, 1, 1))
+    e1 = n._add("e1", LK.ELTWISE, (c4, c4), {"op": "mul"})
+    sg = n.act("sg", c4, LK.SIGMOID)
+    e2 = n._add("e2", LK.ELTWISE, (e1, sg), {"op": "div"})
+    d1 = n.conv("d1", e2, 12, 7, (3, 3, 3), stride=(2, 2, 2), kind=LK.DECONVOLUTION)
+    p2 = n.pool("p2", d1, (2, 2, 2))
+    n.act("out", p2, LK.ELU, 1.0)
+    return n.done()
+
+
+@pytest.mark.parametrize("backend", ["b200", "b200-fp32"])
+def test_all_ops_network_matches_oracle(backend):
+    spec, store = _all_ops_net()
+    plan, _ = P.compile_network(spec, store, fixpoint=True)
+    x = C.make_input(spec, 9, -1.0, 1.0)
+    (name, got), = P.PlanRunner(plan, backend=backend).run(x).items()
+    ref = R.ref_run(spec, store, x)[name]
+    assert got.shape == ref.shape
+    mx, l2 = R.normalized_error(got, ref)
+    if backend == "b200-fp32":
+        assert mx < 2e-5, (mx, l2)
+    else:
+        emu = R.run_plan(plan, x, storage="bf16")[name]
+        e_mx, e_l2 = R.normalized_error(got, emu)
+        assert e_mx < 3e-2 and e_l2 < 1.5e-2, (e_mx, e_l2)
+        assert mx < 5e-2 and l2 < 2e-2, (mx, l2)
