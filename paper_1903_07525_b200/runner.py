@@ -671,8 +671,10 @@ class PlanBatch:
     that each input pack hides behind a conv at least as large as its own
     network's, except that the smallest network goes first (its pack is the
     one nothing hides): config-2 sweep 0.878 ms in listed order, 0.844
-    largest-first, 0.842 smallest + largest-first.  Outputs are returned in
-    the caller's order."""
+    largest-first, 0.842 smallest + largest-first (with the side stream:
+    0.837 smallest + largest-first, 0.841 largest-first, 0.861 ascending —
+    packs running beside the small memory-bound convs slow them most;
+    `tools/batch_timeline.py`).  Outputs are returned in the caller's order."""
 
     def __init__(self, runners, reorder=True):
         torch = _torch()
@@ -685,8 +687,9 @@ class PlanBatch:
         order = list(range(len(self.runners)))
         if reorder and len(order) > 2:
             work = [_conv_flops(r.plan) for r in self.runners]
-            order.sort(key=lambda i: -work[i])
-            if os.environ.get("VXB_BATCH_ORDER", "small_first") == "small_first":
+            mode = os.environ.get("VXB_BATCH_ORDER", "small_first")
+            order.sort(key=lambda i: work[i] if mode == "asc" else -work[i])
+            if mode == "small_first":
                 order = order[-1:] + order[:-1]
         self.order = order
         self.device = dev
