@@ -688,9 +688,12 @@ class PlanBatch:
         if reorder and len(order) > 2:
             work = [_conv_flops(r.plan) for r in self.runners]
             mode = os.environ.get("VXB_BATCH_ORDER", "small_first")
-            order.sort(key=lambda i: work[i] if mode == "asc" else -work[i])
-            if mode == "small_first":
-                order = order[-1:] + order[:-1]
+            if "," in mode:                      # explicit order (experiments)
+                order = [int(t) for t in mode.split(",")]
+            else:
+                order.sort(key=lambda i: work[i] if mode == "asc" else -work[i])
+                if mode == "small_first":
+                    order = order[-1:] + order[:-1]
         self.order = order
         self.device = dev
         self.stream = torch.cuda.Stream(device=dev)
