@@ -35,6 +35,7 @@
 // of tile i+1.  CTA pairs (cta_group::2, M = 256) split the weight stream of
 // unfolded convs.
 #include <cuda_bf16.h>
+#include <type_traits>
 #include "vxb_internal.h"
 #include "vxb_ptx.cuh"
 
@@ -426,7 +427,7 @@ __device__ __forceinline__ void mma_group_fold_pair(
 }
 
 template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN, bool POOL = false>
-__global__ void __launch_bounds__(tc_threads(F32IN), 1)
+__global__ void __maxnreg__(104)
     conv3d_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps) {
   extern __shared__ __align__(1024) uint8_t smem[];
   // warp index broadcast from lane 0 so ptxas treats each role's code as
@@ -682,86 +683,97 @@ __global__ void __launch_bounds__(tc_threads(F32IN), 1)
       // (~5 extra instructions per MMA, which bounded the N = 128 convs).
       const int my_tiles =
           first_tile < p.total_tiles ? (p.total_tiles - first_tile + tile_step - 1) / tile_step : 0;
-      for (int it = 0; it < my_tiles; ++it) {
-        const int acc = it % p.acc_stages;
-        mbar_wait(&t_empty[acc], ((it / p.acc_stages) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d_base = tmem_base + acc * acc_stride;
-        uint32_t accumulate = 0, first = 1;
-        if (p.resident) b_st = 0;
-        cx.first_tile_iter = it == 0;
-        for (int g = 0; g < p.n_groups; ++g) {
-          GroupInfo gi = group_info(p, g);
-          mbar_wait(&a_full[a_st], a_ph);
+      const bool no_mma = (p.dbg_mode & 8) && p.resident;   // debug: epilogue-only timing
+      // The tile loop is instantiated per (walk, tile width): the dispatch
+      // happens once per kernel, not once per K group (per-group work in the
+      // issue loop costs MMA throughput).
+      auto tiles = [&](auto bx_c, auto kind_c) {
+        constexpr int BXV = decltype(bx_c)::value;
+        constexpr int KIND = decltype(kind_c)::value;   // 0 plain, 1 folded, 2 folded pair
+        for (int it = 0; it < my_tiles; ++it) {
+          const int acc = it % p.acc_stages;
+          mbar_wait(&t_empty[acc], ((it / p.acc_stages) & 1) ^ 1);
           tc_fence_after();
-          if (g == 0 && lane == 0) {
-            dbg_mark(p, it, 1);
-            dbg_clock(p, it, 5);
-          }
-          const bool pair = gi.nch == 2;
-          const int tz_n = pair ? p.kz : (p.kz + 1) >> 1;
-          const uint32_t dz_step = pair ? 1u : 2u;
-          const uint32_t a_lo0 =
-              desc_lo(a_base0 + a_st * p.a_stage_bytes, pair ? p.chunk_stride : 16u);
-          const uint32_t dy_wrap = p.hz - tz_n * dz_step, dx_wrap = (p.hy - p.ky) * p.hz;
-#define VXB_GROUP(BXV)                                                                          \
-  mma_group<BXV, PAIR>(a_lo0, a_hi, b_base0, p.b_stage_bytes, b_hi, b_inc, slice_inc, d_base,    \
-                       p.nt, idesc, gi.steps, tz_n, dz_step, dy_wrap, dx_wrap, p.ky, cx, b_st,  \
-                       b_ph, accumulate)
-          if ((p.dbg_mode & 8) && p.resident) {
-            // debug: no MMAs (epilogue-only timing; resident weights only)
-          } else if (PAIR && p.fold) {
-            const uint32_t a_wrap = fold_stride - tz_n * dz_step;
-#define VXB_FOLDP(BXV)                                                                       \
-  mma_group_fold_pair<BXV>(a_lo0, a_hi, b_base0, p.b_stage_bytes, b_hi, b_inc, slice_inc, d_base, \
-                           p.nt, idp, gi.steps, tz_n, dz_step, a_wrap, cx, b_st, b_ph, first)
-            switch (p.bx) {
-              case 1: VXB_FOLDP(1); break;
-              case 2: VXB_FOLDP(2); break;
-              case 3: VXB_FOLDP(3); break;
-              case 4: VXB_FOLDP(4); break;
-              case 6: VXB_FOLDP(6); break;
-              default: VXB_FOLDP(8); break;
+          const uint32_t d_base = tmem_base + acc * acc_stride;
+          uint32_t accumulate = 0, first = 1;
+          if (p.resident) b_st = 0;
+          cx.first_tile_iter = it == 0;
+          for (int g = 0; g < p.n_groups; ++g) {
+            GroupInfo gi = group_info(p, g);
+            mbar_wait(&a_full[a_st], a_ph);
+            tc_fence_after();
+            if (g == 0 && lane == 0) {
+              dbg_mark(p, it, 1);
+              dbg_clock(p, it, 5);
             }
-#undef VXB_FOLDP
-          } else if (!PAIR && p.fold) {
-            const uint32_t a_wrap = fold_stride - tz_n * dz_step;
-#define VXB_FOLD(BXV)                                                                           \
-  mma_group_fold<BXV>(a_lo0, a_hi, b_base0, p.b_stage_bytes, b_hi, b_inc, blk_inc, slice_inc,    \
-                      d_base, p.nt, id1, id2, id3, gi.steps, tz_n, dz_step, a_wrap, cx, b_st,   \
-                      b_ph, first)
-            switch (p.bx) {
-              case 1: VXB_FOLD(1); break;
-              case 2: VXB_FOLD(2); break;
-              case 3: VXB_FOLD(3); break;
-              case 4: VXB_FOLD(4); break;
-              case 6: VXB_FOLD(6); break;
-              default: VXB_FOLD(8); break;
+            const bool pair = gi.nch == 2;
+            const int tz_n = pair ? p.kz : (p.kz + 1) >> 1;
+            const uint32_t dz_step = pair ? 1u : 2u;
+            const uint32_t a_lo0 =
+                desc_lo(a_base0 + a_st * p.a_stage_bytes, pair ? p.chunk_stride : 16u);
+            if (!no_mma) {
+              if constexpr (KIND == 2) {
+                mma_group_fold_pair<BXV>(a_lo0, a_hi, b_base0, p.b_stage_bytes, b_hi, b_inc,
+                                         slice_inc, d_base, p.nt, idp, gi.steps, tz_n, dz_step,
+                                         fold_stride - tz_n * dz_step, cx, b_st, b_ph, first);
+              } else if constexpr (KIND == 1) {
+                mma_group_fold<BXV>(a_lo0, a_hi, b_base0, p.b_stage_bytes, b_hi, b_inc, blk_inc,
+                                    slice_inc, d_base, p.nt, id1, id2, id3, gi.steps, tz_n,
+                                    dz_step, fold_stride - tz_n * dz_step, cx, b_st, b_ph, first);
+              } else {
+                mma_group<BXV, PAIR>(a_lo0, a_hi, b_base0, p.b_stage_bytes, b_hi, b_inc,
+                                     slice_inc, d_base, p.nt, idesc, gi.steps, tz_n, dz_step,
+                                     p.hz - tz_n * dz_step, (p.hy - p.ky) * p.hz, p.ky, cx,
+                                     b_st, b_ph, accumulate);
+              }
             }
-#undef VXB_FOLD
-          } else switch (p.bx) {
-            case 1: VXB_GROUP(1); break;
-            case 2: VXB_GROUP(2); break;
-            case 4: VXB_GROUP(4); break;
-            default: VXB_GROUP(8); break;
+            if (PAIR)
+              umma_commit_pair_elect(&a_empty[a_st], pair_mask);
+            else
+              umma_commit_elect(&a_empty[a_st]);
+            if (++a_st == p.na) {
+              a_st = 0;
+              a_ph ^= 1;
+            }
           }
-#undef VXB_GROUP
           if (PAIR)
-            umma_commit_pair_elect(&a_empty[a_st], pair_mask);
+            umma_commit_pair_elect(&t_full[acc], pair_mask);
           else
-            umma_commit_elect(&a_empty[a_st]);
-          if (++a_st == p.na) {
-            a_st = 0;
-            a_ph ^= 1;
+            umma_commit_elect(&t_full[acc]);
+          if (lane == 0) {
+            dbg_mark(p, it, 2);
+            dbg_clock(p, it, 6);
           }
         }
-        if (PAIR)
-          umma_commit_pair_elect(&t_full[acc], pair_mask);
-        else
-          umma_commit_elect(&t_full[acc]);
-        if (lane == 0) {
-          dbg_mark(p, it, 2);
-          dbg_clock(p, it, 6);
+      };
+      using I1 = std::integral_constant<int, 1>;
+      using I2 = std::integral_constant<int, 2>;
+      using I3 = std::integral_constant<int, 3>;
+      using I4 = std::integral_constant<int, 4>;
+      using I6 = std::integral_constant<int, 6>;
+      using I8 = std::integral_constant<int, 8>;
+      using K0 = std::integral_constant<int, 0>;
+      using K1 = std::integral_constant<int, 1>;
+      using K2 = std::integral_constant<int, 2>;
+      if (p.fold) {
+        auto folded = [&](auto kind_c) {
+          switch (p.bx) {
+            case 1: tiles(I1{}, kind_c); break;
+            case 2: tiles(I2{}, kind_c); break;
+            case 3: tiles(I3{}, kind_c); break;
+            case 4: tiles(I4{}, kind_c); break;
+            case 6: tiles(I6{}, kind_c); break;
+            default: tiles(I8{}, kind_c); break;
+          }
+        };
+        if constexpr (PAIR) folded(K2{});
+        else folded(K1{});
+      } else {
+        switch (p.bx) {
+          case 1: tiles(I1{}, K0{}); break;
+          case 2: tiles(I2{}, K0{}); break;
+          case 4: tiles(I4{}, K0{}); break;
+          default: tiles(I8{}, K0{}); break;
         }
       }
     }

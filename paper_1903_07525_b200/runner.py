@@ -86,12 +86,18 @@ class PlanRunner:
         self.fuse_input = fuse_input
         self._conv_path = _lib.PATH_DIRECT if self.precision == "fp32" else 0
         self.stream = torch.cuda.Stream(device=self.device)
+        # independent input packs (set by PlanBatch while it captures).  A
+        # one-element list, not an attribute read through `self`: the call
+        # closures must not reference the runner, or runner <-> closure
+        # cycles leave dead runners to the cyclic GC, which may then destroy
+        # their CUDA graphs in the middle of another runner's stream capture
+        # (cudaGraphExecDestroy is illegal during capture and invalidates it).
+        self._indep_flag = [False]
         with torch.cuda.device(self.device):
             self._lower()
             self._allocate()
             self._bind()
         self._graph = None
-        self._indep_inputs = False       # set by PlanBatch while it captures
         self.launches = len(self._calls)
 
     # ------------------------------------------------------------ lowering
@@ -333,8 +339,8 @@ class PlanRunner:
                 # single-channel input: z taps packed into the chunk lanes
                 xz, kz, pz = zw
                 self._zwin[id(rs[0][1])] = zw
-                calls.append(lambda s=src, d=xz, kz=kz, pz=pz:
-                             _pack_zwin(s, d, kz, pz, independent=self._indep_inputs))
+                calls.append(lambda s=src, d=xz, kz=kz, pz=pz, f=self._indep_flag:
+                             _pack_zwin(s, d, kz, pz, independent=f[0]))
                 continue
             # The pack reads a network input and writes a buffer only this
             # network's later steps read.  Inside a PlanBatch graph the kernel
@@ -344,7 +350,8 @@ class PlanRunner:
             # written by a kernel (a strided torch copy) it must not overtake.
             if os.environ.get("VXB_DEBUG_SKIP_INPUT_PACK") == "1":
                 continue        # timing experiments only: inputs never reach the network
-            calls.append(lambda s=src, d=v.dt: _copy(s, d, independent=self._indep_inputs))
+            calls.append(lambda s=src, d=v.dt, f=self._indep_flag:
+                         _copy(s, d, independent=f[0]))
         n_in = len(calls)
         self._n_in_calls = n_in          # the input packs come first (PlanBatch side stream)
         self.fused_inputs = len(fused_in)
@@ -504,9 +511,12 @@ class PlanRunner:
         if self._graph is None:
             with torch.cuda.stream(self.stream):
                 self._launch_all()          # warm-up (first launches configure kernels)
-            self.stream.synchronize()
+            # capture from a quiet device, and only this thread's CUDA calls
+            # count against the capture (other threads - staging, a clock
+            # sampler - may call the runtime meanwhile)
+            torch.cuda.synchronize(self.device)
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=self.stream):
+            with torch.cuda.graph(g, stream=self.stream, capture_error_mode="thread_local"):
                 self._launch_all()
             self._graph = g
         with torch.cuda.stream(self.stream):
@@ -732,13 +742,14 @@ class PlanBatch:
             with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
                 for i in self.order:
                     self.runners[i]._launch_all()   # warm-up: first launches configure kernels
-            self.stream.synchronize()
+            torch.cuda.synchronize(self.device)
             indep = os.environ.get("VXB_DEBUG_PACK_DEPENDENT") != "1"
             for r in self.runners:
-                r._indep_inputs = indep
+                r._indep_flag[0] = indep
             try:
                 g = torch.cuda.CUDAGraph()
-                with torch.cuda.device(self.device), torch.cuda.graph(g, stream=self.stream):
+                with torch.cuda.device(self.device), \
+                        torch.cuda.graph(g, stream=self.stream, capture_error_mode="thread_local"):
                     if two:
                         self._capture_two_streams()
                     else:
@@ -746,7 +757,7 @@ class PlanBatch:
                             self.runners[i]._launch_all()
             finally:
                 for r in self.runners:
-                    r._indep_inputs = False
+                    r._indep_flag[0] = False
             self._graph = g
         with torch.cuda.stream(self.stream):
             self._graph.replay()

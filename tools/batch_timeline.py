@@ -23,7 +23,7 @@ for k in C.SWEEP_K:
         r = P.PlanRunner(plan, device=dev)
         for t in r.input_buffers().values():
             t.copy_(torch.rand(t.shape) * 2 - 1)
-        r._indep_inputs = True
+        r._indep_flag[0] = True
         runners.append(("c%d_k%s" % (c, "".join(map(str, k))), r))
 batch = P.PlanBatch([r for _, r in runners])
 order = batch.order
