@@ -9,6 +9,8 @@ Tolerances (stated per precision):
   * pool / crop / concat / layout copies: bit-exact.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -536,3 +538,35 @@ def test_deconv_taps_in_n_matches_replicas(k, cin, cout, monkeypatch):
         if with_base:
             want = R.activation(want + scale.reshape(1, -1, 1, 1, 1) * R.bf16_round(base), "elu")
         assert R.normalized_error(fused, want)[0] < BF16_TOL
+
+
+_FUZZ_N = int(os.environ.get("VXB_FUZZ_N", "12"))   # 300 run clean on a B200 (round 1)
+
+
+@pytest.mark.parametrize("seed", range(_FUZZ_N))
+def test_conv_random_shapes_match_oracle(seed):
+    """Seeded random layer shapes (fmap counts 1-160, 3x3x3 / 1x3x3 / 1x1x1 /
+    3x1x1 kernels, 'same' or valid padding, batch 1-2, optional residual and
+    activation): exercises the tile-shape, fold, CTA-pair, N-split and
+    weight-stage choices together against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    cin = int(rng.choice([1, 3, 8, 12, 16, 20, 28, 32, 36, 48, 64, 80, 96, 128, 160]))
+    cout = int(rng.choice([3, 8, 16, 24, 28, 32, 40, 64, 96, 128, 160]))
+    k = [(3, 3, 3), (1, 3, 3), (1, 1, 1), (3, 1, 1)][int(rng.integers(4))]
+    same = bool(rng.integers(2))
+    pad = tuple(v // 2 for v in k) if same else (0, 0, 0)
+    n = int(rng.integers(1, 3))
+    sp = tuple(int(v) for v in rng.integers([3, 5, 5], [13, 40, 40]))
+    sp = tuple(max(s, kk) for s, kk in zip(sp, k))
+    act = [None, "relu", "elu", "sigmoid"][int(rng.integers(4))]
+    use_base = bool(rng.integers(2))
+    x = rng.uniform(-1, 1, (n, cin) + sp).astype(np.float32)
+    w = (rng.standard_normal((cout, cin) + k) * np.sqrt(2.0 / (cin * np.prod(k)))).astype(np.float32)
+    b = (rng.standard_normal(cout) * 0.1).astype(np.float32)
+    osp = tuple(s + 2 * p - kk + 1 for s, p, kk in zip(sp, pad, k))
+    base = rng.uniform(-1, 1, (n, cout) + osp).astype(np.float32) if use_base else None
+    scale = rng.uniform(0.5, 1.5, cout).astype(np.float32) if use_base else None
+    got, _ = _conv_bf16(x, w, b, pad, act, base, scale)
+    want = _ref_bf16(x, w, b, pad, act, base, scale)
+    mx, l2 = R.normalized_error(got, want)
+    assert mx < BF16_TOL and l2 < 3e-3, (cin, cout, k, pad, n, sp, act, use_base, mx, l2)
