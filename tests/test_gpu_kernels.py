@@ -570,3 +570,41 @@ def test_conv_random_shapes_match_oracle(seed):
     want = _ref_bf16(x, w, b, pad, act, base, scale)
     mx, l2 = R.normalized_error(got, want)
     assert mx < BF16_TOL and l2 < 3e-3, (cin, cout, k, pad, n, sp, act, use_base, mx, l2)
+
+
+@pytest.mark.parametrize("seed", range(_FUZZ_N))
+def test_deconv_random_shapes_match_oracle(seed):
+    """Seeded random transposed convs: k == stride (tensor-core replicas or
+    taps in N) and k != stride (gather), optional skip add + activation."""
+    import torch
+    D, K = _dev()
+    rng = np.random.default_rng(2000 + seed)
+    cin = int(rng.choice([4, 8, 12, 28, 36, 48, 64, 80, 128]))
+    cout = int(rng.choice([3, 8, 20, 28, 36, 48, 64, 96]))
+    k = [(1, 2, 2), (2, 2, 2), (1, 3, 3), (3, 3, 3)][int(rng.integers(4))]
+    stride = k if rng.integers(3) else (1, 2, 2)
+    n = int(rng.integers(1, 3))
+    sp = tuple(int(v) for v in rng.integers([2, 3, 3], [6, 12, 12]))
+    osp = tuple((s - 1) * st + kk for s, st, kk in zip(sp, stride, k))
+    act = [None, "relu", "elu"][int(rng.integers(3))]
+    use_base = bool(rng.integers(2))
+    x = rng.uniform(-1, 1, (n, cin) + sp).astype(np.float32)
+    w = (rng.standard_normal((cout, cin) + k) * 0.2).astype(np.float32)
+    b = rng.standard_normal(cout).astype(np.float32)
+    base = rng.uniform(-1, 1, (n, cout) + osp).astype(np.float32) if use_base else None
+    scale = rng.uniform(0.5, 1.5, cout).astype(np.float32) if use_base else None
+    pk = K.pack_deconv(w, b, stride=stride, base_scale=scale)
+    out = D.empty_blocked(n, cout, osp)
+    K.deconv3d(D.to_device_blocked(x), pk, out,
+               base=D.to_device_blocked(base) if use_base else None,
+               fused_act=(act, 1.0) if act else None)
+    torch.cuda.synchronize()
+    got = D.to_host_standard(out)
+    q = R.bf16_round
+    want = R.deconv3d(q(x), q(w), b, stride)
+    if use_base:
+        want = want + scale.reshape(1, -1, 1, 1, 1) * q(base)
+    if act:
+        want = R.activation(want, act)
+    mx, l2 = R.normalized_error(got, want)
+    assert mx < BF16_TOL and l2 < 3e-3, (cin, cout, k, stride, n, sp, act, use_base, mx, l2)
