@@ -140,6 +140,11 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc is not None:
+            # a timed region shorter than the 20 ms sampling period would get
+            # no sample: wait (<= 100 ms) for one taken at its end
+            t0 = time.time()
+            while len(self.lines) <= self.skip and time.time() - t0 < 0.1:
+                time.sleep(0.005)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
