@@ -686,7 +686,7 @@ class PlanBatch:
     packs running beside the small memory-bound convs slow them most;
     `tools/batch_timeline.py`).  Outputs are returned in the caller's order."""
 
-    def __init__(self, runners, reorder=True):
+    def __init__(self, runners, reorder=True, probe=None):
         torch = _torch()
         if not runners:
             raise ExecutionError("PlanBatch needs at least one runner")
@@ -709,6 +709,13 @@ class PlanBatch:
         self.stream = torch.cuda.Stream(device=dev)
         self.launches = sum(r.launches for r in runners)
         self._graph = None
+        # optional live timing of one network's body inside the graph
+        # (external timing events recorded around it at every replay)
+        self.probe = probe
+        self._probe_ev = None
+        if probe is not None:
+            self._probe_ev = (torch.cuda.Event(enable_timing=True, external=True),
+                              torch.cuda.Event(enable_timing=True, external=True))
 
     def _capture_two_streams(self):
         """Input packs chained on a side stream (launched at background
@@ -729,8 +736,12 @@ class PlanBatch:
         for i, e in zip(self.order, evs):
             r = self.runners[i]
             self.stream.wait_event(e)
+            if i == self.probe:
+                self._probe_ev[0].record(self.stream)
             for c in r._calls[r._n_in_calls:]:
                 c()
+            if i == self.probe:
+                self._probe_ev[1].record(self.stream)
         self.stream.wait_stream(side)
 
     def replay(self):
@@ -761,6 +772,13 @@ class PlanBatch:
             self._graph = g
         with torch.cuda.stream(self.stream):
             self._graph.replay()
+
+    def probe_ms(self) -> float:
+        """Duration of the probed network's body in the last replay (ms;
+        the replay must have completed)."""
+        if self._probe_ev is None:
+            raise ExecutionError("PlanBatch was built without a probe")
+        return self._probe_ev[0].elapsed_time(self._probe_ev[1])
 
     def run_device(self):
         """Replay ordered after the caller's current stream; returns each
