@@ -19,8 +19,8 @@
  *  - Activations live in the channel-blocked layout of the reference
  *    (blocked.py:1-9): (batch, ceil(C/8), X, Y, Z, 8), lane = fmap % 8,
  *    with lanes past the logical fmap count held at zero.  Element type is
- *    bf16 (VXB_BF16) on the production path, fp32 (VXB_F32) at network
- *    boundaries.  A view carries element strides so the interior of a halo
+ *    bf16 (VXB_BF16) on the production path, split bf16 (VXB_BF16X2) on the
+ *    fp32-accurate path, fp32 (VXB_F32) at network boundaries.  A view carries element strides so the interior of a halo
  *    allocation, a crop window or a channel slice of a concat buffer are
  *    all addressable without copies (blocked.py:57-110).
  */
@@ -34,11 +34,24 @@
 extern "C" {
 #endif
 
-#define VXB_ABI_VERSION 3
+#define VXB_ABI_VERSION 4
 
 /* element types */
 #define VXB_BF16 0
 #define VXB_F32 1
+/* split bf16 ("x3" precision): every element is held as two bf16 values,
+ * hi = bf16(v) and lo = bf16(v - hi), so hi + lo keeps ~16 significant bits
+ * (fp32 storage bytes, values exact in fp32).  Blocked views only: the lo
+ * plane of every chunk lies s[1]/2 elements after its hi plane, i.e. the
+ * storage of a dense tensor is (batch, ceil(C/8), 2, X, Y, Z, 8) bf16.  A
+ * tensor-core conv reads a split input as two bf16 K segments,
+ * [hi, lo] x bf16(W) and [hi] x bf16(W - bf16(W)) (weights packed with
+ * VXB_PREC_X3), which reproduces fp32 arithmetic to ~1e-5 relative. */
+#define VXB_BF16X2 2
+
+/* weight-packing precisions (vxb_conv_pack_weights3 / vxb_deconv_pack_weights3) */
+#define VXB_PREC_BF16 0   /* bf16(W): inputs bf16 */
+#define VXB_PREC_X3 1     /* split inputs: [bf16(W); bf16(W); bf16(W - bf16(W))] */
 
 /* activation codes: identical to kernels_cy.py:19 (_ACT_CODE) */
 #define VXB_ACT_NONE 0
@@ -120,7 +133,8 @@ typedef struct vxb_conv_desc {
   float alpha;
   int32_t path;            /* 0 = auto (vxb_conv_select) */
   int32_t pool_mode;       /* VXB_POOL_FUSED_*: also write the pooled output (ops.pool fused) */
-  int32_t reserved[6];
+  int32_t prec;            /* VXB_PREC_* the weights were packed with (X3 <=> split input) */
+  int32_t reserved[5];
   vxb_tensor pool_out;     /* pooled view, logical (n, cout, ox, oy/2, oz/2) */
 } vxb_conv_desc;
 
@@ -141,7 +155,8 @@ typedef struct vxb_deconv_desc {
   int32_t act;
   float alpha;
   int32_t path;            /* 0 = auto, VXB_PATH_TC (k == stride), VXB_PATH_DIRECT (gather) */
-  int32_t reserved[7];
+  int32_t prec;            /* VXB_PREC_* the weights were packed with (X3 <=> split input) */
+  int32_t reserved[6];
 } vxb_deconv_desc;
 
 /* ---- library ---- */
@@ -178,6 +193,14 @@ size_t vxb_conv_weights_bytes2(int cin0, int cin1, int cout, const int k[3],
                                const int stride[3], int path);
 int vxb_conv_pack_weights2(const float *w, int cin0, int cin1, int cout, const int k[3],
                            const int stride[3], int path, void *dst, size_t dst_bytes);
+/* precision-aware variants: prec VXB_PREC_BF16 is the plain packing above;
+ * VXB_PREC_X3 packs the weights of a conv whose input is split bf16
+ * (VXB_BF16X2, single input segment: cin1 must be 0) */
+size_t vxb_conv_weights_bytes3(int cin0, int cin1, int cout, const int k[3],
+                               const int stride[3], int path, int prec);
+int vxb_conv_pack_weights3(const float *w, int cin0, int cin1, int cout, const int k[3],
+                           const int stride[3], int path, int prec, void *dst,
+                           size_t dst_bytes);
 int vxb_conv3d(const vxb_conv_desc *d, void *stream);
 
 /* Sub-image primitive (kernels_py.subimage / _kernels.subimage,
@@ -193,6 +216,11 @@ size_t vxb_deconv_weights_bytes(int cin, int cout, const int k[3], const int str
                                 int path);
 int vxb_deconv_pack_weights(const float *w, int cin, int cout, const int k[3],
                             const int stride[3], int path, void *dst, size_t dst_bytes);
+size_t vxb_deconv_weights_bytes3(int cin, int cout, const int k[3], const int stride[3],
+                                 int path, int prec);
+int vxb_deconv_pack_weights3(const float *w, int cin, int cout, const int k[3],
+                             const int stride[3], int path, int prec, void *dst,
+                             size_t dst_bytes);
 int vxb_deconv3d(const vxb_deconv_desc *d, void *stream);
 
 /* ---- bandwidth kernels (ops.py) ---- */

@@ -35,6 +35,22 @@ def bf16_round(a) -> np.ndarray:
     return r.astype(np.uint32).view(F32).reshape(a.shape)
 
 
+def tf32_trunc(a) -> np.ndarray:
+    """The tf32 operand a tcgen05 kind::tf32 MMA reads from fp32: the low 13
+    mantissa bits dropped (truncation), returned as float32."""
+    a = np.ascontiguousarray(np.asarray(a, dtype=F32))
+    return (a.view(np.uint32) & np.uint32(0xFFFFE000)).view(F32).reshape(a.shape)
+
+
+def split_bf16(a) -> tuple:
+    """(hi, lo): hi = bf16(a), lo = bf16(a - hi), both as float32.  hi + lo
+    holds a to ~16 mantissa bits; the sum is exact in float32."""
+    a = np.asarray(a, dtype=F32)
+    hi = bf16_round(a)
+    lo = bf16_round(a - hi)
+    return hi, lo
+
+
 def conv3d(image, kernel, bias, stride=1, pad=0):
     """oracle.ref_conv3d (oracle.py:37-64)."""
     x = np.asarray(image, F32)
@@ -202,11 +218,24 @@ def ref_run(spec, store, inputs) -> dict:
 def run_plan(plan, inputs, storage="fp32") -> dict:
     """Execute a compiled plan's steps on standard arrays (executor.py:89-198).
 
-    ``storage="bf16"`` rounds the network inputs, every step output and every
-    conv/deconv weight to bf16 — what the B200 runner stores in HBM — while
-    arithmetic stays fp32; biases, base scales and BN coefficients stay fp32.
+    ``storage`` emulates the B200 backends' roundings (arithmetic stays fp32;
+    biases, base scales and BN coefficients stay fp32):
+      * "fp32": none (the reference's own arithmetic, in another order);
+      * "bf16": network inputs, every step output and every conv/deconv weight
+        rounded to bf16 (backend ``b200``);
+      * "tf32": fp32 storage, conv/deconv operands truncated to tf32;
+      * "split": every stored tensor held as bf16 hi + bf16 lo (backend
+        ``b200-x3``), conv(x, W) = conv(x, W_hi) + conv(x_hi, W_lo) with
+        W_hi = bf16(W), W_lo = bf16(W - W_hi).
     """
-    q = bf16_round if storage == "bf16" else (lambda a: np.asarray(a, F32))
+    if storage == "bf16":
+        q = bf16_round
+    elif storage == "split":
+        def q(a):
+            hi, lo = split_bf16(a)
+            return hi + lo
+    else:
+        q = lambda a: np.asarray(a, F32)  # noqa: E731
     w = plan.weights
     if isinstance(inputs, np.ndarray):
         inputs = {plan.inputs[0][0]: inputs}
@@ -221,6 +250,18 @@ def run_plan(plan, inputs, storage="fp32") -> dict:
             arr = np.pad(arr, ((0, 0), (0, 0)) + tuple((h, h) for h in halo))
         return arr
 
+    def contract(fn, x, kern, stride):
+        kern = np.asarray(kern, F32)
+        zero = np.zeros(kern.shape[0], F32)
+        if storage == "bf16":
+            return fn(x, bf16_round(kern), zero, stride, 0)
+        if storage == "tf32":
+            return fn(tf32_trunc(x), tf32_trunc(kern), zero, stride, 0)
+        if storage == "split":
+            whi, wlo = split_bf16(kern)
+            return fn(x, whi, zero, stride, 0) + fn(split_bf16(x)[0], wlo, zero, stride, 0)
+        return fn(x, kern, zero, stride, 0)
+
     for st in plan.steps:
         k = _kind(st)
         p = st.params
@@ -232,13 +273,9 @@ def run_plan(plan, inputs, storage="fp32") -> dict:
             continue
         ins = [read(si) for si in st.inputs]
         if k in ("Convolution", "Deconvolution"):
-            kern = q(w.tensor(st.name, "kernel"))
+            kern = w.tensor(st.name, "kernel")
             bias = np.asarray(w.tensor(st.name, "bias"), F32)
-            zero = np.zeros_like(bias)
-            if k == "Convolution":
-                y = conv3d(ins[0], kern, zero, p["stride"], 0)
-            else:
-                y = deconv3d(ins[0], kern, zero, p["stride"], 0)
+            y = contract(conv3d if k == "Convolution" else deconv3d, ins[0], kern, p["stride"])
             init = np.broadcast_to(bias.reshape(1, -1, 1, 1, 1), y.shape).astype(F32)
             if st.additive:
                 base = read(st.base)

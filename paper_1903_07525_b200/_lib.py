@@ -18,8 +18,11 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 VXB_BF16 = 0
 VXB_F32 = 1
+VXB_BF16X2 = 2       # split bf16: hi plane + lo plane (s[1]/2 apart)
+PREC_BF16 = 0        # VXB_PREC_BF16
+PREC_X3 = 1          # VXB_PREC_X3
 ACT_CODE = {None: 0, "relu": 1, "elu": 2, "sigmoid": 3}   # kernels_cy.py:19
-ABI_VERSION = 3      # include/vxb.h VXB_ABI_VERSION
+ABI_VERSION = 4      # include/vxb.h VXB_ABI_VERSION
 COPY_INDEPENDENT = 1  # VXB_COPY_INDEPENDENT
 PATH_TC = 1
 PATH_DIRECT = 2
@@ -63,7 +66,8 @@ class VxbConvDesc(ctypes.Structure):
         ("alpha", c_float),
         ("path", c_int32),
         ("pool_mode", c_int32),
-        ("reserved", c_int32 * 6),
+        ("prec", c_int32),
+        ("reserved", c_int32 * 5),
         ("pool_out", VxbTensor),
     ]
 
@@ -82,7 +86,8 @@ class VxbDeconvDesc(ctypes.Structure):
         ("act", c_int32),
         ("alpha", c_float),
         ("path", c_int32),
-        ("reserved", c_int32 * 7),
+        ("prec", c_int32),
+        ("reserved", c_int32 * 6),
     ]
 
 
@@ -102,12 +107,18 @@ SIGNATURES = [
     ("vxb_conv_weights_bytes2", c_size_t, [c_int, c_int, c_int, I3, I3, c_int]),
     ("vxb_conv_pack_weights2", c_int,
      [c_void_p, c_int, c_int, c_int, I3, I3, c_int, c_void_p, c_size_t]),
+    ("vxb_conv_weights_bytes3", c_size_t, [c_int, c_int, c_int, I3, I3, c_int, c_int]),
+    ("vxb_conv_pack_weights3", c_int,
+     [c_void_p, c_int, c_int, c_int, I3, I3, c_int, c_int, c_void_p, c_size_t]),
     ("vxb_conv3d", c_int, [POINTER(VxbConvDesc), c_void_p]),
     ("vxb_conv3d_subimage", c_int,
      [POINTER(VxbConvDesc), c_void_p, c_int, c_int, I3, I3, c_int, c_int, c_void_p]),
     ("vxb_deconv_weights_bytes", c_size_t, [c_int, c_int, I3, I3, c_int]),
     ("vxb_deconv_pack_weights", c_int,
      [c_void_p, c_int, c_int, I3, I3, c_int, c_void_p, c_size_t]),
+    ("vxb_deconv_weights_bytes3", c_size_t, [c_int, c_int, I3, I3, c_int, c_int]),
+    ("vxb_deconv_pack_weights3", c_int,
+     [c_void_p, c_int, c_int, I3, I3, c_int, c_int, c_void_p, c_size_t]),
     ("vxb_deconv3d", c_int, [POINTER(VxbDeconvDesc), c_void_p]),
     ("vxb_pool3d", c_int, [TP, TP, I3, I3, c_int, c_void_p]),
     ("vxb_eltwise", c_int, [TP, TP, TP, c_int, c_void_p]),

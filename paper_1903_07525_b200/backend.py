@@ -7,6 +7,10 @@ exactly the three callables the reference runtime binds per conv step
 
 * ``b200``       bf16 activations and weights, fp32 accumulate, tcgen05
                  tensor cores (the production path);
+* ``b200-x3``    split-bf16 storage (hi + lo planes) and three bf16 tensor-
+                 core products per MAC (hi*W_hi + lo*W_hi + hi*W_lo, fp32
+                 accumulate): fp32-grade results (~1e-5 relative per conv)
+                 at ~3x the MMA work of ``b200``;
 * ``b200-fp32``  fp32 everywhere on CUDA cores (verification path; matches
                  the reference's fp32 arithmetic to ~1e-6).
 
@@ -23,7 +27,7 @@ from . import _lib
 from .errors import ExecutionError
 
 BACKEND_ENV = "VOXPLAN_BACKEND"
-NAMES = ("b200", "b200-fp32")
+NAMES = ("b200", "b200-x3", "b200-fp32")
 
 
 class Backend:
@@ -66,7 +70,7 @@ def get_backend(name=None) -> Backend:
     if not compiled_available():
         raise ExecutionError("%s backend requested but libvxb.so is not built" % name)
     from . import kernels_b200
-    return Backend(name, kernels_b200, "fp32" if name == "b200-fp32" else "bf16")
+    return Backend(name, kernels_b200, {"b200-fp32": "fp32", "b200-x3": "x3"}.get(name, "bf16"))
 
 
 def resolve_device_backend(backend) -> Backend:

@@ -142,11 +142,127 @@ def config4(seed=4, spatial=(132, 132, 132), base=32, levels=4, out_ch=3):
     return n.done()
 
 
-def config5(seed=5, patch=(18, 192, 192), feats=(28, 36, 48, 64, 80), out_ch=3):
+# ------------------------------------------------------------------ BN calibration
+# Workload generation only (synthetic weights), not an inference path: the
+# engine has no CPU execution path.  A trained network's BatchNorm holds the
+# running statistics of the activations it normalises; random BN statistics
+# (round 1) let config 5's activations grow through 28 unnormalised convs to
+# |logit| ~ 600, a degenerate sigmoid output of 0s and 1s in which any
+# rounding flips a probability (BASELINE.md §3 note).  Calibrated
+# networks keep |logit| ~ 10.
+
+def _np_conv(x, w, b, pad):
+    px, py, pz = pad
+    x = np.pad(x, ((0, 0), (0, 0), (px, px), (py, py), (pz, pz)))
+    co, _, kx, ky, kz = w.shape
+    n, _, ix, iy, iz = x.shape
+    ox, oy, oz = ix - kx + 1, iy - ky + 1, iz - kz + 1
+    out = np.zeros((co, n, ox, oy, oz), np.float32)
+    for dx in range(kx):
+        for dy in range(ky):
+            for dz in range(kz):
+                out += np.tensordot(w[:, :, dx, dy, dz],
+                                    x[:, :, dx:dx + ox, dy:dy + oy, dz:dz + oz], axes=([1], [1]))
+    return np.moveaxis(out, 0, 1) + b.reshape(1, -1, 1, 1, 1)
+
+
+def _np_deconv_kstride(x, w, b):
+    co, _, kx, ky, kz = w.shape
+    n, _, ix, iy, iz = x.shape
+    out = np.zeros((n, co, ix * kx, iy * ky, iz * kz), np.float32)
+    for dx in range(kx):
+        for dy in range(ky):
+            for dz in range(kz):
+                out[:, :, dx::kx, dy::ky, dz::kz] = np.moveaxis(
+                    np.tensordot(w[:, :, dx, dy, dz], x, axes=([1], [1])), 0, 1)
+    return out + b.reshape(1, -1, 1, 1, 1)
+
+
+def calibrate_bn(spec, store, x):
+    """Set every BatchNorm's (mean, var) to the per-fmap statistics of its own
+    input on volume ``x`` (one forward in topological order, each BN applied
+    with its calibrated statistics before later layers see it).  Supports the
+    layer kinds of the BASELINE U-nets."""
+    blobs = {}
+    for idx in spec.topological_order():
+        lay = spec.layers[idx]
+        k, prm = lay.kind, lay.params
+        ins = [blobs[b] for b in lay.bottoms]
+
+        def t(role):
+            return store.tensor(lay.name, role)
+        if k is LayerKind.INPUT:
+            out = np.asarray(x, np.float32)
+        elif k is LayerKind.CONVOLUTION:
+            if tuple(prm.get("stride", (1, 1, 1))) != (1, 1, 1):
+                raise ValueError("calibrate_bn: strided conv")
+            out = _np_conv(ins[0], t(ROLE_KERNEL), t(ROLE_BIAS), prm["pad"])
+        elif k is LayerKind.DECONVOLUTION:
+            out = _np_deconv_kstride(ins[0], t(ROLE_KERNEL), t(ROLE_BIAS))
+        elif k is LayerKind.POOLING:
+            wx, wy, wz = prm["window"]
+            a = ins[0]
+            n_, c_, X, Y, Z = a.shape
+            out = a[:, :, :X // wx * wx, :Y // wy * wy, :Z // wz * wz].reshape(
+                n_, c_, X // wx, wx, Y // wy, wy, Z // wz, wz).max(axis=(3, 5, 7))
+        elif k is LayerKind.ELTWISE:
+            out = ins[0] + ins[1]
+        elif k is LayerKind.BATCH_NORM:
+            a = ins[0].astype(np.float64)
+            mean = a.mean(axis=(0, 2, 3, 4))
+            var = a.var(axis=(0, 2, 3, 4))
+            store.put(lay.name + "." + ROLE_BN_MEAN, mean)
+            store.put(lay.name + "." + ROLE_BN_VAR, var)
+            eps = float(np.asarray(store.tensor(lay.name, ROLE_BN_EPS)))
+            f = (1.0 / np.sqrt(var + eps)).astype(np.float32)
+            out = (ins[0] - mean.astype(np.float32).reshape(1, -1, 1, 1, 1)) * f.reshape(
+                1, -1, 1, 1, 1)
+        elif k is LayerKind.SCALE:
+            out = ins[0] * t(ROLE_SCALE_GAMMA).reshape(1, -1, 1, 1, 1) + \
+                t(ROLE_SCALE_BETA).reshape(1, -1, 1, 1, 1)
+        elif k is LayerKind.ELU:
+            a = ins[0]
+            out = np.where(a > 0, a, np.float32(prm.get("alpha", 1.0)) * np.expm1(np.minimum(a, 0)))
+        elif k is LayerKind.RELU:
+            out = np.maximum(ins[0], 0)
+        elif k is LayerKind.SIGMOID:
+            out = 1.0 / (1.0 + np.exp(-ins[0]))
+        else:
+            raise ValueError("calibrate_bn: layer kind %s" % k)
+        blobs[lay.tops[0]] = np.asarray(out, np.float32)
+    return store
+
+
+CALIB_PATCH5 = (18, 96, 96)     # calibration volume for config 5 (smaller than a patch)
+_CAL_CACHE: dict = {}
+
+
+def config5(seed=5, patch=(18, 192, 192), feats=(28, 36, 48, 64, 80), out_ch=3, bn="calibrated"):
     """Anisotropic residual symmetric U-net (Lee et al. 2017 style) on one patch.
     Level block: c0 1x3x3 -> BN/Scale/ELU = a0 -> c1 3^3 -> BN/Scale/ELU ->
     c2 3^3 -> add(c2, a0) -> BN/Scale/ELU; 1x2x2 maxpool; 1x2x2 s(1,2,2)
-    deconv + summation skip; 1^3 head to 3 fmaps + sigmoid."""
+    deconv + summation skip; 1^3 head to 3 fmaps + sigmoid.
+
+    ``bn="calibrated"`` (default): BN statistics measured on a seeded U[0,1)
+    calibration volume of min(patch, CALIB_PATCH5) (calibrate_bn), as a
+    trained network holds them; ``bn="random"``: round 1's random statistics
+    (bn_mean N(0, 0.1), bn_var U[0.5, 1.5])."""
+    key = (seed, tuple(patch), tuple(feats), out_ch, bn)
+    if key in _CAL_CACHE:
+        spec, store = _CAL_CACHE[key]
+        return spec, store.copy()
+    spec, store = _config5_random(seed, patch, feats, out_ch)
+    if bn == "calibrated":
+        cp = tuple(min(a, b) for a, b in zip(patch, CALIB_PATCH5))
+        xc = np.random.default_rng(55555).uniform(0, 1, (1, 1) + cp).astype(np.float32)
+        calibrate_bn(spec, store, xc)
+    elif bn != "random":
+        raise ValueError("bn must be 'calibrated' or 'random'")
+    _CAL_CACHE[key] = (spec, store.copy())
+    return spec, store
+
+
+def _config5_random(seed, patch, feats, out_ch):
     n = _Net("cfg5_unet_aniso", seed)
     top, cin = n.input((1, 1) + tuple(patch)), 1
 

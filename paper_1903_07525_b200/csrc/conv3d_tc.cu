@@ -114,8 +114,45 @@ __device__ __forceinline__ float apply_act(float v, int act, float alpha) {
   return v;
 }
 
+// split bf16 (VXB_BF16X2): 8 lanes = a hi and a lo bf16 chunk, s[1]/2 apart
+__device__ __forceinline__ void unpack_bf16x8(const uint4 &u, float (&x)[8]) {
+  const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    x[2 * i] = f.x;
+    x[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void split8(const float (&x)[8], uint4 &hi, uint4 &lo) {
+  __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&hi);
+  __nv_bfloat162 *l = reinterpret_cast<__nv_bfloat162 *>(&lo);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    h[i] = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
+    const float2 f = __bfloat1622float2(h[i]);
+    l[i] = __floats2bfloat162_rn(x[2 * i] - f.x, x[2 * i + 1] - f.y);
+  }
+}
+__device__ __forceinline__ void store8_split(const EpiView &v, long long off, const float (&x)[8]) {
+  uint4 hi, lo;
+  split8(x, hi, lo);
+  __nv_bfloat16 *p = static_cast<__nv_bfloat16 *>(v.data) + off;
+  *reinterpret_cast<uint4 *>(p) = hi;
+  *reinterpret_cast<uint4 *>(p + (v.s[1] >> 1)) = lo;
+}
+
 __device__ __forceinline__ void load8(const EpiView &v, long long off, bool blocked_lane_stride1,
                                       float (&x)[8]) {
+  if (v.dtype == VXB_BF16X2) {   // blocked only
+    const __nv_bfloat16 *p = static_cast<const __nv_bfloat16 *>(v.data) + off;
+    float lo[8];
+    unpack_bf16x8(*reinterpret_cast<const uint4 *>(p), x);
+    unpack_bf16x8(*reinterpret_cast<const uint4 *>(p + (v.s[1] >> 1)), lo);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] += lo[i];
+    return;
+  }
   if (v.dtype == VXB_BF16) {
     const __nv_bfloat16 *p = static_cast<const __nv_bfloat16 *>(v.data) + off;
     if (blocked_lane_stride1) {
@@ -149,6 +186,10 @@ __device__ __forceinline__ void load8(const EpiView &v, long long off, bool bloc
 // lanes (tail lanes are written as zero, ops.py:18-23 zero_tail semantics)
 __device__ __forceinline__ void store8(const EpiView &v, long long off, bool blocked,
                                        int nvalid, const float (&x)[8]) {
+  if (v.dtype == VXB_BF16X2) {   // blocked only
+    store8_split(v, off, x);
+    return;
+  }
   if (v.dtype == VXB_BF16) {
     __nv_bfloat16 *p = static_cast<__nv_bfloat16 *>(v.data) + off;
     if (blocked) {
@@ -1045,7 +1086,12 @@ __global__ void __maxnreg__(104)
             }
           } else if (FASTOUT) {
             if (ov.blocked) {
-              if (valid && !(p.dbg_mode & 512)) store8_bf16_blocked(ov, obase + (c0 >> 3) * ov.s[1], r);
+              if (valid && !(p.dbg_mode & 512)) {
+                if (ov.dtype == VXB_BF16X2)
+                  store8_split(ov, obase + (c0 >> 3) * ov.s[1], r);
+                else
+                  store8_bf16_blocked(ov, obase + (c0 >> 3) * ov.s[1], r);
+              }
             } else if (valid) {
               // fused unpack: fp32 NCDHW network output written directly
               // (one pointer walked across the channel planes)
@@ -1128,13 +1174,7 @@ template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN = false, bool 
 static int launch_variant(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t stream,
                           size_t smem) {
   auto kern = conv3d_tc_kernel<ACT, FASTOUT, BASE, PAIR, F32IN, POOL>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(conv3d_tc)");
-    configured = true;
-  }
+  if (int rc = ensure_smem_attr(kern, 232448, "cudaFuncSetAttribute(conv3d_tc)")) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(tc_threads(F32IN));
@@ -1179,7 +1219,7 @@ static int launch_f32in(const TcParams &p, const TcMaps &maps, int grid, cudaStr
 template <bool BASE, bool PAIR>
 static int launch_act(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t s,
                       size_t smem) {
-  const bool fast = (p.out.dtype == VXB_BF16 && p.out.blocked) ||
+  const bool fast = ((p.out.dtype == VXB_BF16 || p.out.dtype == VXB_BF16X2) && p.out.blocked) ||
                     (p.out.dtype == VXB_F32 && !p.out.blocked);
   if (p.pool) {
     if (PAIR || p.f32in || p.out.dtype != VXB_BF16 || !p.out.blocked ||

@@ -26,15 +26,48 @@ __device__ __forceinline__ long long voff(const DView &v, int b, int c, int x, i
   return b * v.s[0] + (v.blocked ? (c >> 3) * v.s[1] + (c & 7) : c * v.s[1]) + x * v.s[2] +
          y * v.s[3] + z * v.s[4];
 }
+// element access; split bf16 (VXB_BF16X2, blocked) holds hi at i and lo at
+// i + s[1]/2, the value is their (exact) fp32 sum
 __device__ __forceinline__ float vld(const DView &v, long long i) {
+  if (v.dtype == VXB_BF16X2) {
+    const __nv_bfloat16 *p = static_cast<const __nv_bfloat16 *>(v.data);
+    return __bfloat162float(p[i]) + __bfloat162float(p[i + (v.s[1] >> 1)]);
+  }
   return v.dtype == VXB_BF16 ? __bfloat162float(static_cast<const __nv_bfloat16 *>(v.data)[i])
                              : static_cast<const float *>(v.data)[i];
 }
 __device__ __forceinline__ void vst(const DView &v, long long i, float f) {
-  if (v.dtype == VXB_BF16)
+  if (v.dtype == VXB_BF16X2) {
+    __nv_bfloat16 *p = static_cast<__nv_bfloat16 *>(v.data);
+    const __nv_bfloat16 hi = __float2bfloat16_rn(f);
+    p[i] = hi;
+    p[i + (v.s[1] >> 1)] = __float2bfloat16_rn(f - __bfloat162float(hi));
+  } else if (v.dtype == VXB_BF16) {
     static_cast<__nv_bfloat16 *>(v.data)[i] = __float2bfloat16_rn(f);
-  else
+  } else {
     static_cast<float *>(v.data)[i] = f;
+  }
+}
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4 &u, float (&r)[8]) {
+  const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    r[2 * i] = f.x;
+    r[2 * i + 1] = f.y;
+  }
+}
+// hi = bf16(r), lo = bf16(r - hi), 8 lanes each
+__device__ __forceinline__ void f32_to_split8(const float (&r)[8], uint4 &hi, uint4 &lo) {
+  __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&hi);
+  __nv_bfloat162 *l = reinterpret_cast<__nv_bfloat162 *>(&lo);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    h[i] = __floats2bfloat162_rn(r[2 * i], r[2 * i + 1]);
+    const float2 f = __bfloat1622float2(h[i]);
+    l[i] = __floats2bfloat162_rn(r[2 * i] - f.x, r[2 * i + 1] - f.y);
+  }
 }
 
 // chunk-granular access: lanes [0, 8) of chunk `ch` at voxel (b,x,y,z)
@@ -42,7 +75,14 @@ __device__ __forceinline__ void ld_chunk(const DView &v, int b, int ch, int x, i
                                          float (&r)[8]) {
   if (v.blocked) {
     long long o = b * v.s[0] + ch * v.s[1] + x * v.s[2] + y * v.s[3] + z * v.s[4];
-    if (v.dtype == VXB_BF16) {
+    if (v.dtype == VXB_BF16X2) {
+      const __nv_bfloat16 *p = static_cast<const __nv_bfloat16 *>(v.data) + o;
+      float lo[8];
+      bf16x8_to_f32(*reinterpret_cast<const uint4 *>(p), r);
+      bf16x8_to_f32(*reinterpret_cast<const uint4 *>(p + (v.s[1] >> 1)), lo);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) r[i] += lo[i];
+    } else if (v.dtype == VXB_BF16) {
       uint4 u = *reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(v.data) + o);
       const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
 #pragma unroll
@@ -71,7 +111,13 @@ __device__ __forceinline__ void st_chunk(const DView &v, int b, int ch, int x, i
                                          const float (&r)[8]) {
   if (v.blocked) {
     long long o = b * v.s[0] + ch * v.s[1] + x * v.s[2] + y * v.s[3] + z * v.s[4];
-    if (v.dtype == VXB_BF16) {
+    if (v.dtype == VXB_BF16X2) {
+      uint4 hi, lo;
+      f32_to_split8(r, hi, lo);
+      __nv_bfloat16 *p = static_cast<__nv_bfloat16 *>(v.data) + o;
+      *reinterpret_cast<uint4 *>(p) = hi;
+      *reinterpret_cast<uint4 *>(p + (v.s[1] >> 1)) = lo;
+    } else if (v.dtype == VXB_BF16) {
       uint4 u;
       __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&u);
 #pragma unroll
@@ -511,9 +557,10 @@ static dim3 grid3(const DView &v, int threads) {
   return dim3((v.y * v.z + threads - 1) / threads, v.x, v.n * ((v.c + 7) / 8));
 }
 
-// Network-boundary pack: fp32 NCDHW (z contiguous) -> bf16 blocked.  Each
-// thread converts 4 consecutive z of one 8-fmap chunk: 8 float4 loads (one
-// per fmap plane, 512 B per warp instruction) and 4 16-byte stores.
+// Network-boundary pack: fp32 NCDHW (z contiguous) -> bf16 blocked (or split
+// bf16: hi and lo chunks).  Each thread converts 4 consecutive z of one
+// 8-fmap chunk: 8 float4 loads (one per fmap plane, 512 B per warp
+// instruction) and 4 16-byte stores (8 when split).
 // One pack item: 4 consecutive z of one 8-fmap chunk at (b, ch, x, y).
 __device__ __forceinline__ void pack_item(const DView &src, const DView &dst, int b, int ch, int x,
                                           int y, int z) {
@@ -532,6 +579,19 @@ __device__ __forceinline__ void pack_item(const DView &src, const DView &dst, in
   }
   __nv_bfloat16 *o = static_cast<__nv_bfloat16 *>(dst.data) + b * dst.s[0] + ch * dst.s[1] +
                      x * dst.s[2] + y * dst.s[3] + z * dst.s[4];
+  if (dst.dtype == VXB_BF16X2) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float r[8];
+#pragma unroll
+      for (int l = 0; l < 8; ++l) r[l] = v[l][q];
+      uint4 hi, lo;
+      f32_to_split8(r, hi, lo);
+      *reinterpret_cast<uint4 *>(o + q * dst.s[4]) = hi;
+      *reinterpret_cast<uint4 *>(o + q * dst.s[4] + (dst.s[1] >> 1)) = lo;
+    }
+    return;
+  }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     uint4 u;
@@ -599,12 +659,20 @@ __global__ void pack_zwin_kernel(DView src, DView dst, int kz, int pz, int trigg
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     if (z0 + q >= dst.z) break;
+    float r[8];
+#pragma unroll
+    for (int l = 0; l < 8; ++l) r[l] = l < kz ? v[q + l] : 0.f;
+    if (dst.dtype == VXB_BF16X2) {
+      uint4 hi, lo;
+      f32_to_split8(r, hi, lo);
+      *reinterpret_cast<uint4 *>(o + (z0 + q) * dst.s[4]) = hi;
+      *reinterpret_cast<uint4 *>(o + (z0 + q) * dst.s[4] + (dst.s[1] >> 1)) = lo;
+      continue;
+    }
     uint4 u;
     __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&u);
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      h[k] = __floats2bfloat162_rn(2 * k < kz ? v[q + 2 * k] : 0.f,
-                                   2 * k + 1 < kz ? v[q + 2 * k + 1] : 0.f);
+    for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(r[2 * k], r[2 * k + 1]);
     *reinterpret_cast<uint4 *>(o + (z0 + q) * dst.s[4]) = u;
   }
 }
@@ -621,15 +689,15 @@ __global__ void unpack_std_f32_kernel(DView src, DView dst) {
   const __nv_bfloat16 *p = static_cast<const __nv_bfloat16 *>(src.data) + b * src.s[0] +
                            ch * src.s[1] + x * src.s[2] + y * src.s[3] + z * src.s[4];
   float v[4][8];
+  const bool split = src.dtype == VXB_BF16X2;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const uint4 u = *reinterpret_cast<const uint4 *>(p + q * src.s[4]);
-    const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+    bf16x8_to_f32(*reinterpret_cast<const uint4 *>(p + q * src.s[4]), v[q]);
+    if (split) {
+      float lo[8];
+      bf16x8_to_f32(*reinterpret_cast<const uint4 *>(p + q * src.s[4] + (src.s[1] >> 1)), lo);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float2 f = __bfloat1622float2(h[k]);
-      v[q][2 * k] = f.x;
-      v[q][2 * k + 1] = f.y;
+      for (int k = 0; k < 8; ++k) v[q][k] += lo[k];
     }
   }
 #pragma unroll
@@ -648,6 +716,10 @@ static bool std_f32_vec4(const DView &t) {
          (t.s[1] & 3) == 0 && (t.s[2] & 3) == 0 && (t.s[3] & 3) == 0;
 }
 static bool blocked_bf16(const DView &t) { return t.blocked && t.dtype == VXB_BF16; }
+// bf16 or split bf16 blocked (the boundary pack / unpack kernels handle both)
+static bool blocked_bf16ish(const DView &t) {
+  return t.blocked && (t.dtype == VXB_BF16 || t.dtype == VXB_BF16X2);
+}
 
 static int pack_trigger() {
   const char *v = getenv("VXB_PACK_TRIGGER");
@@ -655,7 +727,7 @@ static int pack_trigger() {
 }
 
 int launch_copy(const DView &src, const DView &dst, cudaStream_t s, bool independent) {
-  if (std_f32_vec4(src) && blocked_bf16(dst)) {
+  if (std_f32_vec4(src) && blocked_bf16ish(dst)) {
     dim3 g((dst.y * (dst.z >> 2) + 127) / 128, dst.x, dst.n * ((dst.c + 7) / 8));
     if (independent)
       return check_cuda(launch_pdl_prio(pack_std_f32_indep_kernel, g, dim3(128), 0, s, true, src,
@@ -664,7 +736,7 @@ int launch_copy(const DView &src, const DView &dst, cudaStream_t s, bool indepen
     return check_cuda(launch_pdl(pack_std_f32_kernel, g, dim3(128), 0, s, src, dst),
                       "pack_std_f32_kernel");
   }
-  if (blocked_bf16(src) && std_f32_vec4(dst)) {
+  if (blocked_bf16ish(src) && std_f32_vec4(dst)) {
     dim3 g((src.y * (src.z >> 2) + 127) / 128, src.x, src.n * ((src.c + 7) / 8));
     return check_cuda(launch_pdl(unpack_std_f32_kernel, g, dim3(128), 0, s, src, dst),
                       "unpack_std_f32_kernel");
@@ -734,13 +806,9 @@ int launch_conv_direct(DirectParams p, cudaStream_t s) {
                 sizeof(float);
   if (smem > 227 * 1024)
     return set_error(VXB_EUNSUPPORTED, "direct conv: staged patch of %zu bytes exceeds smem", smem);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv_direct_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(conv_direct)");
-    configured = true;
-  }
+  if (int rc = ensure_smem_attr(conv_direct_kernel, 227 * 1024,
+                                "cudaFuncSetAttribute(conv_direct)"))
+    return rc;
   dim3 grid(p.tiles_x * p.tiles_y * p.tiles_z, (p.cout + DCO - 1) / DCO, p.out.n);
   return check_cuda(launch_pdl(conv_direct_kernel, grid, dim3(128), smem, s, p),
                     "conv_direct_kernel");

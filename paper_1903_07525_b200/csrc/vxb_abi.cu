@@ -7,7 +7,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
+#include <utility>
 #include <vector>
 #include "vxb_internal.h"
 
@@ -39,6 +42,17 @@ static int env_int(const char *name, int dflt) {
 }
 
 bool pdl_enabled() { return env_int("VXB_PDL", 1) != 0; }
+
+static std::mutex g_attr_mu;
+static std::set<std::pair<const void *, int>> g_attr_done;
+bool smem_attr_done(const void *kern, int dev) {
+  std::lock_guard<std::mutex> g(g_attr_mu);
+  return g_attr_done.count({kern, dev}) != 0;
+}
+void smem_attr_mark(const void *kern, int dev) {
+  std::lock_guard<std::mutex> g(g_attr_mu);
+  g_attr_done.insert({kern, dev});
+}
 int launch_priority(bool background) {
   static int lo = 0, hi = 0, init = 0;
   if (!init) {
@@ -74,13 +88,17 @@ static EpiView to_epi(const vxb_tensor &t) {
 
 static int check_view(const vxb_tensor *t, const char *what) {
   if (!t || !t->data) return set_error(VXB_EINVAL, "%s: null tensor", what);
-  if (t->dtype != VXB_BF16 && t->dtype != VXB_F32)
+  if (t->dtype != VXB_BF16 && t->dtype != VXB_F32 && t->dtype != VXB_BF16X2)
     return set_error(VXB_EINVAL, "%s: bad dtype %d", what, t->dtype);
+  if (t->dtype == VXB_BF16X2 && (!t->blocked || t->s[1] % 16 != 0))
+    return set_error(VXB_EINVAL,
+                     "%s: split bf16 views are blocked with the lo plane at s[1]/2 (s[1] %% 16 == 0)",
+                     what);
   if (t->n < 1 || t->c < 1 || t->x < 1 || t->y < 1 || t->z < 1)
     return set_error(VXB_EINVAL, "%s: non-positive extent (%d,%d,%d,%d,%d)", what, t->n, t->c,
                      t->x, t->y, t->z);
   if (t->blocked) {
-    size_t esz = t->dtype == VXB_BF16 ? 2 : 4;
+    size_t esz = t->dtype == VXB_F32 ? 4 : 2;
     uintptr_t a = reinterpret_cast<uintptr_t>(t->data);
     if (a % (8 * esz) != 0)
       return set_error(VXB_EINVAL, "%s: blocked view base must be %zu-byte aligned", what, 8 * esz);
@@ -92,6 +110,21 @@ static int check_view(const vxb_tensor *t, const char *what) {
 }
 
 static cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// A split (VXB_BF16X2) input as the two bf16 K segments the tensor-core conv
+// reads: `both` = every chunk's hi and lo planes as 2*CB chunks of 8 lanes
+// (hi_0, lo_0, hi_1, lo_1, ...), `hi` = the CB hi planes alone.  Weights
+// packed with VXB_PREC_X3 multiply them by bf16(W) and bf16(W - bf16(W)).
+static void split_segments(const vxb_tensor &t, vxb_tensor &both, vxb_tensor &hi) {
+  const int cb = (t.c + 7) / 8;
+  both = t;
+  both.dtype = VXB_BF16;
+  both.c = 16 * cb;
+  both.s[1] = t.s[1] / 2;
+  hi = t;
+  hi.dtype = VXB_BF16;
+  hi.c = 8 * cb;
+}
 
 // ------------------------------------------------------------------ TC geometry
 
@@ -418,14 +451,19 @@ static int make_input_map(const vxb_tensor &t, int hx, int hy, int hz, CUtensorM
 static void *g_dbg = nullptr;
 static const size_t kDbgBytes = 1024 * 64 * 8 * sizeof(unsigned long long);
 
+// SM count of the calling thread's current device (cached per device: the
+// threads of a multi-GPU run_tiled each drive their own device)
 static int device_sms() {
-  static int sms = -1;
-  if (sms < 0) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-      sms = -1;
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (dev >= 0 && dev < 64) {
+    const int c = __atomic_load_n(&cache[dev], __ATOMIC_RELAXED);
+    if (c > 0) return c;
   }
+  int sms = -1;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  if (dev >= 0 && dev < 64) __atomic_store_n(&cache[dev], sms, __ATOMIC_RELAXED);
   return sms;
 }
 
@@ -491,7 +529,7 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
   // folded low-fmap convs run as CTA pairs when N = 3nt <= 96: an M = 256
   // MMA then costs what an M = 128 one does (tools/umma_align.cu)
   const int pair_env = env_int("VXB_TC_PAIR", 1);
-  const bool out_ok = (a.out.dtype == VXB_BF16 && a.out.blocked) ||
+  const bool out_ok = ((a.out.dtype == VXB_BF16 || a.out.dtype == VXB_BF16X2) && a.out.blocked) ||
                       (a.out.dtype == VXB_F32 && !a.out.blocked);
   // Measured (config-2 shapes, 128x256x256): 3x3x3 at nt = 16 gains 14 %;
   // 1x3x3 and nt = 32 lose (their tiles are bound by the A-halo stream, and
@@ -685,6 +723,32 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
   return launch_conv3d_tc(p, maps, grid, stream);
 }
 
+// x3 precision: the conv's K segments over a split input of cin fmaps
+static inline int x3_cin0(int cin) { return 16 * ceil_div(cin, 8); }
+static inline int x3_cin1(int cin) { return 8 * ceil_div(cin, 8); }
+
+static inline float bf16_bits_to_f32(uint16_t h) {
+  const uint32_t u = static_cast<uint32_t>(h) << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+static inline float bf16_round_host(float v) { return bf16_bits_to_f32(f32_to_bf16_bits(v)); }
+
+// Weight of K column ci of the x3 segments (split_segments): ci < 16 CB is
+// lane ci % 8 of plane (ci / 8) % 2 of chunk ci / 16 -> bf16(W); ci >= 16 CB
+// is the hi plane again -> bf16(W - bf16(W)).  Lanes past cin are zero.
+template <class WFn>
+static float x3_weight(WFn wstd, int cin, int co, int ci, int dx, int dy, int dz) {
+  const int c0 = x3_cin0(cin);
+  const bool lo_term = ci >= c0;
+  const int c = lo_term ? ci - c0 : (ci / 16) * 8 + (ci % 8);
+  if (c >= cin) return 0.f;
+  const float v = wstd(co, c, dx, dy, dz);
+  const float hi = bf16_round_host(v);
+  return lo_term ? v - hi : hi;
+}
+
 }  // namespace vxb
 
 using namespace vxb;
@@ -766,29 +830,55 @@ static size_t direct_bytes(int cin, int cout, const int k[3]) {
          8 * DCO_DIRECT * sizeof(float);
 }
 
-size_t vxb_conv_weights_bytes2(int cin0, int cin1, int cout, const int k[3], const int stride[3],
-                               int path) {
+size_t vxb_conv_weights_bytes3(int cin0, int cin1, int cout, const int k[3], const int stride[3],
+                               int path, int prec) {
+  if (prec == VXB_PREC_X3) {
+    if (cin1 != 0) return 0;
+    if (path == 0) path = vxb_conv_select(cin0, cout, k, stride);
+    if (is_tc(path))
+      return tc_bytes_per_rep(tc_layout(x3_cin0(cin0), x3_cin1(cin0), cout, k, path_folds(path),
+                                        path_nt_cap(path)));
+    return direct_bytes(cin0, cout, k);   // CUDA cores read split inputs as fp32 sums
+  }
   if (path == 0) path = vxb_conv_select(cin0 + cin1, cout, k, stride);
   if (is_tc(path))
     return tc_bytes_per_rep(tc_layout(cin0, cin1, cout, k, path_folds(path), path_nt_cap(path)));
   return direct_bytes(cin0 + cin1, cout, k);
 }
 
+size_t vxb_conv_weights_bytes2(int cin0, int cin1, int cout, const int k[3], const int stride[3],
+                               int path) {
+  return vxb_conv_weights_bytes3(cin0, cin1, cout, k, stride, path, VXB_PREC_BF16);
+}
+
 size_t vxb_conv_weights_bytes(int cin, int cout, const int k[3], const int stride[3], int path) {
   return vxb_conv_weights_bytes2(cin, 0, cout, k, stride, path);
 }
 
-int vxb_conv_pack_weights2(const float *w, int cin0, int cin1, int cout, const int k[3],
-                           const int stride[3], int path, void *dst, size_t dst_bytes) {
+int vxb_conv_pack_weights3(const float *w, int cin0, int cin1, int cout, const int k[3],
+                           const int stride[3], int path, int prec, void *dst, size_t dst_bytes) {
   const int cin = cin0 + cin1;
   if (!w || !dst) return set_error(VXB_EINVAL, "pack: null pointer");
+  if (prec != VXB_PREC_BF16 && prec != VXB_PREC_X3)
+    return set_error(VXB_EINVAL, "pack: bad precision %d", prec);
+  if (prec == VXB_PREC_X3 && cin1 != 0)
+    return set_error(VXB_EUNSUPPORTED, "pack: x3 precision takes a single input segment");
   if (path == 0) path = vxb_conv_select(cin, cout, k, stride);
-  size_t need = vxb_conv_weights_bytes2(cin0, cin1, cout, k, stride, path);
+  size_t need = vxb_conv_weights_bytes3(cin0, cin1, cout, k, stride, path, prec);
   if (dst_bytes < need) return set_error(VXB_EINVAL, "pack: need %zu bytes, got %zu", need, dst_bytes);
   auto wtap = [&](int co, int ci, int dx, int dy, int dz) {
     return w[((((static_cast<size_t>(co) * cin) + ci) * k[0] + dx) * k[1] + dy) * k[2] + dz];
   };
   if (is_tc(path)) {
+    if (prec == VXB_PREC_X3) {
+      const int a = x3_cin0(cin), b = x3_cin1(cin);
+      TcLayout L = tc_layout(a, b, cout, k, path_folds(path), path_nt_cap(path));
+      auto wx3 = [&](int co, int ci, int dx, int dy, int dz) {
+        return x3_weight(wtap, cin, co, ci, dx, dy, dz);
+      };
+      tc_pack(L, a, b, cout, k, wx3, static_cast<uint8_t *>(dst));
+      return VXB_OK;
+    }
     TcLayout L = tc_layout(cin0, cin1, cout, k, path_folds(path), path_nt_cap(path));
     tc_pack(L, cin0, cin1, cout, k, wtap, static_cast<uint8_t *>(dst));
     return VXB_OK;
@@ -808,6 +898,12 @@ int vxb_conv_pack_weights2(const float *w, int cin0, int cin1, int cout, const i
           }
       }
   return VXB_OK;
+}
+
+int vxb_conv_pack_weights2(const float *w, int cin0, int cin1, int cout, const int k[3],
+                           const int stride[3], int path, void *dst, size_t dst_bytes) {
+  return vxb_conv_pack_weights3(w, cin0, cin1, cout, k, stride, path, VXB_PREC_BF16, dst,
+                                dst_bytes);
 }
 
 int vxb_conv_pack_weights(const float *w, int cin, int cout, const int k[3], const int stride[3],
@@ -834,6 +930,37 @@ int vxb_conv3d(const vxb_conv_desc *d, void *stream) {
     if (d->k[i] < 1 || d->stride[i] < 1 || d->pad[i] < 0)
       return set_error(VXB_EINVAL, "conv3d: bad kernel/stride/pad");
   if (d->act < 0 || d->act > 3) return set_error(VXB_EINVAL, "conv3d: bad act %d", d->act);
+  // extents: every output voxel's window (after the segment's crop offset)
+  // lies inside the input plus its virtual zero padding; batches agree; a
+  // residual operand has the output's shape (the epilogue reads it at
+  // output coordinates)
+  {
+    const int oe[3] = {d->out.x, d->out.y, d->out.z};
+    for (int sg = 0; sg < (two ? 2 : 1); ++sg) {
+      const vxb_tensor &t = sg ? d->in1 : d->in0;
+      const int *off = sg ? d->off1 : d->off0;
+      const int ie[3] = {t.x, t.y, t.z};
+      if (t.n != d->out.n)
+        return set_error(VXB_EINVAL, "conv3d: in%d batch %d != out batch %d", sg, t.n, d->out.n);
+      for (int i = 0; i < 3; ++i)
+        if (off[i] < 0 || (oe[i] - 1) * d->stride[i] + d->k[i] > ie[i] - off[i] + 2 * d->pad[i])
+          return set_error(VXB_EINVAL,
+                           "conv3d: output extent %d on axis %d needs more than in%d extent %d "
+                           "(offset %d, pad %d, k %d, stride %d)",
+                           oe[i], i, sg, ie[i], off[i], d->pad[i], d->k[i], d->stride[i]);
+    }
+    if (additive && (d->base.n != d->out.n || d->base.c != d->out.c || d->base.x != d->out.x ||
+                     d->base.y != d->out.y || d->base.z != d->out.z))
+      return set_error(VXB_EINVAL, "conv3d: base view must have the output's shape");
+  }
+  const bool split_in = d->in0.dtype == VXB_BF16X2;
+  if (d->prec != VXB_PREC_BF16 && d->prec != VXB_PREC_X3)
+    return set_error(VXB_EINVAL, "conv3d: bad prec %d", d->prec);
+  if (split_in != (d->prec == VXB_PREC_X3))
+    return set_error(VXB_EINVAL,
+                     "conv3d: a split (VXB_BF16X2) input needs VXB_PREC_X3 weights and vice versa");
+  if (split_in && two)
+    return set_error(VXB_EUNSUPPORTED, "conv3d: split inputs take a single input segment");
   const int path = d->path ? d->path : vxb_conv_select(d->cin, d->cout, d->k, d->stride);
   cudaStream_t s = as_stream(stream);
   if (is_tc(path)) {
@@ -843,16 +970,23 @@ int vxb_conv3d(const vxb_conv_desc *d, void *stream) {
     memset(&a, 0, sizeof(a));
     a.allow_fold = path_folds(path);
     a.nt_cap = path_nt_cap(path);
-    a.in[0] = &d->in0;
-    a.in[1] = two ? &d->in1 : nullptr;
+    vxb_tensor both, hi;
+    if (split_in) {
+      split_segments(d->in0, both, hi);
+      a.in[0] = &both;
+      a.in[1] = &hi;
+    } else {
+      a.in[0] = &d->in0;
+      a.in[1] = two ? &d->in1 : nullptr;
+    }
     for (int i = 0; i < 3; ++i) {
       a.off[0][i] = d->off0[i];
-      a.off[1][i] = d->off1[i];
+      a.off[1][i] = split_in ? d->off0[i] : d->off1[i];
       a.k[i] = d->k[i];
       a.pad[i] = d->pad[i];
     }
-    a.cin0 = cin0;
-    a.cin1 = cin1;
+    a.cin0 = split_in ? x3_cin0(cin0) : cin0;
+    a.cin1 = split_in ? x3_cin1(cin0) : cin1;
     a.cout = d->cout;
     a.ox = d->out.x;
     a.oy = d->out.y;
@@ -868,6 +1002,8 @@ int vxb_conv3d(const vxb_conv_desc *d, void *stream) {
     a.act = d->act;
     a.alpha = d->alpha;
     if (d->pool_mode == VXB_POOL_FUSED_MAX122) {
+      if (split_in || d->out.dtype == VXB_BF16X2)
+        return set_error(VXB_EUNSUPPORTED, "fused pooling: bf16 storage only");
       if ((rc = check_view(&d->pool_out, "conv3d.pool_out"))) return rc;
       const vxb_tensor &pv = d->pool_out;
       if (pv.n != d->out.n || pv.c != d->cout || pv.x != d->out.x || pv.y != d->out.y / 2 ||
@@ -974,56 +1110,81 @@ static int deconv_rep_n(int cout, const int k[3], const int stride[3], int path)
   return ntr;
 }
 
-size_t vxb_deconv_weights_bytes(int cin, int cout, const int k[3], const int stride[3],
-                                int path) {
-  if (const int rn = deconv_rep_n(cout, k, stride, path)) {
-    int one[3] = {1, 1, 1};
-    return tc_bytes_per_rep(tc_layout(cin, 0, k[0] * k[1] * k[2] * rn, one));
-  }
-  if (deconv_tc(k, stride, path)) {
-    int one[3] = {1, 1, 1};
-    return static_cast<size_t>(k[0] * k[1] * k[2]) * tc_bytes_per_rep(tc_layout(cin, 0, cout, one));
-  }
+// K segments of a tensor-core deconv's 1x1x1 GEMM: the input fmaps, or the
+// two x3 segments over a split input
+static void deconv_segments(int cin, int prec, int &c0, int &c1) {
+  c0 = prec == VXB_PREC_X3 ? x3_cin0(cin) : cin;
+  c1 = prec == VXB_PREC_X3 ? x3_cin1(cin) : 0;
+}
+
+size_t vxb_deconv_weights_bytes3(int cin, int cout, const int k[3], const int stride[3], int path,
+                                 int prec) {
+  int one[3] = {1, 1, 1}, c0, c1;
+  deconv_segments(cin, prec, c0, c1);
+  if (const int rn = deconv_rep_n(cout, k, stride, path))
+    return tc_bytes_per_rep(tc_layout(c0, c1, k[0] * k[1] * k[2] * rn, one));
+  if (deconv_tc(k, stride, path))
+    return static_cast<size_t>(k[0] * k[1] * k[2]) * tc_bytes_per_rep(tc_layout(c0, c1, cout, one));
   return static_cast<size_t>(cout) * cin * k[0] * k[1] * k[2] * sizeof(float);
 }
 
-int vxb_deconv_pack_weights(const float *w, int cin, int cout, const int k[3], const int stride[3],
-                            int path, void *dst, size_t dst_bytes) {
+size_t vxb_deconv_weights_bytes(int cin, int cout, const int k[3], const int stride[3],
+                                int path) {
+  return vxb_deconv_weights_bytes3(cin, cout, k, stride, path, VXB_PREC_BF16);
+}
+
+int vxb_deconv_pack_weights3(const float *w, int cin, int cout, const int k[3],
+                             const int stride[3], int path, int prec, void *dst,
+                             size_t dst_bytes) {
   if (!w || !dst) return set_error(VXB_EINVAL, "deconv pack: null pointer");
+  if (prec != VXB_PREC_BF16 && prec != VXB_PREC_X3)
+    return set_error(VXB_EINVAL, "deconv pack: bad precision %d", prec);
   if (path == VXB_PATH_TC && !deconv_tc_ok(k, stride))
     return set_error(VXB_EUNSUPPORTED, "tensor-core deconv needs k == stride, <= 8 taps");
-  size_t need = vxb_deconv_weights_bytes(cin, cout, k, stride, path);
+  size_t need = vxb_deconv_weights_bytes3(cin, cout, k, stride, path, prec);
   if (dst_bytes < need) return set_error(VXB_EINVAL, "deconv pack: need %zu bytes", need);
   if (!deconv_tc(k, stride, path)) {
     memcpy(dst, w, need);
     return VXB_OK;
   }
-  int one[3] = {1, 1, 1};
+  int one[3] = {1, 1, 1}, c0, c1;
+  deconv_segments(cin, prec, c0, c1);
+  // weight of GEMM K column ci for output column co at tap (dx, dy, dz)
+  auto wk = [&](int co, int ci, int dx, int dy, int dz) -> float {
+    auto wstd = [&](int o, int i, int a, int b, int c) {
+      return w[((((static_cast<size_t>(o) * cin) + i) * k[0] + a) * k[1] + b) * k[2] + c];
+    };
+    if (prec == VXB_PREC_X3) return x3_weight(wstd, cin, co, ci, dx, dy, dz);
+    return wstd(co, ci, dx, dy, dz);
+  };
   if (const int rn = deconv_rep_n(cout, k, stride, path)) {
     // column co' = tap * rn + co, taps in (dx, dy, dz) order
     const int reps = k[0] * k[1] * k[2];
-    TcLayout L = tc_layout(cin, 0, reps * rn, one);
+    TcLayout L = tc_layout(c0, c1, reps * rn, one);
     auto wtap = [&](int cop, int ci, int, int, int) {
       const int r = cop / rn, co = cop - r * rn;
       if (co >= cout) return 0.f;
       const int dz = r % k[2], dy = (r / k[2]) % k[1], dx = r / (k[2] * k[1]);
-      return w[((((static_cast<size_t>(co) * cin) + ci) * k[0] + dx) * k[1] + dy) * k[2] + dz];
+      return wk(co, ci, dx, dy, dz);
     };
-    tc_pack(L, cin, 0, reps * rn, one, wtap, static_cast<uint8_t *>(dst));
+    tc_pack(L, c0, c1, reps * rn, one, wtap, static_cast<uint8_t *>(dst));
     return VXB_OK;
   }
-  TcLayout L = tc_layout(cin, 0, cout, one);
+  TcLayout L = tc_layout(c0, c1, cout, one);
   size_t per = tc_bytes_per_rep(L);
   int r = 0;
   for (int dx = 0; dx < k[0]; ++dx)
     for (int dy = 0; dy < k[1]; ++dy)
       for (int dz = 0; dz < k[2]; ++dz, ++r) {
-        auto wtap = [&](int co, int ci, int, int, int) {
-          return w[((((static_cast<size_t>(co) * cin) + ci) * k[0] + dx) * k[1] + dy) * k[2] + dz];
-        };
-        tc_pack(L, cin, 0, cout, one, wtap, static_cast<uint8_t *>(dst) + r * per);
+        auto wtap = [&](int co, int ci, int, int, int) { return wk(co, ci, dx, dy, dz); };
+        tc_pack(L, c0, c1, cout, one, wtap, static_cast<uint8_t *>(dst) + r * per);
       }
   return VXB_OK;
+}
+
+int vxb_deconv_pack_weights(const float *w, int cin, int cout, const int k[3], const int stride[3],
+                            int path, void *dst, size_t dst_bytes) {
+  return vxb_deconv_pack_weights3(w, cin, cout, k, stride, path, VXB_PREC_BF16, dst, dst_bytes);
 }
 
 int vxb_deconv3d(const vxb_deconv_desc *d, void *stream) {
@@ -1044,13 +1205,26 @@ int vxb_deconv3d(const vxb_deconv_desc *d, void *stream) {
   cudaStream_t s = as_stream(stream);
   if (d->path == VXB_PATH_TC && !deconv_tc_ok(d->k, d->stride))
     return set_error(VXB_EUNSUPPORTED, "tensor-core deconv needs k == stride, <= 8 taps");
+  const bool split_in = d->in.dtype == VXB_BF16X2;
+  if (d->prec != VXB_PREC_BF16 && d->prec != VXB_PREC_X3)
+    return set_error(VXB_EINVAL, "deconv3d: bad prec %d", d->prec);
+  if (split_in != (d->prec == VXB_PREC_X3))
+    return set_error(VXB_EINVAL,
+                     "deconv3d: a split (VXB_BF16X2) input needs VXB_PREC_X3 weights and vice versa");
   if (deconv_tc(d->k, d->stride, d->path)) {
     TcLaunch a;
     memset(&a, 0, sizeof(a));
-    a.in[0] = &d->in;
-    a.in[1] = nullptr;
+    vxb_tensor both, hi;
+    if (split_in) {
+      split_segments(d->in, both, hi);
+      a.in[0] = &both;
+      a.in[1] = &hi;
+    } else {
+      a.in[0] = &d->in;
+      a.in[1] = nullptr;
+    }
     for (int i = 0; i < 3; ++i) a.k[i] = 1;
-    a.cin0 = d->cin;
+    deconv_segments(d->cin, d->prec, a.cin0, a.cin1);
     a.cout = d->cout;
     a.ox = d->in.x;
     a.oy = d->in.y;
@@ -1198,8 +1372,10 @@ int vxb_pack_zwin(const vxb_tensor *src, const vxb_tensor *dst, int kz, int pz, 
     return rc;
   if (src->blocked || src->dtype != VXB_F32 || src->c != 1)
     return set_error(VXB_EINVAL, "pack_zwin: source must be a 1-channel fp32 standard view");
-  if (!dst->blocked || dst->dtype != VXB_BF16 || dst->c != kz || kz < 1 || kz > 8)
-    return set_error(VXB_EINVAL, "pack_zwin: destination must be bf16 blocked with c == kz <= 8");
+  if (!dst->blocked || (dst->dtype != VXB_BF16 && dst->dtype != VXB_BF16X2) || dst->c != kz ||
+      kz < 1 || kz > 8)
+    return set_error(VXB_EINVAL,
+                     "pack_zwin: destination must be (split) bf16 blocked with c == kz <= 8");
   if (pz < 0 || dst->n != src->n || dst->x != src->x || dst->y != src->y ||
       dst->z != src->z + 2 * pz - kz + 1)
     return set_error(VXB_EINVAL, "pack_zwin: shape mismatch (dst z = src z + 2 pz - kz + 1)");

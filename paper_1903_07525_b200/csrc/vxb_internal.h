@@ -152,6 +152,25 @@ constexpr int DCO_DIRECT = 16;  // output fmaps per direct-conv CTA
 int set_error(int code, const char *fmt, ...);
 int check_cuda(cudaError_t e, const char *what);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-device setting:
+// done once per (kernel, device), thread-safe (run_tiled drives several GPUs
+// from one thread each).  Keyed by the kernel's address: every instantiation
+// of a template kernel is its own function.
+bool smem_attr_done(const void *kern, int dev);   // vxb_abi.cu
+void smem_attr_mark(const void *kern, int dev);
+template <typename... KArgs>
+int ensure_smem_attr(void (*kern)(KArgs...), int bytes, const char *what) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return check_cuda(e, what);
+  const void *k = reinterpret_cast<const void *>(kern);
+  if (smem_attr_done(k, dev)) return 0;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return check_cuda(e, what);
+  smem_attr_mark(k, dev);
+  return 0;
+}
+
 // ---- programmatic dependent launch (PDL)
 // Every vxb kernel is launched with programmatic stream serialization: it
 // may start while its predecessor drains, signals its own dependents at

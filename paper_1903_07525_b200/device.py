@@ -46,6 +46,9 @@ class DTensor:
     t: object                 # torch.Tensor: 6-D blocked or 5-D standard view
     c: int                    # logical fmap count
     blocked: bool = True
+    # split bf16 (VXB_BF16X2): t is (n, 2*ceil(C/8), x, y, z, 8) bf16 with
+    # chunk 2j = hi plane and 2j+1 = lo plane of fmap chunk j
+    split: bool = False
 
     @property
     def n(self) -> int:
@@ -65,6 +68,8 @@ class DTensor:
     @property
     def dtype_code(self) -> int:
         torch = _torch()
+        if self.split:
+            return _lib.VXB_BF16X2
         if self.t.dtype == torch.bfloat16:
             return _lib.VXB_BF16
         if self.t.dtype == torch.float32:
@@ -83,22 +88,26 @@ class DTensor:
             raise LayoutError("blocked view must have a contiguous lane axis")
         for i in range(5):
             v.s[i] = int(st[i])
+        if self.split:
+            v.s[1] = 2 * int(st[1])      # one fmap chunk = a hi and a lo plane
         return v
 
     def window(self, lo, size) -> "DTensor":
         """Spatial sub-view [lo, lo+size) (crop), no copy."""
         sl = tuple(slice(int(a), int(a) + int(b)) for a, b in zip(lo, size))
-        return DTensor(self.t[(slice(None), slice(None)) + sl], self.c, self.blocked)
+        return DTensor(self.t[(slice(None), slice(None)) + sl], self.c, self.blocked, self.split)
 
 
 def empty_blocked(n, c, spatial, dtype="bf16", device=None, zero=False) -> DTensor:
+    """dtype: "bf16", "fp32" or "split" (hi + lo bf16 planes per chunk)."""
     torch = _torch()
-    td = torch.bfloat16 if dtype == "bf16" else torch.float32
+    td = torch.float32 if dtype == "fp32" else torch.bfloat16
     x, y, z = (int(v) for v in spatial)
-    shape = (int(n), chunks(c), x, y, z, LANES)
+    planes = 2 if dtype == "split" else 1
+    shape = (int(n), planes * chunks(c), x, y, z, LANES)
     dev = device or torch.device("cuda", torch.cuda.current_device())
     t = torch.zeros(shape, dtype=td, device=dev) if zero else torch.empty(shape, dtype=td, device=dev)
-    return DTensor(t, int(c), True)
+    return DTensor(t, int(c), True, dtype == "split")
 
 
 def standard(t, c=None) -> DTensor:

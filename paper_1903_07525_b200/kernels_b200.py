@@ -107,18 +107,20 @@ def _packed(inv, precision, transposed):
         scale = None
         if inv.additive and inv.base_scale is not None:
             scale = np.asarray(inv.base_scale, dtype=np.float32).reshape(-1)[:inv.out_fmaps]
+        prec = "x3" if precision == "x3" else "bf16"
         if transposed:
             cache[key] = K.pack_deconv(w, bias, stride=inv.stride, base_scale=scale,
-                                       force_gather=(precision == "fp32"))
+                                       force_gather=(precision == "fp32"), precision=prec)
         else:
             path = _lib.PATH_DIRECT if precision == "fp32" else 0
-            cache[key] = K.pack_conv(w, bias, stride=inv.stride, base_scale=scale, path=path)
+            cache[key] = K.pack_conv(w, bias, stride=inv.stride, base_scale=scale, path=path,
+                                     precision=prec)
     return cache[key]
 
 
 def _run(inv: ConvInvocation, precision: str, transposed: bool) -> None:
     import torch
-    if precision not in ("bf16", "fp32"):
+    if precision not in ("bf16", "fp32", "x3"):
         raise ExecutionError("unknown precision %r" % (precision,))
     pk = _packed(inv, precision, transposed)
     if _is_device(inv.in_view):
@@ -126,7 +128,7 @@ def _run(inv: ConvInvocation, precision: str, transposed: bool) -> None:
         base = inv.base_view if inv.additive else None
         host_out = None
     else:
-        dt = "fp32" if precision == "fp32" else "bf16"
+        dt = {"fp32": "fp32", "x3": "split"}.get(precision, "bf16")
         x = _to_dev(inv.in_view, inv.in_fmaps, dt)
         base = _to_dev(inv.base_view, inv.out_fmaps, dt) if inv.additive else None
         _, _, ox, oy, oz, _ = inv.out_view.shape

@@ -47,17 +47,23 @@ class PackedConv:
     k: tuple
     stride: tuple
     path: int
+    prec: int = 0        # _lib.PREC_BF16 / PREC_X3 (split-bf16 inputs)
 
     @property
     def cin(self) -> int:
         return self.cin0 + self.cin1
 
 
+PRECISIONS = {"bf16": _lib.PREC_BF16, "x3": _lib.PREC_X3}
+
+
 def pack_conv(kernel, bias, *, stride=(1, 1, 1), base_scale=None, cin_split=None,
-              path=0, out_shape=None, device=None) -> PackedConv:
+              path=0, out_shape=None, device=None, precision="bf16") -> PackedConv:
     """Pack a standard (cout, cin, kx, ky, kz) fp32 kernel bank for vxb_conv3d.
     ``out_shape`` (x, y, z) of the output, when known, lets the library pick
-    the tile layout (vxb_conv_select_shape)."""
+    the tile layout (vxb_conv_select_shape).  ``precision="x3"`` packs for a
+    split-bf16 input: bf16(W) against its hi and lo planes and
+    bf16(W - bf16(W)) against hi (VXB_PREC_X3)."""
     import torch
     L = _lib.lib()
     w = np.ascontiguousarray(np.asarray(kernel, dtype=np.float32))
@@ -76,15 +82,16 @@ def pack_conv(kernel, bias, *, stride=(1, 1, 1), base_scale=None, cin_split=None
             path = L.vxb_conv_select(cin, cout, _lib.i3(k), _lib.i3(stride))
     if cin1 and path not in _lib.TC_PATHS:
         raise ExecutionError("a two-input (fused concat) conv needs the tensor-core path")
-    nbytes = L.vxb_conv_weights_bytes2(cin0, cin1, cout, _lib.i3(k), _lib.i3(stride), path)
-    host = np.zeros(nbytes, dtype=np.uint8)
-    _lib.check(L.vxb_conv_pack_weights2(w.ctypes.data, cin0, cin1, cout, _lib.i3(k),
-                                        _lib.i3(stride), path, host.ctypes.data, nbytes),
-               "vxb_conv_pack_weights2")
+    prec = PRECISIONS[precision]
+    nbytes = L.vxb_conv_weights_bytes3(cin0, cin1, cout, _lib.i3(k), _lib.i3(stride), path, prec)
+    host = np.zeros(max(nbytes, 1), dtype=np.uint8)
+    _lib.check(L.vxb_conv_pack_weights3(w.ctypes.data, cin0, cin1, cout, _lib.i3(k),
+                                        _lib.i3(stride), path, prec, host.ctypes.data, nbytes),
+               "vxb_conv_pack_weights3")
     dev = device or torch.device("cuda", torch.cuda.current_device())
     scale = None if base_scale is None else device_vector(base_scale, cout, dev)
     return PackedConv(torch.from_numpy(host).to(dev), device_vector(bias, cout, dev), scale,
-                      cin0, cin1, cout, k, stride, path)
+                      cin0, cin1, cout, k, stride, path, prec)
 
 
 def conv3d(x: DTensor, pk: PackedConv, out: DTensor, *, pad=(0, 0, 0), base: DTensor = None,
@@ -110,6 +117,7 @@ def conv3d(x: DTensor, pk: PackedConv, out: DTensor, *, pad=(0, 0, 0), base: DTe
     d.pad = _lib.i3(pad)
     d.act, d.alpha = _act(fused_act)
     d.path = pk.path
+    d.prec = pk.prec
     if pool_out is not None:
         d.pool_mode = 1
         d.pool_out = pool_out.vxb()
@@ -149,10 +157,11 @@ class PackedDeconv:
     k: tuple
     stride: tuple
     path: int = 0
+    prec: int = 0
 
 
 def pack_deconv(kernel, bias, *, stride, base_scale=None, force_gather=False,
-                device=None) -> PackedDeconv:
+                device=None, precision="bf16") -> PackedDeconv:
     """Pack a (cout, cin, kx, ky, kz) deconv bank (oracle.py:67-93 orientation)."""
     import torch
     L = _lib.lib()
@@ -161,15 +170,16 @@ def pack_deconv(kernel, bias, *, stride, base_scale=None, force_gather=False,
     k = tuple(int(v) for v in w.shape[2:])
     stride = tuple(int(s) for s in stride)
     path = _lib.PATH_DIRECT if force_gather else 0
-    nbytes = L.vxb_deconv_weights_bytes(cin, cout, _lib.i3(k), _lib.i3(stride), path)
+    prec = PRECISIONS[precision]
+    nbytes = L.vxb_deconv_weights_bytes3(cin, cout, _lib.i3(k), _lib.i3(stride), path, prec)
     host = np.zeros(nbytes, dtype=np.uint8)
-    _lib.check(L.vxb_deconv_pack_weights(w.ctypes.data, cin, cout, _lib.i3(k), _lib.i3(stride),
-                                         path, host.ctypes.data, nbytes),
-               "vxb_deconv_pack_weights")
+    _lib.check(L.vxb_deconv_pack_weights3(w.ctypes.data, cin, cout, _lib.i3(k), _lib.i3(stride),
+                                          path, prec, host.ctypes.data, nbytes),
+               "vxb_deconv_pack_weights3")
     dev = device or torch.device("cuda", torch.cuda.current_device())
     scale = None if base_scale is None else device_vector(base_scale, cout, dev)
     return PackedDeconv(torch.from_numpy(host).to(dev), device_vector(bias, cout, dev), scale,
-                        cin, cout, k, stride, path)
+                        cin, cout, k, stride, path, prec)
 
 
 def deconv3d(x: DTensor, pk: PackedDeconv, out: DTensor, *, base: DTensor = None,
@@ -188,6 +198,7 @@ def deconv3d(x: DTensor, pk: PackedDeconv, out: DTensor, *, base: DTensor = None
     d.stride = _lib.i3(pk.stride)
     d.act, d.alpha = _act(fused_act)
     d.path = pk.path
+    d.prec = pk.prec
     _lib.check(L.vxb_deconv3d(ctypes.byref(d), stream or current_stream_handle()), "vxb_deconv3d")
 
 

@@ -62,7 +62,7 @@ class _Value:
     @property
     def nbytes(self):
         n, c, x, y, z = self.dims
-        esz = 2 if self.dtype == "bf16" else 4
+        esz = 2 if self.dtype == "bf16" else 4     # fp32, or split bf16 (hi + lo)
         return n * chunks(c) * x * y * z * LANES * esz
 
 
@@ -70,7 +70,7 @@ class PlanRunner:
     """Executes one ExecutionPlan on one B200; reusable, deterministic."""
 
     def __init__(self, plan, backend=None, *, device=None, use_graph=True, fuse_concat=True,
-                 fuse_pool=False, fuse_input=False):
+                 fuse_pool=False, fuse_input=False, probe=None):
         torch = _torch()
         from .backend import resolve_device_backend
         self.backend = resolve_device_backend(backend)
@@ -81,6 +81,10 @@ class PlanRunner:
             "cuda", torch.cuda.current_device())
         self.use_graph = use_graph
         self.precision = self.backend.precision
+        # activation storage: bf16, fp32 (CUDA-core path) or split bf16 (x3)
+        self.storage = {"x3": "split"}.get(self.precision, self.precision)
+        # weight packing precision of the tensor-core paths
+        self._prec = "x3" if self.precision == "x3" else "bf16"
         self.fuse_concat = fuse_concat and self.precision == "bf16"
         self.fuse_pool = fuse_pool and self.precision == "bf16"
         self.fuse_input = fuse_input
@@ -93,6 +97,13 @@ class PlanRunner:
         # their CUDA graphs in the middle of another runner's stream capture
         # (cudaGraphExecDestroy is illegal during capture and invalidates it).
         self._indep_flag = [False]
+        # live timing of one step (bench roofline): external timing events
+        # recorded around that step's launch, inside the captured graph
+        self.probe = probe
+        self._probe_ev = None
+        if probe is not None:
+            self._probe_ev = (torch.cuda.Event(enable_timing=True, external=True),
+                              torch.cuda.Event(enable_timing=True, external=True))
         with torch.cuda.device(self.device):
             self._lower()
             self._allocate()
@@ -109,7 +120,7 @@ class PlanRunner:
         self._ops = []       # (kind, step, info dict)
 
         def new_value(dims):
-            v = _Value(dims, self.precision)
+            v = _Value(dims, self.storage)
             self._values.append(v)
             return v
 
@@ -296,10 +307,11 @@ class PlanRunner:
             if v.slot is None:
                 continue
             n, c, x, y, z = v.dims
-            td = torch.bfloat16 if v.dtype == "bf16" else torch.float32
-            numel = n * chunks(c) * x * y * z * LANES
-            t = self._storage[v.slot].view(td)[:numel].view(n, chunks(c), x, y, z, LANES)
-            v.dt = DTensor(t, c, True)
+            td = torch.float32 if v.dtype == "fp32" else torch.bfloat16
+            planes = 2 if v.dtype == "split" else 1     # split: hi, lo plane per chunk
+            numel = n * planes * chunks(c) * x * y * z * LANES
+            t = self._storage[v.slot].view(td)[:numel].view(n, planes * chunks(c), x, y, z, LANES)
+            v.dt = DTensor(t, c, True, v.dtype == "split")
         # network boundary: fp32 standard staging tensors (device + pinned host)
         self._in_std = {name: torch.empty(self._input_dims[name], dtype=torch.float32,
                                           device=self.device)
@@ -390,7 +402,7 @@ class PlanRunner:
                         np.transpose(np.asarray(kern, np.float32)[:, 0], (0, 3, 1, 2))[..., None])
                     pk = K.pack_conv(kz_w, w.tensor(st.name, ROLE_BIAS), stride=stride,
                                      base_scale=scale, out_shape=tuple(info["out"].dims[2:]),
-                                     device=dev)
+                                     device=dev, precision=self._prec)
                     pool = info["pool_out"].dt if "pool_out" in info else None
                     calls.append(lambda x=xz, pk=pk, out=out, base=base,
                                  pad=(info["pad"][0], info["pad"][1], 0), act=st.fused_act,
@@ -400,7 +412,8 @@ class PlanRunner:
                 else:
                     pk = K.pack_conv(kern, w.tensor(st.name, ROLE_BIAS), stride=stride,
                                      base_scale=scale, path=self._conv_path,
-                                     out_shape=tuple(info["out"].dims[2:]), device=dev)
+                                     out_shape=tuple(info["out"].dims[2:]), device=dev,
+                                     precision=self._prec)
                     x = fused_in.get(id(info), info["x"].dt)
                     if id(info) in fused_in and pk.path not in _lib.TC_PATHS:
                         raise ExecutionError("fused fp32 input needs the tensor-core conv path")
@@ -414,7 +427,8 @@ class PlanRunner:
                 scale = st.base_scale if st.additive else None
                 pk = K.pack_deconv(w.tensor(st.name, ROLE_KERNEL), w.tensor(st.name, ROLE_BIAS),
                                    stride=tuple(st.params["stride"]), base_scale=scale,
-                                   force_gather=self.precision == "fp32", device=dev)
+                                   force_gather=self.precision == "fp32", device=dev,
+                                   precision=self._prec)
                 calls.append(lambda x=info["ins"][0].dt, pk=pk, out=out, base=base,
                              act=st.fused_act: K.deconv3d(x, pk, out, base=base, fused_act=act))
             elif kind is LayerKind.POOLING:
@@ -446,6 +460,19 @@ class PlanRunner:
             else:
                 raise ExecutionError("plan step %r has unrunnable kind %s" % (st.name, kind))
         self.op_calls = calls[n_in:n_in + len(self._ops)]   # one device call per lowered op
+        self.op_names = [st.name for _, st, _ in self._ops]
+        if self.probe is not None:
+            if self.probe not in self.op_names:
+                raise ExecutionError("probe step %r is not a lowered op of this plan" % self.probe)
+            i = n_in + self.op_names.index(self.probe)
+            ev = self._probe_ev
+
+            def probed(c=calls[i], ev=ev):
+                torch = _torch()
+                ev[0].record(torch.cuda.current_stream())
+                c()
+                ev[1].record(torch.cuda.current_stream())
+            calls[i] = probed
         for name, v in self._out_values.items():
             if name in self._fused_outputs:
                 continue
@@ -458,7 +485,7 @@ class PlanRunner:
         stride-1 tensor-core conv with <= 8 z taps (the U-nets' first layer:
         its 8-lane chunks would otherwise be 7/8 padding).  Returns the
         packed input tensor (n, kz, x, y, oz), kz and the z pad, or None."""
-        if self.precision != "bf16" or os.environ.get("VXB_ZWIN", "1") != "1":
+        if self.precision not in ("bf16", "x3") or os.environ.get("VXB_ZWIN", "1") != "1":
             return None
         if v.dims[1] != 1 or v.readers != 1 or len(rs) != 1:
             return None
@@ -477,7 +504,8 @@ class PlanRunner:
         n, _, x, y, z = v.dims
         oz = z + 2 * pz - k[2] + 1
         from .device import empty_blocked
-        return empty_blocked(n, k[2], (x, y, oz), "bf16", self.device, zero=True), k[2], pz
+        return (empty_blocked(n, k[2], (x, y, oz), self.storage, self.device, zero=True), k[2],
+                pz)
 
     def _f32in_ok(self, name, st, info) -> bool:
         """Can this conv read network input `name` as fp32 NCDHW directly
@@ -606,7 +634,7 @@ class PlanRunner:
             if o is None or tuple(o.shape) != tuple(t.shape) or not staging.is_pinned(o):
                 raise ExecutionError("run_async needs a pinned float32 out[%r] of shape %s"
                                      % (name, tuple(t.shape)))
-        if self._graph is None:
+        if self._graph is None and self.use_graph:
             self._replay()              # first call: capture (synchronous once)
             self.stream.synchronize()
         with torch.cuda.stream(self.stream):
@@ -618,6 +646,12 @@ class PlanRunner:
             ev = torch.cuda.Event()
             ev.record(self.stream)
         return PendingRun(ev, {name: out[name] for name in self._out_std})
+
+    def probe_ms(self) -> float:
+        """Duration of the probed step in the last completed run (ms)."""
+        if self._probe_ev is None:
+            raise ExecutionError("PlanRunner was built without a probe")
+        return self._probe_ev[0].elapsed_time(self._probe_ev[1])
 
     def input_buffers(self) -> dict:
         """The static device input tensors the captured graph reads.  Filling

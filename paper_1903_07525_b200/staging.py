@@ -112,3 +112,84 @@ def download(device_tensor, pinned, stream, out=None) -> np.ndarray:
     for f in futs:
         f.result()
     return out
+
+
+# ------------------------------------------------------------------ row staging
+# DeviceTiler.run_host streams a large volume row by row.  Page-locked host
+# arrays move by direct DMA; pageable ones go through two pinned staging
+# slots per direction, filled / drained by the thread pool while the copy
+# engines and the convolutions work on the neighbouring rows.
+
+def _plane_jobs(dst: np.ndarray, src: np.ndarray):
+    """(dst, src) pairs of (b, c, x-block) sub-blocks of about CHUNK_BYTES."""
+    nb, nc, nx = dst.shape[:3]
+    plane = max(1, int(np.prod(dst.shape[3:])) * 4)
+    step = max(1, CHUNK_BYTES // plane)
+    return [(dst[b, c, x:x + step], src[b, c, x:x + step])
+            for b in range(nb) for c in range(nc) for x in range(0, nx, step)]
+
+
+class RowStager:
+    """Two pinned staging slots per direction for pageable volumes."""
+
+    def __init__(self):
+        self._in = [None, None]      # (pinned tensor, DMA-done event)
+        self._out = [None, None]     # (pinned tensor, host-copy future)
+
+    @staticmethod
+    def _grow(entry, numel):
+        import torch
+        if entry is None or entry[0].numel() < numel:
+            return torch.empty(numel, dtype=torch.float32, pin_memory=True)
+        return entry[0]
+
+    def upload(self, slot, src_view: np.ndarray, dst, stream) -> None:
+        """dst (contiguous device tensor) <- src_view (any host float32 view)."""
+        import torch
+        ent = self._in[slot]
+        if ent is not None and ent[1] is not None:
+            ent[1].synchronize()                 # the slot's previous DMA has read it
+        buf = self._grow(ent, dst.numel())
+        st = buf[:dst.numel()].view(dst.shape)
+        st_np = st.numpy()
+        futs = [pool().submit(np.copyto, d, s) for d, s in _plane_jobs(st_np, src_view)]
+        for f in futs:
+            f.result()
+        with torch.cuda.stream(stream):
+            dst.copy_(st, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        self._in[slot] = (buf, ev)
+
+    def download(self, slot, src, out_view: np.ndarray, stream) -> None:
+        """out_view (host view) <- src (contiguous device tensor), asynchronously:
+        the DMA is enqueued on ``stream``, a pool thread copies the staged
+        result into out_view once it lands (``finish`` waits for all)."""
+        import torch
+        ent = self._out[slot]
+        if ent is not None and ent[1] is not None:
+            ent[1].result()                      # the slot's previous host copy is done
+        buf = self._grow(ent, src.numel())
+        st = buf[:src.numel()].view(src.shape)
+        with torch.cuda.stream(stream):
+            st.copy_(src, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        st_np = st.numpy()
+
+        def land():
+            ev.synchronize()
+            jobs = _plane_jobs(out_view, st_np)
+            half = len(jobs) // 2
+            # the other half in a second pool thread (at most two rows land
+            # at once, so the pool never waits on itself)
+            f = pool().submit(lambda: [np.copyto(d, s) for d, s in jobs[half:]])
+            for d, s in jobs[:half]:
+                np.copyto(d, s)
+            f.result()
+        self._out[slot] = (buf, pool().submit(land))
+
+    def finish(self) -> None:
+        for ent in self._out:
+            if ent is not None and ent[1] is not None:
+                ent[1].result()

@@ -141,15 +141,27 @@ def partition(n_tiles: int, parts: int, rank: int) -> range:
 
 
 class DeviceTiler:
-    """Runs a block of tiles of one grid on one GPU, volume slab resident.
+    """Runs blocks of tiles of one grid on one GPU.
 
     ``streams`` PlanRunners (each with its own graph, buffers and CUDA
-    stream) take the tiles round robin, so consecutive patches overlap: the
-    deep U-net levels of one patch leave most SMs idle (few output tiles),
-    and the next patch's large levels fill them.  Patches are independent,
-    so this changes no result."""
+    stream) take the patch batches round robin, so consecutive batches
+    overlap: the deep U-net levels of one batch leave most SMs idle (few
+    output tiles), and the next batch's large levels fill them.  Patches are
+    independent, so this changes no result.
 
-    def __init__(self, plan, grid: TileGrid, device, backend=None, streams=None, batch=None):
+    Two ways to feed it:
+      * resident (``bind_slabs`` + ``run``): an input slab and an output slab
+        already in HBM (the bench's device-timed value);
+      * streamed (``run_host``): tiles are processed x-row by x-row (a row =
+        the tiles sharing one x cut); each row's input slab is uploaded on a
+        copy stream while the previous row computes, and each row's output is
+        downloaded while the next one computes (two-deep device rings), so
+        PCIe traffic overlaps the convolutions.  Page-locked host arrays
+        (``staging.pinned_empty``) move by direct DMA; pageable ones go through
+        pinned staging chunks copied by a thread pool."""
+
+    def __init__(self, plan, grid: TileGrid, device, backend=None, streams=None, batch=None,
+                 probe=None):
         import torch
         from .plan import rebatch
         from .runner import PlanRunner
@@ -161,18 +173,25 @@ class DeviceTiler:
         # one kernel (their few output tiles alone leave most SMs idle).
         # Config-5 volume, 2 streams: 1 -> 170.6 ms, 2 -> 149.9, 3 -> 138.4,
         # 4 -> 136.0 ms
-
         self.batch = max(1, int(batch if batch is not None else
                                 os.environ.get("VOXPLAN_PATCH_BATCH", "4")))
-        if plan.inputs[0][2][0] != 1:
+        self.vol_batch = int(plan.inputs[0][2][0])
+        if self.vol_batch != 1:
             self.batch = 1                 # the volume's own batch already fills the plan
         bplan = rebatch(plan, self.batch) if self.batch > 1 else plan
         with torch.cuda.device(self.device):
-            self.runners = [PlanRunner(bplan, backend=backend, device=self.device)
-                            for _ in range(max(1, n))]
+            self.runners = [PlanRunner(bplan, backend=backend, device=self.device,
+                                       probe=probe if i == 0 else None)
+                            for i in range(max(1, n))]
+            self.copy_in = torch.cuda.Stream(device=self.device)
+            self.copy_out = torch.cuda.Stream(device=self.device)
         self.runner = self.runners[0]
         self.in_name = plan.inputs[0][0]
+        self.out_fmaps = int(plan.outputs[0][2][1])
+        self._rings = None
+        self.slab = self.out_slab = None
 
+    # ------------------------------------------------------------ geometry
     def slab_bounds(self, tiles):
         lo = [min(t.in_lo[d] for t in tiles) for d in range(3)]
         hi = [max(t.in_lo[d] + self.grid.patch_in[d] for t in tiles) for d in range(3)]
@@ -180,19 +199,16 @@ class DeviceTiler:
         ohi = [max(t.out_lo[d] + t.keep_hi[d] - t.keep_lo[d] for t in tiles) for d in range(3)]
         return lo, hi, olo, ohi
 
-    def upload(self, volume, tiles):
-        """Copy the input slab the tiles read to the device (one H2D)."""
-        torch = self.torch
-        lo, hi, olo, ohi = self.slab_bounds(tiles)
-        win = (slice(None), slice(None)) + tuple(slice(a, b) for a, b in zip(lo, hi))
-        host = torch.from_numpy(np.ascontiguousarray(volume[win], dtype=np.float32))
-        with torch.cuda.device(self.device):
-            self.slab = host.pin_memory().to(self.device, non_blocking=True)
-            out_shape = (host.shape[0],) + tuple(
-                self.runner._out_std[next(iter(self.runner._out_std))].shape[1:2])
-            self.out_slab = torch.empty(out_shape + tuple(b - a for a, b in zip(olo, ohi)),
-                                        dtype=torch.float32, device=self.device)
-        self.lo, self.olo = lo, olo
+    @staticmethod
+    def rows(tiles):
+        """Tiles grouped by x cut (consecutive runs of equal in_lo[0])."""
+        out = []
+        for t in tiles:
+            if out and out[-1][0].in_lo[0] == t.in_lo[0]:
+                out[-1].append(t)
+            else:
+                out.append([t])
+        return out
 
     @property
     def launches_per_tile(self) -> float:
@@ -202,58 +218,201 @@ class DeviceTiler:
         """Kernel launches to run n_tiles (batches of self.batch patches)."""
         return self.runner.launches * -(-n_tiles // self.batch)
 
+    # ------------------------------------------------------------ resident
+    def bind_slabs(self, slab, lo, out_slab, olo):
+        """Device input slab (n, c, X, Y, Z) whose voxel (0,0,0) is volume
+        coordinate ``lo``, and output slab whose (0,0,0) is output ``olo``."""
+        self.slab, self.lo, self.out_slab, self.olo = slab, tuple(lo), out_slab, tuple(olo)
+
+    def upload(self, volume, tiles):
+        """Copy the input slab the tiles read to the device and allocate the
+        matching output slab (resident mode)."""
+        torch = self.torch
+        lo, hi, olo, ohi = self.slab_bounds(tiles)
+        win = (slice(None), slice(None)) + tuple(slice(a, b) for a, b in zip(lo, hi))
+        with torch.cuda.device(self.device):
+            slab = torch.from_numpy(np.ascontiguousarray(volume[win], dtype=np.float32)).to(
+                self.device)
+            out_slab = torch.empty((volume.shape[0], self.out_fmaps) +
+                                   tuple(b - a for a, b in zip(olo, ohi)),
+                                   dtype=torch.float32, device=self.device)
+        self.bind_slabs(slab, lo, out_slab, olo)
+
     def run(self, tiles):
-        """Run the tiles from the resident slab into the resident output slab
+        """Run the tiles from the bound input slab into the bound output slab
         (enqueued; the current stream is made to wait for all of them)."""
         torch = self.torch
-        pin = self.grid.patch_in
         with torch.cuda.device(self.device):
             cur = torch.cuda.current_stream(self.device)
             for r in self.runners:
                 r.stream.wait_stream(cur)       # slab / output slab are ready
-            B = self.batch
-            groups = [tiles[i:i + B] for i in range(0, len(tiles), B)]
-            for gi, group in enumerate(groups):
-                r = self.runners[gi % len(self.runners)]
-                xin = r._in_std[self.in_name]
-                with torch.cuda.stream(r.stream):
-                    for b in range(B):
-                        t = group[min(b, len(group) - 1)]   # a short last group repeats
-                        src = tuple(slice(a - l, a - l + p)
-                                    for a, l, p in zip(t.in_lo, self.lo, pin))
-                        xin[b:b + 1].copy_(self.slab[(slice(None), slice(None)) + src])
-                res = next(iter(r.run_on_stream({self.in_name: xin}).values()))
-                with torch.cuda.stream(r.stream):
-                    for b, t in enumerate(group):
-                        dst = tuple(slice(o - l, o - l + (e - a)) for o, l, a, e in
-                                    zip(t.out_lo, self.olo, t.keep_lo, t.keep_hi))
-                        self.out_slab[(slice(None), slice(None)) + dst].copy_(
-                            res[(slice(b, b + 1), slice(None)) + t.local_window])
+            self._enqueue(tiles, self.slab, self.lo, self.out_slab, self.olo)
             for r in self.runners:
                 cur.wait_stream(r.stream)
 
-    def download(self, out: np.ndarray, tiles):
-        """Copy the output slab into the host volume (one D2H)."""
-        _, _, olo, ohi = self.slab_bounds(tiles)
-        host = self.out_slab.cpu().numpy()
-        win = (slice(None), slice(None)) + tuple(slice(a, b) for a, b in zip(olo, ohi))
-        # tiles of one block may not tile a full box: copy only what they wrote
-        for t in tiles:
-            dst = (slice(None), slice(None)) + t.out_window
-            src = (slice(None), slice(None)) + tuple(
-                slice(o - l, o - l + (b - a))
-                for o, l, a, b in zip(t.out_lo, olo, t.keep_lo, t.keep_hi))
-            out[dst] = host[src]
-        del win
+    def _enqueue(self, tiles, slab, lo, out_slab, olo, start=0):
+        """Enqueue the tiles' batches on the runner streams (round robin from
+        runner `start`); returns the next runner index."""
+        torch = self.torch
+        pin = self.grid.patch_in
+        B = self.batch
+        # rebatched plans (volume batch 1) stack B patches along the batch
+        # axis; a plan whose own batch is > 1 runs one patch of the whole
+        # volume batch per launch (B == 1)
+        whole = self.vol_batch > 1
+        groups = [tiles[i:i + B] for i in range(0, len(tiles), B)]
+        k = start
+        for group in groups:
+            r = self.runners[k % len(self.runners)]
+            k += 1
+            xin = r._in_std[self.in_name]
+            with torch.cuda.stream(r.stream):
+                for b in range(B):
+                    t = group[min(b, len(group) - 1)]   # a short last group repeats
+                    src = tuple(slice(a - l, a - l + p) for a, l, p in zip(t.in_lo, lo, pin))
+                    dst_b = slice(None) if whole else slice(b, b + 1)
+                    xin[dst_b].copy_(slab[(slice(None), slice(None)) + src])
+            res = next(iter(r.run_on_stream({self.in_name: xin}).values()))
+            with torch.cuda.stream(r.stream):
+                for b, t in enumerate(group):
+                    dst = tuple(slice(o - l, o - l + (e - a)) for o, l, a, e in
+                                zip(t.out_lo, olo, t.keep_lo, t.keep_hi))
+                    src_b = slice(None) if whole else slice(b, b + 1)
+                    out_slab[(slice(None), slice(None)) + dst].copy_(
+                        res[(src_b, slice(None)) + t.local_window])
+        return k
+
+    # ------------------------------------------------------------ streamed
+    def _ring(self, nb, cin, in_ext, out_ext):
+        """Two input and two output row slabs on the device (flat buffers for
+        the largest row, viewed per row so every row slab is contiguous)."""
+        torch = self.torch
+        nin = nb * cin * int(np.prod(in_ext))
+        nout = nb * self.out_fmaps * int(np.prod(out_ext))
+        if self._rings is None or self._rings[0] < nin or self._rings[1] < nout:
+            with torch.cuda.device(self.device):
+                ins = [torch.empty(nin, dtype=torch.float32, device=self.device)
+                       for _ in range(2)]
+                outs = [torch.empty(nout, dtype=torch.float32, device=self.device)
+                        for _ in range(2)]
+            self._rings = (nin, nout, ins, outs)
+        return self._rings[2], self._rings[3]
+
+    def run_host(self, volume, out, tiles):
+        """Stream the tiles' input rows from host ``volume`` and their kept
+        outputs into host ``out`` (both (n, c, X, Y, Z) float32).  Returns
+        when ``out`` holds the results."""
+        from . import staging
+        torch = self.torch
+        rows = self.rows(list(tiles))
+        if not rows:
+            return
+        bounds = [self.slab_bounds(r) for r in rows]
+        in_ext = [max(b[1][d] - b[0][d] for b in bounds) for d in range(3)]
+        out_ext = [max(b[3][d] - b[2][d] for b in bounds) for d in range(3)]
+        nb, cin = int(volume.shape[0]), int(volume.shape[1])
+        ins, outs = self._ring(nb, cin, in_ext, out_ext)
+        vol_t = torch.from_numpy(volume) if staging.is_pinned(volume) else None
+        out_t = torch.from_numpy(out) if staging.is_pinned(out) else None
+        if getattr(self, "_stager", None) is None:
+            self._stager = staging.RowStager()     # pinned slots, reused across calls
+        stager = self._stager
+        ev_in = [None, None]        # input slot free: its row's compute is done
+        ev_out = [None, None]       # output slot free: its row's download is done
+        k = 0
+
+        def full_yz(lo, hi, shape):
+            return lo[1] == 0 and lo[2] == 0 and hi[1] == shape[3] and hi[2] == shape[4]
+
+        with torch.cuda.device(self.device):
+            cur = torch.cuda.current_stream(self.device)
+            self.copy_in.wait_stream(cur)
+            self.copy_out.wait_stream(cur)
+            for ri, (row, (lo, hi, olo, ohi)) in enumerate(zip(rows, bounds)):
+                slot = ri % 2
+                ishape = (nb, cin) + tuple(b - a for a, b in zip(lo, hi))
+                oshape = (nb, self.out_fmaps) + tuple(b - a for a, b in zip(olo, ohi))
+                xin = ins[slot][:int(np.prod(ishape))].view(ishape)
+                yout = outs[slot][:int(np.prod(oshape))].view(oshape)
+                win = (slice(None), slice(None)) + tuple(slice(a, b) for a, b in zip(lo, hi))
+                owin = (slice(None), slice(None)) + tuple(slice(a, b) for a, b in zip(olo, ohi))
+                # ---- upload row ri once row ri-2's compute released the slot
+                if ev_in[slot] is not None:
+                    self.copy_in.wait_event(ev_in[slot])
+                if vol_t is not None and full_yz(lo, hi, volume.shape):
+                    with torch.cuda.stream(self.copy_in):
+                        for b in range(nb):
+                            for c in range(cin):   # contiguous x-range of one fmap
+                                xin[b, c].copy_(vol_t[b, c, lo[0]:hi[0]], non_blocking=True)
+                else:
+                    stager.upload(slot, volume[win], xin, self.copy_in)
+                up = torch.cuda.Event()
+                up.record(self.copy_in)
+                # ---- compute (after the upload, and once row ri-2's output
+                # left this slot)
+                for r in self.runners:
+                    r.stream.wait_event(up)
+                    if ev_out[slot] is not None:
+                        r.stream.wait_event(ev_out[slot])
+                k = self._enqueue(row, xin, lo, yout, olo, start=k)
+                done = []
+                for r in self.runners:
+                    e = torch.cuda.Event()
+                    e.record(r.stream)
+                    done.append(e)
+                # ---- download the row's kept output
+                for e in done:
+                    self.copy_out.wait_event(e)
+                freed = torch.cuda.Event()
+                freed.record(self.copy_out)
+                ev_in[slot] = freed
+                if out_t is not None and full_yz(olo, ohi, out.shape):
+                    with torch.cuda.stream(self.copy_out):
+                        for b in range(nb):
+                            for c in range(self.out_fmaps):
+                                out_t[b, c, olo[0]:ohi[0]].copy_(yout[b, c], non_blocking=True)
+                else:
+                    stager.download(slot, yout, out[owin], self.copy_out)
+                fin = torch.cuda.Event()
+                fin.record(self.copy_out)
+                ev_out[slot] = fin
+            for r in self.runners:
+                cur.wait_stream(r.stream)
+            cur.wait_stream(self.copy_out)
+        self.copy_out.synchronize()
+        stager.finish()
+
+
+_TILER_CACHE: dict = {}
+_TILER_LOCK = threading.Lock()
+
+
+def device_tiler(plan, grid: TileGrid, device, backend=None) -> DeviceTiler:
+    """A cached DeviceTiler per (plan, grid, device, backend, batching knobs):
+    repeated run_tiled calls reuse bound runners and captured graphs."""
+    key = (id(plan), grid.patch_in, grid.volume_in, grid.overlap, str(device), repr(backend),
+           os.environ.get("VOXPLAN_PATCH_BATCH", "4"), os.environ.get("VOXPLAN_STREAMS", "2"))
+    with _TILER_LOCK:
+        hit = _TILER_CACHE.get(key)
+        if hit is not None and hit[0] is plan:
+            return hit[1]
+    dt = DeviceTiler(plan, grid, device, backend)
+    with _TILER_LOCK:
+        if len(_TILER_CACHE) >= 8:
+            _TILER_CACHE.pop(next(iter(_TILER_CACHE)))
+        _TILER_CACHE[key] = (plan, dt)
+    return dt
 
 
 def run_tiled(plan, volume, *, overlap=None, backend=None, workers=None, grid=None,
-              devices=None) -> np.ndarray:
+              devices=None, out=None) -> np.ndarray:
     """Run ``plan`` patchwise over a (batch, fmap, x, y, z) volume (tiling.py:189-237).
 
     ``devices``: list of CUDA devices (default: ``workers`` devices, default 1,
     capped by ``VOXPLAN_WORKERS`` and the visible GPU count).  Each device gets
-    a contiguous block of tiles and one host thread.
+    a contiguous block of tiles and one host thread, and streams its input
+    rows in and its output rows out (DeviceTiler.run_host).  ``out``: an
+    optional preallocated (e.g. page-locked) result array.
     """
     import torch
     volume = np.asarray(volume)
@@ -271,7 +430,13 @@ def run_tiled(plan, volume, *, overlap=None, backend=None, workers=None, grid=No
         ndev = min(worker_count(workers), max(1, torch.cuda.device_count()))
         devices = ["cuda:%d" % i for i in range(ndev)]
     devices = list(devices)[:len(grid.tiles)]
-    out = np.empty(tuple(out_dims[:2]) + tuple(grid.volume_out), dtype=np.float32)
+    shape = tuple(out_dims[:2]) + tuple(grid.volume_out)
+    if out is None:
+        out = np.empty(shape, dtype=np.float32)
+    elif tuple(out.shape) != shape or out.dtype != np.float32:
+        raise ExecutionError("out must be a float32 array of shape %s" % (shape,))
+    if volume.dtype != np.float32:
+        volume = volume.astype(np.float32)
     blocks = [[grid.tiles[i] for i in partition(len(grid.tiles), len(devices), r)]
               for r in range(len(devices))]
     errors = []
@@ -280,11 +445,8 @@ def run_tiled(plan, volume, *, overlap=None, backend=None, workers=None, grid=No
         try:
             if not blocks[r]:
                 return
-            dt = DeviceTiler(plan, grid, devices[r], backend)
-            dt.upload(volume, blocks[r])
-            dt.run(blocks[r])
-            torch.cuda.synchronize(dt.device)
-            dt.download(out, blocks[r])
+            dt = device_tiler(plan, grid, devices[r], backend)
+            dt.run_host(volume, out, blocks[r])
         except Exception as exc:  # surfaced below
             errors.append(exc)
 

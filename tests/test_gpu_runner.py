@@ -61,8 +61,13 @@ def _small(cfg):
             5: lambda: C.config5(patch=(6, 48, 48), feats=(8, 12, 16, 20))}[cfg]()
 
 
+# b200-x3 vs ref_run: ~3x the split-storage emulation of each small config
+# (run_plan(storage="split"): cfg1 6.6e-6, cfg3 6.9e-6, cfg4 3.0e-5, cfg5 6.5e-4)
+X3_NET_TOL = {1: 3e-5, 3: 3e-5, 4: 1e-4, 5: 2e-3}
+
+
 @pytest.mark.parametrize("cfg", [1, 3, 4, 5])
-@pytest.mark.parametrize("backend", ["b200", "b200-fp32"])
+@pytest.mark.parametrize("backend", ["b200", "b200-x3", "b200-fp32"])
 def test_config_networks(cfg, backend):
     spec, store = _small(cfg)
     plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
@@ -75,6 +80,8 @@ def test_config_networks(cfg, backend):
     if backend == "b200-fp32":
         # fp32 rounding differences are amplified by config 5's deep chain too
         assert mx < {5: 2e-4}.get(cfg, 2e-5), mx
+    elif backend == "b200-x3":
+        assert mx < X3_NET_TOL[cfg], mx
     else:
         emu = R.run_plan(plan, x, storage="bf16")[name]
         emx, el2 = R.normalized_error(got, emu)
