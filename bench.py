@@ -1,27 +1,34 @@
 #!/usr/bin/env python
-"""Benchmark: B200 fused conv3d inference vs the reference CPU engine.
+"""Benchmark: B200 fused conv3d U-net inference vs the reference CPU engine.
 
 Contract (one JSON line on rank 0):
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl b200|reference]
 
-Workloads (BASELINE.json configs; synthetic seeded inputs):
-  --config 2 (default, BASELINE configs[1]): the featuremap sweep — conv
-      C->C (C in 8..128) with kernels 3x3x3 and 1x3x3, 'same' padding, fused
-      bias + ELU, on 1xCx32x128x128 fp32 inputs.  One step = all 10 layers,
-      each through its PlanRunner (fp32 NCDHW in HBM -> bf16 blocked ->
-      tcgen05 conv -> fp32 NCDHW out).  Unit: output voxels/s.
-  --config 1, 3, 4: the single layer, residual block and Cicek U-net.
-  --config 5: the anisotropic residual U-net over the 128x1024x1024 volume,
-      288 patches of 18x192x192 split across ranks (strong scaling).
+Headline (default, --config 5): BASELINE configs[4], the anisotropic
+residual U-net over the synthetic 128x1024x1024 volume, tiled into the
+reference's (8, 6, 6) grid of 18x192x192 patches (overlap 0).  One step =
+the whole volume.  ``value`` = output voxels/s with the volume resident in
+HBM (device-timed, max over ranks); ``e2e`` = the same through the public
+``run_tiled`` with the host volume in page-locked memory and the result read
+back into a page-locked host volume (row-streamed H2D / D2H inside the timed
+region).  Under torchrun (N > 1) ranks take contiguous blocks of tiles
+(strong scaling, no collective on the data path) and rank 0 gathers the
+output volume over NCCL afterwards (timed separately: ``gather_ms``).
+``bench.py --gpus N`` without torchrun re-launches itself under torchrun.
 
-Timing: W warm-up steps, then K steps bracketed by barrier + synchronize,
-CUDA events on the runner streams, max over ranks.  The L2 (126 MB) is
-flushed with a 512 MB write between steps, outside the timed windows.
-``e2e`` repeats the metric through the public host API (PlanRunner.run with
-host fp32 arrays: pinned H2D + graph + D2H inside the timed region).
-``roofline`` is the dominant conv kernel alone (CUDA graph of that launch),
-``cpu_baseline`` the reference's own compiled kernel (oracle/_ref) on the
-host cores on a bounded sample.
+At N = 1 the line also carries ``configs``: configs 1-4 (single fused
+layer, featuremap sweep, residual block, Cicek U-net), each with its own
+value, roofline, e2e and cpu_baseline, and ``x3``: config 5 on the
+fp32-grade split-bf16 backend.
+
+Timing rules: W >= 3 warm-up steps; the L2 (126 MB) is flushed with a 512 MB
+write before every timed step, outside the timed window; CUDA events on the
+launching streams; nvidia-smi clocks sampled during the timed region.
+``roofline`` = the dominant conv kernel, timed live by external CUDA events
+captured around its launch in the runner's graph (every timed step).
+``cpu_baseline`` / ``--impl reference`` = the reference engine itself
+(oracle/_ref: voxplan.run_tiled / PlanRunner(backend="compiled")) on the
+host cores, on a bounded sample.
 """
 
 from __future__ import annotations
@@ -29,6 +36,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -41,19 +49,24 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "output voxels/sec for 3D U-net inference; conv3d TFLOP/s vs tensor-core peak"
+DATA = ("synthetic: seeded U[0,1) / U[-1,1) volumes (BASELINE.json shapes and "
+        "distributions), He-normal weights, BN statistics calibrated (config 5)")
 
 
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--backend", default="b200", choices=["b200", "b200-x3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=20.0,
-                    help="target CPU-baseline sample duration")
+    ap.add_argument("--no-subconfigs", action="store_true",
+                    help="config 5 only (skip the configs 1-4 sub-lines and x3)")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="target CPU-baseline sample duration per config")
     return ap.parse_args()
 
 
@@ -69,36 +82,11 @@ def load_peaks():
                 "source": "fallback (B200_PROFILING.md)"}
 
 
-# ------------------------------------------------------------------ workloads
-
-def build_workload(cfg):
-    """[(name, spec, store, flops)] for a config."""
-    from paper_1903_07525_b200 import configs as C
-    if cfg == 2:
-        out = []
-        for k in C.SWEEP_K:
-            for c in C.SWEEP_C:
-                spec, store = C.config2(c, k)
-                out.append(("c%d_k%s" % (c, "".join(map(str, k))), spec, store))
-    elif cfg == 1:
-        out = [("cfg1",) + C.config1()]
-    elif cfg == 3:
-        out = [("cfg3",) + C.config3()]
-    elif cfg == 4:
-        out = [("cfg4",) + C.config4()]
-    else:
-        out = [("cfg5",) + C.config5()]
-    return [(n, s, st, C.conv_flops(s)) for n, s, st in out]
-
-
-def output_voxels(spec):
-    from paper_1903_07525_b200.shapes import validate_shapes
-    shapes = validate_shapes(spec)
-    total = 0
-    for blob in spec.output_blobs():
-        n, _, x, y, z = shapes[blob]
-        total += n * x * y * z
-    return total
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
 
 # ------------------------------------------------------------------ clocks
@@ -119,7 +107,6 @@ class ClockSampler:
                 self.lines.append(line)
 
     def __enter__(self):
-        import threading
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
@@ -130,18 +117,14 @@ class ClockSampler:
             return self
         self.thread = threading.Thread(target=self._reader, daemon=True)
         self.thread.start()
-        # nvidia-smi takes a few hundred ms to start: only open the timed
-        # region once it is sampling
         t0 = time.time()
         while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
             time.sleep(0.01)
-        self.skip = len(self.lines)          # samples taken before the timed region
+        self.skip = len(self.lines)
         return self
 
     def __exit__(self, *a):
         if self.proc is not None:
-            # a timed region shorter than the 20 ms sampling period would get
-            # no sample: wait (<= 100 ms) for one taken at its end
             t0 = time.time()
             while len(self.lines) <= self.skip and time.time() - t0 < 0.1:
                 time.sleep(0.005)
@@ -156,8 +139,8 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in self.lines:
-            parts = [p.strip() for p in l.split(",")]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
             if len(parts) < 8:
                 continue
             try:
@@ -172,237 +155,64 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ------------------------------------------------------------------ B200 arm
+# ------------------------------------------------------------------ algorithmic work
 
-def run_b200(args, rank, world, local_rank):
-    import torch
-    import paper_1903_07525_b200 as P
-    from paper_1903_07525_b200 import configs as C, ops as K
-    dev = torch.device("cuda", local_rank)
-    torch.cuda.set_device(dev)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-    peaks = load_peaks()
-    lo, hi = C.input_range(args.config)
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-
-    def barrier():
-        torch.cuda.synchronize(dev)
-        if dist is not None:
-            dist.barrier()
-
-    if args.config == 5:
-        return run_tiled_volume(args, rank, world, dev, dist, peaks, flush)
-
-    work = build_workload(args.config)
-    layers = []
-    for name, spec, store, flops in work:
-        plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
-        runner = P.PlanRunner(plan, backend="b200", device=dev)
-        x = C.make_input(spec, seed=100 + rank, low=lo, high=hi)
-        # inputs resident in HBM: written once into the runner's static input
-        # buffer (the tensor its CUDA graph reads), so run_device copies nothing
-        xd = runner.input_buffers()
-        xd[plan.inputs[0][0]].copy_(torch.from_numpy(x))
-        layers.append({"name": name, "plan": plan, "runner": runner, "x": x, "xd": xd,
-                       "flops": flops, "vox": output_voxels(spec)})
-
-    # The step: every layer's network once, as one CUDA graph (PlanBatch):
-    # each network's fp32 -> bf16 input pack runs beside the previous
-    # network's conv (independent launch), each conv waits for its own pack.
-    # the dominant network (most conv FLOPs) is timed live inside every
-    # timed replay (external events around its body in the graph)
-    dom = max(range(len(layers)), key=lambda i: layers[i]["flops"])
-    batch = P.PlanBatch([L["runner"] for L in layers])
-    # the same batch with timing events around the dominant network's body
-    # (its conv): replayed after the timed steps, since the two event nodes
-    # cost the step ~20 us (they cut the conv's programmatic-launch overlap)
-    pbatch = P.PlanBatch([L["runner"] for L in layers], probe=dom)
-
-    def batch_step():
-        """One timed window around the whole sweep on the batch stream (a
-        short device-side spin first, so the window holds GPU time only)."""
-        cs = torch.cuda.current_stream(dev)
-        torch.cuda._sleep(200_000)
-        batch.stream.wait_stream(cs)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(batch.stream)
-        batch.replay()
-        e1.record(batch.stream)
-        cs.wait_stream(batch.stream)
-        return e0, e1
-
-    def step(timed):
-        """Per-layer breakdown (not the headline): one network at a time,
-        each in its own window; returns per-layer event pairs."""
-        evs = []
-        torch.cuda._sleep(200_000)
-        for L in layers:
-            s = L["runner"].stream
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            # start only once the previous layer (ordered via the current
-            # stream) has finished, so the windows do not overlap
-            s.wait_stream(torch.cuda.current_stream(dev))
-            e0.record(s)
-            L["runner"].run_device(L["xd"])
-            e1.record(s)
-            evs.append((e0, e1))
-        return evs
-
-    for _ in range(max(3, args.warmup)):
-        batch_step()
-        step(False)
-    barrier()
-    total_ms = 0.0
-    live_ms = 0.0
-    with ClockSampler(local_rank) as clk:
-        for _ in range(args.steps):
-            flush.fill_(1.0)            # L2 flush, outside the timed window
-            barrier()
-            a, b = batch_step()
-            torch.cuda.synchronize(dev)
-            total_ms += a.elapsed_time(b)
-    barrier()
-    probe_steps = max(3, min(args.steps, 20))
-    for i in range(probe_steps + 2):
-        flush.fill_(1.0)
-        torch.cuda.synchronize(dev)
-        pbatch.run_device()
-        torch.cuda.synchronize(dev)
-        if i >= 2:
-            live_ms += pbatch.probe_ms()
-    live_ms = live_ms / probe_steps * args.steps
-    per_layer_ms = [0.0] * len(layers)
-    layer_steps = max(3, min(args.steps, 10))
-    for _ in range(layer_steps):
-        flush.fill_(1.0)
-        evs = step(True)
-        torch.cuda.synchronize(dev)
-        for i, (a, b) in enumerate(evs):
-            per_layer_ms[i] += a.elapsed_time(b) * args.steps / layer_steps
-    if dist is not None:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = t.item()
-    vox_step = sum(L["vox"] for L in layers)
-    ms_per_step = total_ms / args.steps
-    value = vox_step * world / (ms_per_step * 1e-3)
-
-    # ---- dominant kernel: timed live in the step (above) and alone
-    rd = layers[dom]["runner"]
-    single = len(rd._calls) - rd._n_in_calls == 1   # body = the conv alone (config 2)
-    roof = kernel_roofline(layers[dom], dev, peaks,
-                           live_ms=live_ms / args.steps if single else None)
-
-    result = {
-        "metric": METRIC, "value": value, "unit": "output voxels/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (seeded uniform inputs, He-normal weights, BASELINE.json shapes)",
-        "config": {"workload": workload_name(args.config),
-                   "layers": [L["name"] for L in layers],
-                   "output_voxels_per_step": vox_step,
-                   "parallelism": "replicas" if world > 1 else "single",
-                   "l2": "flushed (512 MB write) between steps, outside timed region"},
-        "tflops": sum(L["flops"] for L in layers) * world / (ms_per_step * 1e-3) / 1e12,
-        "layers_note": "per network run alone (sequential windows, %d passes); the step "
-                       "runs them as one graph with input packs overlapping the previous "
-                       "network's conv" % layer_steps,
-        "layers": {L["name"]: {"ms": per_layer_ms[i] / args.steps,
-                               "tflops": L["flops"] / (per_layer_ms[i] / args.steps * 1e-3) / 1e12}
-                   for i, L in enumerate(layers)},
-        "roofline": roof,
-        "gpu_launches": sum(L["runner"].launches for L in layers) * args.steps,
-        "clocks": clk.summary(),
-    }
-    if not args.no_e2e:
-        result["e2e"] = e2e_layers(layers, args, dev, dist, world)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(args, work, target_s=args.cpu_seconds)
-    return result
-
-
-def workload_name(cfg):
-    return {1: "config1: conv3d 3x3x3 C16->16 + bias + ReLU, 1x16x32x64x64",
-            2: "config2: featuremap sweep C in {8..128} x k in {3x3x3, 1x3x3}, conv + bias + "
-               "ELU on 1xCx32x128x128 (BASELINE configs[1])",
-            3: "config3: residual block C64 on 1x64x24x128x128",
-            4: "config4: Cicek 3D U-net 132^3 -> 3x44^3",
-            5: "config5: anisotropic residual U-net, 128x1024x1024 volume, 18x192x192 patches"}[cfg]
-
-
-def kernel_roofline(L, dev, peaks, live_ms=None):
-    """Roofline of the dominant conv kernel.  ``live_ms``: its duration inside
-    the timed steps (external events around it in the step's graph, L2
-    flushed before each step) - the figure `achieved` is computed from.  It is
-    also timed alone (its launch replayed from a CUDA graph 20 times between
-    events on the graph's stream) for reference."""
-    import torch
-    from paper_1903_07525_b200.netspec import LayerKind
+def op_work(plan, storage_bytes=2):
+    """Per plan step: (name, kind, flops, bytes) at the plan's batch.
+    FLOPs = 2 x MACs of the reference arithmetic; bytes = the step's input
+    and output tensors (and residual operand) once each at the storage
+    width (no halo re-reads, no padding lanes); a network output
+    is written as fp32 by the producing conv's epilogue (4 B)."""
     from paper_1903_07525_b200.formats import ROLE_KERNEL
-    runner = L["runner"]
-    plan = L["plan"]
-    # the network's largest conv (by FLOPs): its own algorithmic FLOPs and
-    # bytes (bf16 blocked input, output bf16 or the fused fp32 network output,
-    # residual operand if any; weights negligible)
-    out_vals = {id(v): name for name, v in runner._out_values.items()}
-    best = None
-    for c, (kind, st, info) in zip(runner.op_calls, runner._ops):
-        if kind is not LayerKind.CONVOLUTION:
-            continue
-        kshape = plan.weights.tensor(st.name, ROLE_KERNEL).shape
-        n, cout, ox, oy, oz = st.output.dims
-        f = 2.0 * float(np.prod(kshape)) * n * ox * oy * oz
-        # input tensors read (a fused concat reads both segments)
-        ins = list(info["segments"][:2]) if "segments" in info else [info["x"]]
-        in_b = 2.0 * sum(v.dims[1] * float(np.prod(v.dims[2:])) * v.dims[0] for v in ins)
-        fused = out_vals.get(id(info["out"])) in runner._fused_outputs
-        out_b = (4.0 if fused else 2.0) * cout * n * ox * oy * oz
-        base_b = 2.0 * cout * n * ox * oy * oz if st.additive else 0.0
-        if best is None or f > best[1]:
-            best = (c, f, in_b + out_b + base_b, st.name)
-    call, flops, alg_bytes, conv_name = best
-    s = torch.cuda.Stream(device=dev)
-    with torch.cuda.stream(s):
-        call()
-    s.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=s):
-        call()
-    reps = 20
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(s):
-        for _ in range(3):
-            g.replay()
-        torch.cuda._sleep(200_000)
-        e0.record(s)
-        for _ in range(reps):
-            g.replay()
-        e1.record(s)
-    s.synchronize()
-    alone_ms = e0.elapsed_time(e1) / reps
-    ms = live_ms if live_ms else alone_ms
-    ai = flops / alg_bytes
-    ridge = peaks["bf16"] * 1e12 / (peaks["hbm"] * 1e9)
-    if ai >= ridge:
-        achieved = flops / (ms * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16"],
-                "unit": "TFLOP/s", "frac": achieved / peaks["bf16"]}
-    else:
-        achieved = alg_bytes / (ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm"]}
-    label = L["name"] if conv_name == "conv" or len(runner._ops) <= 2 else \
-        "%s/%s" % (L["name"], conv_name)
-    roof.update({"kernel": "conv3d_tc_kernel (%s)" % label, "ms_per_launch": ms,
-                 "timing": ("in-step: events around it in replays of the step's graph "
-                            "(L2 flushed before each)") if live_ms else "alone, 20 graph replays",
-                 "alone_ms_per_launch": alone_ms,
-                 "alg_flops": flops, "alg_bytes": alg_bytes, "peak_source": peaks["source"],
-                 "traffic": ncu_traffic(L["name"])})
-    return roof
+    from paper_1903_07525_b200.netspec import LayerKind
+    out_bids = {bid for _, bid, _ in plan.outputs}
+    out = []
+    for st in plan.steps:
+        if st.kind is LayerKind.PAD:
+            continue                  # virtual on the device (TMA zero fill)
+        d_out = tuple(st.output.dims)
+        n, co = d_out[0], d_out[1]
+        vox_out = int(np.prod(d_out[2:]))
+        ins = [tuple(si.dims) for si in st.inputs]
+        in_elems = sum(d[0] * d[1] * int(np.prod(d[2:])) for d in ins)
+        if st.kind is LayerKind.CONVOLUTION:
+            k = plan.weights.tensor(st.name, ROLE_KERNEL).shape
+            f = 2.0 * float(np.prod(k)) * n * vox_out
+        elif st.kind is LayerKind.DECONVOLUTION:
+            k = plan.weights.tensor(st.name, ROLE_KERNEL).shape
+            vin = int(np.prod(ins[0][2:]))
+            f = 2.0 * float(np.prod(k)) * n * vin
+        else:
+            f = 0.0
+        out_b = 4 if (st.output.buffer in out_bids and st.kind in (
+            LayerKind.CONVOLUTION, LayerKind.DECONVOLUTION)) else storage_bytes
+        b = storage_bytes * in_elems + out_b * n * co * vox_out
+        if st.additive and st.base is not None:
+            b += storage_bytes * n * co * vox_out
+        out.append((st.name, st.kind, f, float(b)))
+    return out
+
+
+def roof_of(flops, nbytes, ms, peaks, peak_key):
+    """Roofline dict for one kernel: tensor-bound when its arithmetic
+    intensity is past the ridge of the chosen peak."""
+    peak_tc = peaks[peak_key]
+    ridge = peak_tc * 1e12 / (peaks["hbm"] * 1e9)
+    if flops / max(nbytes, 1.0) >= ridge:
+        ach = flops / (ms * 1e-3) / 1e12
+        return {"bound": "tensor", "achieved": ach, "peak": peak_tc, "unit": "TFLOP/s",
+                "frac": ach / peak_tc}
+    ach = nbytes / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s",
+            "frac": ach / peaks["hbm"]}
+
+
+def network_roofline(work, ms, peaks, peak_key, repeat=1):
+    """sum_l max(F_l / P, B_l / BW) / T (SURVEY §8d per-network roofline)."""
+    t = sum(max(f / (peaks[peak_key] * 1e12), b / (peaks["hbm"] * 1e9)) for _, _, f, b in work)
+    t *= repeat
+    return {"frac": t / (ms * 1e-3), "roofline_ms": t * 1e3,
+            "peak_tflops": peaks[peak_key], "peak_hbm_gbs": peaks["hbm"]}
 
 
 def ncu_traffic(name):
@@ -414,71 +224,60 @@ def ncu_traffic(name):
         return None
 
 
-def e2e_layers(layers, args, dev, dist, world):
-    """Same metric through the public host API (PlanRunner.run on host arrays).
-    The step's inputs sit in page-locked host memory and results land in
-    page-locked arrays (staging.pinned_empty), so each call is one H2D DMA,
-    the graph replay and one D2H DMA."""
-    import torch
-    from paper_1903_07525_b200 import staging
-    for L in layers:
-        xp = staging.pinned_empty(L["x"].shape)
-        xp[...] = L["x"]
-        L["xp"] = xp
-        L["outp"] = {n: staging.pinned_empty(t.shape) for n, t in L["runner"]._out_std.items()}
-        L["runner"].run(L["xp"], out=L["outp"])
-    torch.cuda.synchronize(dev)
-    if dist is not None:
-        dist.barrier()
-    steps = max(1, min(args.steps, 5))
-    t0 = time.perf_counter()
-    pend = []
-    for _ in range(steps):
-        # every layer's volume is in flight at once: its upload overlaps the
-        # other layers' compute and downloads (PlanRunner.run_async); runs on
-        # one runner are ordered by its stream
-        pend += [L["runner"].run_async(L["xp"], out=L["outp"]) for L in layers]
-    for h in pend:
-        h.wait()
-    torch.cuda.synchronize(dev)
-    el = time.perf_counter() - t0
-    if dist is not None:
-        t = torch.tensor([el], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        el = t.item()
-    vox = sum(L["vox"] for L in layers)
-    return {"value": vox * world * steps / el, "unit": "output voxels/s",
-            "h2d_bytes_per_step": sum(L["runner"].h2d_bytes for L in layers),
-            "d2h_bytes_per_step": sum(L["runner"].d2h_bytes for L in layers),
-            "steps": steps, "timer": "host wall clock around PlanRunner.run_async + wait for every layer "
-                                     "(H2D from pinned host input, graph replay, D2H into "
-                                     "pinned host output; layers pipelined across streams)"}
+# ------------------------------------------------------------------ reference CPU arm
+
+def ref_volume_sample(spec, store, threads):
+    """The reference engine on `threads` config-5 tiles: voxplan.run_tiled
+    (tiling.py:189-237, backend "compiled", workers = threads) over a
+    (1, 1, 18, 192, 192 * threads) slice of the synthetic volume (overlap 0:
+    exactly `threads` disjoint 18x192x192 tiles, each costing what a tile of
+    the full 288-tile grid costs).  Returns (run, voxels per run, tiles)."""
+    from oracle import ref_voxplan as RV
+    plan = RV.compile_reference(spec, store)
+    patch = spec.input_layers()[0].params["shape"][2:]
+    vol = np.random.default_rng(77).uniform(
+        0, 1, (1, 1, patch[0], patch[1], patch[2] * threads)).astype(np.float32)
+
+    def run():
+        RV.run_tiled(plan, vol, workers=threads)
+    return run, threads * int(np.prod(patch)), threads
 
 
-# ------------------------------------------------------------------ CPU baseline
+def ref_network_sample(spec, store, x, threads):
+    """The reference engine's PlanRunner(plan, "compiled") (executor.py:51-198)
+    on `threads` independent copies of the volume, one runner per host
+    thread (the reference's only parallelism: independent volumes/patches per
+    worker, tiling.py:211-225).  Returns (run, output voxels per run)."""
+    import psutil
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import ref_voxplan as RV
+    V = RV.voxplan()
+    plan = RV.compile_reference(spec, store)
+    arena = plan.arena_bytes
+    avail = psutil.virtual_memory().available
+    n = max(1, min(threads, int(avail * 0.5 // max(arena, 1))))
+    runners = [V.PlanRunner(plan, backend="compiled") for _ in range(n)]
+    pool = ThreadPoolExecutor(max_workers=n)
+    from bench_util import output_voxels
+    vox = output_voxels(spec)
 
-def cpu_threads():
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
+    def run():
+        list(pool.map(lambda r: r.run(x), runners))
+    return run, vox * n, n
 
 
-def reference_sample_runner(work, threads, target_s):
-    """Bind the reference's compiled kernel for every layer; pick an x-slab
-    sample per layer so one pass takes about target_s seconds."""
+def ref_sweep_sample(work, threads, target_s):
+    """Config 2: the reference's compiled _kernels.conv3d (oracle/_ref) on
+    x-slabs of each layer across the host threads (round-1 arm)."""
+    from concurrent.futures import ThreadPoolExecutor
     from oracle import ref_engine as E
-    from oracle import ref_numpy as R
     from paper_1903_07525_b200.formats import ROLE_BIAS, ROLE_KERNEL
     if not E.available():
         return None
     items = []
-    for name, spec, store, flops in work:
-        conv = [l for l in spec.layers if l.kind.value == "Convolution"]
-        if len(conv) != 1:
-            return None       # multi-layer nets: see DESIGN.md (config 2 is the bench line)
-        lay = conv[0]
-        act = [l for l in spec.layers if l.kind.value in ("ReLU", "ELU", "Sigmoid")]
+    for name, spec, store, _ in work:
+        lay = [layer for layer in spec.layers if layer.kind.value == "Convolution"][0]
+        act = [layer for layer in spec.layers if layer.kind.value in ("ReLU", "ELU", "Sigmoid")]
         kind = act[0].kind.value.lower() if act else None
         stp = E.ConvStep(store.tensor(lay.name, ROLE_KERNEL), store.tensor(lay.name, ROLE_BIAS),
                          pad=lay.params["pad"], act=kind)
@@ -487,9 +286,8 @@ def reference_sample_runner(work, threads, target_s):
         xb = stp.prepare(x)
         ox = shape[2]
         out = np.zeros((1, -(-stp.fo // 8), ox) + tuple(shape[3:]) + (8,), np.float32)
-        items.append({"name": name, "step": stp, "xb": xb, "out": out, "ox": ox,
-                      "vox_per_row": int(np.prod(shape[3:])), "flops": flops})
-    # calibrate rows per layer on one row of each
+        items.append({"step": stp, "xb": xb, "out": out, "ox": ox,
+                      "vox_per_row": int(np.prod(shape[3:]))})
     t0 = time.perf_counter()
     for it in items:
         it["step"].run_blocked(it["xb"], it["out"], None, (0, 1))
@@ -497,135 +295,167 @@ def reference_sample_runner(work, threads, target_s):
     rows = max(1, min(items[0]["ox"], int(target_s * threads / max(one_row_all, 1e-6))))
     rows = max(threads, (rows // threads) * threads) if rows >= threads else rows
     rows = min(rows, items[0]["ox"])
-    from concurrent.futures import ThreadPoolExecutor
     pool = ThreadPoolExecutor(max_workers=threads)
 
-    def one_pass():
-        vox = 0
+    def run():
         for it in items:
             cuts = np.linspace(0, rows, min(threads, rows) + 1).astype(int)
             list(pool.map(lambda i: it["step"].run_blocked(it["xb"], it["out"], None,
                                                           (cuts[i], cuts[i + 1])),
                           range(len(cuts) - 1)))
-            vox += rows * it["vox_per_row"]
-        return vox
-
-    return one_pass, rows
+    return run, rows * sum(it["vox_per_row"] for it in items), rows
 
 
-def cpu_baseline(args, work, target_s):
-    threads = cpu_threads()
-    r = reference_sample_runner(work, threads, target_s)
-    if r is None:
-        return {"value": None, "unit": "output voxels/s", "cores": threads, "kind": "reference",
-                "sample": "unavailable (oracle/_ref not built or multi-layer config)"}
-    one_pass, rows = r
-    # whole passes until the sample holds at least ~min(10 s, target) of CPU work
+def timed_passes(run, min_s, max_passes=100):
     t0 = time.perf_counter()
-    vox, passes = 0, 0
+    n = 0
     while True:
-        vox += one_pass()
-        passes += 1
+        run()
+        n += 1
         el = time.perf_counter() - t0
-        if el >= min(10.0, target_s) or passes >= 100:
-            break
-    return {"value": vox / el, "unit": "output voxels/s", "cores": threads, "kind": "reference",
-            "sample": "%d pass(es) over %d of 32 x-rows of every config-2 layer (%d output "
-                      "voxels), reference _kernels.conv3d from oracle/_ref, x-slabs on %d "
-                      "threads, %.1f s" % (passes, rows, vox, threads, el)}
+        if el >= min_s or n >= max_passes:
+            return n, el
+
+
+def cpu_baseline(cfg, nets, target_s):
+    """The reference engine on this box's host cores, bounded sample."""
+    threads = cpu_threads()
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    try:
+        if cfg == 5:
+            spec, store = nets[0][1], nets[0][2]
+            run, vox, tiles = ref_volume_sample(spec, store, threads)
+            passes, el = timed_passes(run, min(target_s, 1.0))
+            return {"value": vox * passes / el, "unit": "output voxels/s", "cores": threads,
+                    "kind": "reference",
+                    "sample": "%d pass(es) of %d config-5 tiles through voxplan.run_tiled("
+                              "backend='compiled', workers=%d) (oracle/_ref), %.1f s; the "
+                              "288-tile volume rate is the same per tile" %
+                              (passes, tiles, threads, el)}
+        if cfg == 2:
+            r = ref_sweep_sample(nets, threads, target_s)
+            if r is None:
+                raise RuntimeError("oracle/_ref not built")
+            run, vox, rows = r
+            passes, el = timed_passes(run, min(target_s, 10.0))
+            return {"value": vox * passes / el, "unit": "output voxels/s", "cores": threads,
+                    "kind": "reference",
+                    "sample": "%d pass(es) over %d of 32 x-rows of every config-2 layer, the "
+                              "reference's _kernels.conv3d (oracle/_ref) on x-slabs, %d threads, "
+                              "%.1f s" % (passes, rows, threads, el)}
+        name, spec, store, x = nets[0]
+        run, vox, n = ref_network_sample(spec, store, x, threads)
+        passes, el = timed_passes(run, min(target_s, 3.0))
+        return {"value": vox * passes / el, "unit": "output voxels/s", "cores": n,
+                "kind": "reference",
+                "sample": "%d pass(es) of %d concurrent volumes, one voxplan.PlanRunner(plan, "
+                          "'compiled') per thread (oracle/_ref), %.1f s" % (passes, n, el)}
+    except Exception as exc:  # the baseline is reported, not required
+        return {"value": None, "unit": "output voxels/s", "cores": threads, "kind": "reference",
+                "sample": "unavailable: %s" % exc}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's own CPU implementation on the host cores."""
+    """--impl reference: the reference's own CPU engine on the host cores,
+    on the same config / metric; each step a bounded sample."""
     if world > 1 and rank != 0:
         return None
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     threads = cpu_threads()
-    work = build_workload(args.config)
-    r = reference_sample_runner(work, threads, target_s=min(8.0, args.cpu_seconds))
-    if r is None:
-        return {"impl": "reference", "metric": METRIC,
-                "unavailable": "reference CPU arm implemented for configs 1-2 (oracle/_ref)"}
-    one_pass, rows = r
+    from bench_util import build_nets, workload_name
+    nets = build_nets(args.config)
+    if args.config == 5:
+        run, vox, tiles = ref_volume_sample(nets[0][1], nets[0][2], threads)
+        sample = ("%d tiles per step (one per worker) through voxplan.run_tiled(backend="
+                  "'compiled', workers=%d), oracle/_ref" % (tiles, threads))
+    elif args.config == 2:
+        r = ref_sweep_sample(nets, threads, min(8.0, args.cpu_seconds))
+        if r is None:
+            return {"impl": "reference", "metric": METRIC,
+                    "unavailable": "oracle/_ref not built"}
+        run, vox, rows = r
+        sample = "%d of 32 x-rows of every sweep layer per step, %d threads" % (rows, threads)
+    else:
+        name, spec, store, x = nets[0]
+        run, vox, n = ref_network_sample(spec, store, x, threads)
+        threads = n
+        sample = "%d concurrent volumes per step, one voxplan.PlanRunner per thread" % n
     for _ in range(args.warmup):
-        one_pass()
+        run()
     t0 = time.perf_counter()
-    vox = 0
     for _ in range(args.steps):
-        vox += one_pass()
+        run()
     el = time.perf_counter() - t0
-    value = vox / el
+    value = vox * args.steps / el
     return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "output voxels/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": workload_name(args.config), "sample_rows": rows},
+        "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong" if args.config == 5 else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": DATA,
+        "config": {"workload": workload_name(args.config), "sample": sample},
         "cpu_baseline": {"value": value, "unit": "output voxels/s", "cores": threads,
-                         "kind": "reference",
-                         "sample": "%d of 32 x-rows per layer per step, %d threads" % (rows, threads)},
+                         "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "output voxels/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
 
 
-# ------------------------------------------------------------------ config 5
+# ------------------------------------------------------------------ B200 arm
 
-def run_tiled_volume(args, rank, world, dev, dist, peaks, flush):
+def run_b200(args, rank, world, local_rank):
     import torch
-    import paper_1903_07525_b200 as P
-    from paper_1903_07525_b200 import configs as C, tiling
-    spec, store = C.config5()
-    plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
-    grid = P.grid_for(plan, C.VOLUME5, overlap=0)
-    mine = [grid.tiles[i] for i in tiling.partition(len(grid.tiles), world, rank)]
-    dt = tiling.DeviceTiler(plan, grid, dev)
-    # synthetic volume slab for this rank's tiles only (seeded per x-range)
-    lo, hi, olo, ohi = dt.slab_bounds(mine)
-    rng = np.random.default_rng(500 + rank)
-    slab = rng.uniform(0, 1, (1, 1) + tuple(b - a for a, b in zip(lo, hi))).astype(np.float32)
-    dt.slab = torch.from_numpy(slab).to(dev)
-    dt.out_slab = torch.empty((1, 3) + tuple(b - a for a, b in zip(olo, ohi)),
-                              dtype=torch.float32, device=dev)
-    dt.lo, dt.olo = lo, olo
-    s = dt.runner.stream
-    for _ in range(max(1, args.warmup)):
-        dt.run(mine[:4])
-    torch.cuda.synchronize(dev)
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    peaks = load_peaks()
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    import bench_util as U
+    if args.config == 5:
+        res = U.bench_volume(args, rank, world, dev, dist, peaks, flush, backend=args.backend)
+        if rank == 0 and world == 1 and not args.no_subconfigs:
+            sub = {}
+            for c in (1, 2, 3, 4):
+                sub["config%d" % c] = U.bench_network(c, args, dev, peaks, flush,
+                                                      with_cpu=not args.no_cpu_baseline,
+                                                      with_e2e=not args.no_e2e,
+                                                      cpu_fn=cpu_baseline)
+            res["configs"] = sub
+            if args.backend == "b200":
+                res["x3"] = U.bench_volume(args, rank, world, dev, None, peaks, flush,
+                                           backend="b200-x3", light=True)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            res["cpu_baseline"] = cpu_baseline(5, U.build_nets(5), args.cpu_seconds)
+    else:
+        res = U.bench_network(args.config, args, dev, peaks, flush,
+                              with_cpu=(rank == 0 and world == 1 and not args.no_cpu_baseline),
+                              with_e2e=not args.no_e2e, headline=True, world=world, dist=dist,
+                              cpu_fn=cpu_baseline)
     if dist is not None:
         dist.barrier()
-    tot = 0.0
-    with ClockSampler(dev.index) as clk:
-        for _ in range(args.steps):
-            flush.fill_(1.0)
-            torch.cuda.synchronize(dev)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(torch.cuda.current_stream(dev))
-            dt.run(mine)
-            e1.record(torch.cuda.current_stream(dev))
-            torch.cuda.synchronize(dev)
-            tot += e0.elapsed_time(e1)
-    if dist is not None:
-        t = torch.tensor([tot], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot = t.item()
-    vox = int(np.prod(grid.volume_out))
-    ms = tot / args.steps
-    flops_patch = C.conv_flops(spec)
-    return {
-        "metric": METRIC, "value": vox / (ms * 1e-3), "unit": "output voxels/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic", "config": {"workload": workload_name(5), "tiles": len(grid.tiles),
-                                        "patches_per_launch": dt.batch,
-                                        "parallelism": "tiles/%d ranks" % world},
-        "tflops": flops_patch * len(grid.tiles) / (ms * 1e-3) / 1e12,
-        "gpu_launches": dt.launches_for(len(mine)) * args.steps,
-        "clocks": clk.summary(),
-    }
+        dist.destroy_process_group()
+    return res
+
+
+def spawn(args):
+    """bench.py --gpus N without torchrun: re-launch under torchrun, one
+    rank per GPU (127.0.0.1 rendezvous), and pass rank 0's line through."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))

@@ -13,6 +13,7 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libvxb.so")
+    config.addinivalue_line("markers", "slow: full-size parity against the host oracle (minutes)")
 
 
 @pytest.fixture

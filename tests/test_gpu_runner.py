@@ -85,12 +85,13 @@ def test_config_networks(cfg, backend):
     else:
         emu = R.run_plan(plan, x, storage="bf16")[name]
         emx, el2 = R.normalized_error(got, emu)
-        # config 5 is a 28-conv chain with unnormalised activations (|logit|
-        # up to ~600): single bf16 rounding flips are amplified, so only the
-        # L2 bound is meaningful there
-        tol_max, tol_l2 = {5: (0.5, 5e-2)}.get(cfg, (2e-2, 1e-2))
-        assert emx < tol_max and el2 < tol_l2, (emx, el2)
-        assert l2 < {5: 6e-2}.get(cfg, 3e-2), l2
+        # vs the same-rounding emulation: fp32 summation order plus the odd
+        # bf16 rounding flip of an intermediate tensor; vs the fp32 oracle:
+        # ~2x the emulated storage error (emulated: cfg1 3.4e-3, cfg3 3.8e-3,
+        # cfg4 1.5e-2, cfg5 1.7e-2 max-normalised)
+        assert emx < 2e-2 and el2 < 1e-2, (emx, el2)
+        tol = {1: (5e-3, 5e-3), 3: (8e-3, 8e-3), 4: (3e-2, 2.5e-2), 5: (4e-2, 1e-2)}[cfg]
+        assert mx < tol[0] and l2 < tol[1], (mx, l2)
 
 
 def test_runner_graph_replay_deterministic_and_validates():
@@ -261,10 +262,7 @@ def test_zwin_first_layer_matches_plain_pack(cfg, monkeypatch):
     assert mx < 2e-2 and l2 < 5e-3, (mx, l2)
     emu = R.run_plan(plan, x, storage="bf16")[n]
     mx, l2 = R.normalized_error(a, emu)
-    # config 5's chain of unnormalised He-init convs amplifies single bf16
-    # rounding flips (same bound as test_config_networks)
-    tol = (0.5, 5e-2) if cfg == 5 else (2e-2, 1e-2)
-    assert mx < tol[0] and l2 < tol[1], (mx, l2)
+    assert mx < 2e-2 and l2 < 1e-2, (mx, l2)
 
 
 def test_pack_zwin_lanes_exact():
