@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define VXB_ABI_VERSION 4
+#define VXB_ABI_VERSION 5
 
 /* element types */
 #define VXB_BF16 0
@@ -136,6 +136,19 @@ typedef struct vxb_conv_desc {
   int32_t prec;            /* VXB_PREC_* the weights were packed with (X3 <=> split input) */
   int32_t reserved[5];
   vxb_tensor pool_out;     /* pooled view, logical (n, cout, ox, oy/2, oz/2) */
+  /* Fused 1x1x1 head: the network's next step when it is a 1x1x1 conv that
+   * alone reads this conv's output (the U-nets' output layer, SURVEY §8f
+   * rank 3).  head_out = head_act(head_b + head_w . y), y = this conv's
+   * activated output per voxel, which is then never stored (out gives only
+   * the shape).  head_w: (head_cout, cout) fp32; head_out: fp32 standard
+   * (NCDHW) view (n, head_cout, ox, oy, oz).  head_cout 0 = no head. */
+  const float *head_w;
+  const float *head_b;
+  int32_t head_cout;       /* 0 .. 4 */
+  int32_t head_act;        /* VXB_ACT_* */
+  float head_alpha;
+  int32_t head_reserved_;
+  vxb_tensor head_out;
 } vxb_conv_desc;
 
 /* Transposed convolution (kernels_py.deconv3d, kernels_py.py:162-196):

@@ -22,7 +22,7 @@ VXB_BF16X2 = 2       # split bf16: hi plane + lo plane (s[1]/2 apart)
 PREC_BF16 = 0        # VXB_PREC_BF16
 PREC_X3 = 1          # VXB_PREC_X3
 ACT_CODE = {None: 0, "relu": 1, "elu": 2, "sigmoid": 3}   # kernels_cy.py:19
-ABI_VERSION = 4      # include/vxb.h VXB_ABI_VERSION
+ABI_VERSION = 5      # include/vxb.h VXB_ABI_VERSION
 COPY_INDEPENDENT = 1  # VXB_COPY_INDEPENDENT
 PATH_TC = 1
 PATH_DIRECT = 2
@@ -69,6 +69,13 @@ class VxbConvDesc(ctypes.Structure):
         ("prec", c_int32),
         ("reserved", c_int32 * 5),
         ("pool_out", VxbTensor),
+        ("head_w", c_void_p),
+        ("head_b", c_void_p),
+        ("head_cout", c_int32),
+        ("head_act", c_int32),
+        ("head_alpha", c_float),
+        ("head_reserved_", c_int32),
+        ("head_out", VxbTensor),
     ]
 
 

@@ -62,23 +62,32 @@ struct TileCoord {
   bool dummy;   // padding tile of a CTA pair: loads as tile 0, stores nothing
 };
 
+__device__ __forceinline__ int fdiv(int t, unsigned long long m) {
+  return static_cast<int>((static_cast<unsigned long long>(static_cast<unsigned>(t)) * m) >> 40);
+}
+
 __device__ __forceinline__ TileCoord decode_tile(const TcParams &p, int t) {
   TileCoord c;
-  int sp = t % p.spatial_pad;
-  const int rn = t / p.spatial_pad;
+  const int rn = fdiv(t, p.dm[0]);
+  int sp = t - rn * p.spatial_pad;
   c.dummy = sp >= p.spatial_real;
   if (c.dummy) sp = 0;
   t = sp + rn * p.spatial_real;
-  int tz = t % p.tiles_z;
-  t /= p.tiles_z;
-  int ty = t % p.tiles_y;
-  t /= p.tiles_y;
-  int tx = t % p.tiles_x;
-  t /= p.tiles_x;
-  c.b = t % p.nb;
-  t /= p.nb;
-  c.nt = t % p.n_tiles;
-  c.rep = t / p.n_tiles;
+  int q = fdiv(t, p.dm[1]);
+  const int tz = t - q * p.tiles_z;
+  t = q;
+  q = fdiv(t, p.dm[2]);
+  const int ty = t - q * p.tiles_y;
+  t = q;
+  q = fdiv(t, p.dm[3]);
+  const int tx = t - q * p.tiles_x;
+  t = q;
+  q = fdiv(t, p.dm[4]);
+  c.b = t - q * p.nb;
+  t = q;
+  q = fdiv(t, p.dm[5]);
+  c.nt = t - q * p.n_tiles;
+  c.rep = q;
   c.x0 = tx * p.ex;
   c.y0 = ty * p.ey;
   c.z0 = tz * TILE_Z;
@@ -230,16 +239,29 @@ __device__ __forceinline__ void dbg_clock(const TcParams &p, int it, int slot) {
     p.dbg[(static_cast<size_t>(blockIdx.x) * 64 + it) * 8 + slot] = clock64();
 }
 
-constexpr int EPI_WARPS = 12;
-constexpr int TC_THREADS = 96 + 32 * EPI_WARPS;   // A-TMA, MMA, B-TMA + epilogue
+// Epilogue warps (a multiple of 4: EPI/4 per TMEM lane quarter).  16 when
+// the 104-register budget allows (608 threads = 63.2 K registers); the
+// fp32-input variant adds 4 converter warps and keeps 12.
+#ifndef VXB_EPI_WARPS
+#define VXB_EPI_WARPS 16
+#endif
+__host__ __device__ constexpr int epi_warps(bool f32in) { return f32in ? 12 : VXB_EPI_WARPS; }
+// registers per thread: warps are spread over the 4 SM sub-partitions
+// (16 K registers each), so 19-20 warps need <= 96 per thread; 15-16 warps
+// (12 epilogue warps + roles + converters) fit 104
+#if VXB_EPI_WARPS > 12
+#define VXB_TC_MAXNREG 96
+#else
+#define VXB_TC_MAXNREG 104
+#endif
 constexpr int CVT_WARPS = 4;                      // fp32-input converters (F32IN)
 __host__ __device__ constexpr int tc_threads(bool f32in) {
-  return TC_THREADS + (f32in ? 32 * CVT_WARPS : 0);
+  return 96 + 32 * epi_warps(f32in) + (f32in ? 32 * CVT_WARPS : 0);
 }
 
 // Byte offsets inside the dynamic smem block (all derivable from p).
 struct SmemMap {
-  uint32_t a, b, stg, bias, scale, bars;
+  uint32_t a, b, stg, bias, scale, head, bars;
 };
 __host__ __device__ inline SmemMap smem_map(const TcParams &p) {
   SmemMap m;
@@ -249,7 +271,8 @@ __host__ __device__ inline SmemMap smem_map(const TcParams &p) {
   m.bias = m.stg + p.n_stg * p.stg_bytes;
   const uint32_t cpad = p.n_tiles * p.nt;
   m.scale = m.bias + cpad * 4;
-  m.bars = (m.scale + cpad * 4 + 15) & ~15u;
+  m.head = m.scale + cpad * 4;                 // fused head weights [head_cout][cpad]
+  m.bars = (m.head + (p.head_cout > 0 ? 4 * cpad * 4 : 0) + 15) & ~15u;
   return m;
 }
 
@@ -467,10 +490,12 @@ __device__ __forceinline__ void mma_group_fold_pair(
   }
 }
 
-template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN, bool POOL = false>
-__global__ void __maxnreg__(104)
+template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN, bool POOL = false,
+          bool HEAD = false>
+__global__ void __maxnreg__(VXB_TC_MAXNREG)
     conv3d_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int EPI_WARPS = epi_warps(F32IN);
   // warp index broadcast from lane 0 so ptxas treats each role's code as
   // warp-uniform (as CUTLASS's canonical_warp_idx_sync does)
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
@@ -483,6 +508,7 @@ __global__ void __maxnreg__(104)
   uint8_t *b_buf = smem + sm.b;
   float *s_bias = reinterpret_cast<float *>(smem + sm.bias);
   float *s_scale = reinterpret_cast<float *>(smem + sm.scale);
+  float *s_head = reinterpret_cast<float *>(smem + sm.head);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + sm.bars);
   uint64_t *a_full = bars;
   uint64_t *a_empty = a_full + p.na;
@@ -522,6 +548,11 @@ __global__ void __maxnreg__(104)
     s_bias[c] = cr < p.cout ? p.bias[cr] : 0.f;
     s_scale[c] = (cr < p.cout && p.scale) ? p.scale[cr] : 1.f;
   }
+  if (HEAD)
+    for (int i = threadIdx.x; i < 4 * cpad; i += blockDim.x) {
+      const int j = i / cpad, c = i - j * cpad;
+      s_head[i] = (j < p.head_cout && c < p.cout) ? p.head_w[j * p.cout + c] : 0.f;
+    }
   fence_proxy_async_smem();
 
   if (warp == 0 && lane == 0) {
@@ -732,8 +763,8 @@ __global__ void __maxnreg__(104)
         constexpr int BXV = decltype(bx_c)::value;
         constexpr int KIND = decltype(kind_c)::value;   // 0 plain, 1 folded, 2 folded pair
         for (int it = 0; it < my_tiles; ++it) {
-          const int acc = it % p.acc_stages;
-          mbar_wait(&t_empty[acc], ((it / p.acc_stages) & 1) ^ 1);
+          const int acc = (it & (p.acc_stages - 1));
+          mbar_wait(&t_empty[acc], (((p.acc_stages == 2 ? (it >> 1) : it) & 1)) ^ 1);
           tc_fence_after();
           const uint32_t d_base = tmem_base + acc * acc_stride;
           uint32_t accumulate = 0, first = 1;
@@ -926,7 +957,7 @@ __global__ void __maxnreg__(104)
     int it = 0;
     for (int tile = first_tile; tile < p.total_tiles; tile += tile_step, ++it) {
       TileCoord tc = decode_tile(p, tile);
-      const int acc = it % p.acc_stages;
+      const int acc = (it & (p.acc_stages - 1));
       const int rc = (p.slice_y ? tc.x0 : tc.y0) + ra, z = tc.z0 + zz;
       const int sc0 = p.slice_y ? tc.y0 : tc.x0, slim = p.slice_y ? p.oy : p.ox;
       const bool yz_ok = rc < (p.slice_y ? p.ox : p.oy) && z < p.oz && !tc.dummy;
@@ -1110,6 +1141,53 @@ __global__ void __maxnreg__(104)
         }
       };
 
+      if constexpr (HEAD) {
+        // fused 1x1x1 head: this warp takes whole slices (every column item
+        // of a slice), so each thread holds all fmaps of its voxel; the
+        // activated values feed head_cout dot products and are never stored
+        mbar_wait_sleep(&t_full[acc], ((p.acc_stages == 2 ? (it >> 1) : it) & 1));
+        tc_fence_after();
+        const EpiView &hv = p.head_out;
+        for (int s = sub; s < p.bx; s += NSUB) {
+          float hsum[4] = {0.f, 0.f, 0.f, 0.f};
+          const int x = sc0 + s;
+          for (int ci = 0; ci < col_items; ++ci) {
+            const int item = s * col_items + ci;
+            uint32_t rv[16];
+            tmem_ld16_issue(taddr_of(item), rv);
+            float bq[16];
+            if (BASE) {
+              uint4 qd[2];
+              if (braw) base_issue(item, qd);
+              base_get(item, qd, bq);
+            }
+            tmem_wait_ld16(rv);
+            const int col = tc.nt * p.nt + ci * 16;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float r = __uint_as_float(rv[i]) + s_bias[col + i];
+              if (BASE) r = fmaf(s_scale[col + i], bq[i], r);
+              if (act == VXB_ACT_RELU) r = fmaxf(r, 0.f);
+              else if (act == VXB_ACT_ELU) r = fast_elu(r, p.alpha);
+              else if (act == VXB_ACT_SIGMOID) r = fast_sigmoid(r);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) hsum[j] = fmaf(r, s_head[j * cpad + col + i], hsum[j]);
+            }
+          }
+          if (yz_ok && x < slim) {
+            float *op = static_cast<float *>(hv.data) + tc.b * hv.s[0] + rc * hv.s[ra_dim] +
+                        z * hv.s[4] + x * hv.s[sl_dim];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (j < p.head_cout) op[j * hv.s[1]] = apply_act(hsum[j] + p.head_b[j], p.head_act,
+                                                               p.head_alpha);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&t_empty[acc]);
+        continue;
+      }
       uint32_t ra[16], rb[16];
       uint4 qa[2], qb[2];
       float bv[16];
@@ -1118,7 +1196,7 @@ __global__ void __maxnreg__(104)
         if (item < items) base_issue(item, qa);
         if (item + NSUB < items) base_issue(item + NSUB, qb);
       }
-      mbar_wait_sleep(&t_full[acc], (it / p.acc_stages) & 1);
+      mbar_wait_sleep(&t_full[acc], ((p.acc_stages == 2 ? (it >> 1) : it) & 1));
       if (warp == 3 && lane == 0) dbg_mark(p, it, 3);
       tc_fence_after();
       if (item < items) tmem_ld16_issue(taddr_of(item), ra);
@@ -1170,10 +1248,11 @@ size_t tc_smem_bytes(const TcParams &p) {
          16;
 }
 
-template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN = false, bool POOL = false>
+template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN = false, bool POOL = false,
+          bool HEAD = false>
 static int launch_variant(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t stream,
                           size_t smem) {
-  auto kern = conv3d_tc_kernel<ACT, FASTOUT, BASE, PAIR, F32IN, POOL>;
+  auto kern = conv3d_tc_kernel<ACT, FASTOUT, BASE, PAIR, F32IN, POOL, HEAD>;
   if (int rc = ensure_smem_attr(kern, 232448, "cudaFuncSetAttribute(conv3d_tc)")) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1221,6 +1300,12 @@ static int launch_act(const TcParams &p, const TcMaps &maps, int grid, cudaStrea
                       size_t smem) {
   const bool fast = ((p.out.dtype == VXB_BF16 || p.out.dtype == VXB_BF16X2) && p.out.blocked) ||
                     (p.out.dtype == VXB_F32 && !p.out.blocked);
+  if (p.head_cout > 0) {
+    if (PAIR || p.f32in || p.pool || p.rep_n || p.reps != 1 || p.n_tiles != 1)
+      return set_error(VXB_EUNSUPPORTED,
+                       "fused head: single-CTA tiles, one N tile, no fp32 input / pooling");
+    return launch_variant<-1, true, BASE, false, false, false, true>(p, maps, grid, s, smem);
+  }
   if (p.pool) {
     if (PAIR || p.f32in || p.out.dtype != VXB_BF16 || !p.out.blocked ||
         p.pool_out.dtype != VXB_BF16 || !p.pool_out.blocked)

@@ -486,6 +486,11 @@ struct TcLaunch {
   int nt_cap;
   int pool;
   EpiView pool_out;
+  // fused 1x1x1 head
+  const float *head_w, *head_b;
+  int head_cout, head_act;
+  float head_alpha;
+  EpiView head_out;
 };
 
 static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
@@ -547,10 +552,14 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
   const long long spatial_min =
       static_cast<long long>(ceil_div(slice_y ? a.oy : a.ox, 8)) *
       ceil_div(slice_y ? a.ox : a.oy, TILE_Y) * ceil_div(a.oz, TILE_Z);
-  const bool can_pair = (!L.fold || fold_pair) && !a.pool && spatial_min >= 2 && L.nt % 16 == 0 &&
-                        L.nt / 8 <= 256 && out_ok && (pair_env == 1 || pair_env == 2);
-  int rc = tc_configure(L, a.k, slice_y ? a.oy : a.ox, other_tiles, sms, a.reps, stg_bytes,
-                        can_pair, pair_env, fold_pair, c);
+  const bool can_pair = (!L.fold || fold_pair) && !a.pool && !a.head_cout && spatial_min >= 2 &&
+                        L.nt % 16 == 0 && L.nt / 8 <= 256 && out_ok &&
+                        (pair_env == 1 || pair_env == 2);
+  // a fused head keeps its weights in smem: 4 rows x the padded fmaps
+  const int head_smem = a.head_cout ? 4 * L.n_tiles * L.nt * 4 : 0;
+  int rc = tc_configure(L, a.k, slice_y ? a.oy : a.ox, other_tiles, sms, a.reps,
+                        stg_bytes + head_smem, can_pair && !(fold_pair && a.head_cout), pair_env,
+                        fold_pair && !a.head_cout, c);
   if (rc) return rc;
   TcParams p;
   memset(&p, 0, sizeof(p));
@@ -580,6 +589,15 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
   p.spatial_real = static_cast<int>(spatial);
   p.spatial_pad = static_cast<int>(spatial_pad);
   p.total_tiles = static_cast<int>(total);
+  {
+    const int ds[6] = {p.spatial_pad, p.tiles_z, p.tiles_y, p.tiles_x, p.nb, p.n_tiles};
+    for (int i = 0; i < 6; ++i) {
+      const unsigned long long d = static_cast<unsigned long long>(std::max(1, ds[i]));
+      if (static_cast<unsigned long long>(total) * d >= (1ull << 40))
+        return set_error(VXB_EUNSUPPORTED, "tile grid too large for the fast tile decode");
+      p.dm[i] = ((1ull << 40) + d - 1) / d;
+    }
+  }
   p.kx = a.k[0];
   p.ky = a.k[1];
   p.kz = a.k[2];
@@ -688,6 +706,12 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
   }
   p.rep_n = a.rep_n;
   (void)rep_offsets;
+  p.head_w = a.head_w;
+  p.head_b = a.head_b;
+  p.head_cout = a.head_cout;
+  p.head_act = a.head_act;
+  p.head_alpha = a.head_alpha;
+  p.head_out = a.head_out;
   p.cout = a.cout;
   p.act = a.act;
   p.alpha = a.alpha;
@@ -1014,10 +1038,30 @@ int vxb_conv3d(const vxb_conv_desc *d, void *stream) {
     } else if (d->pool_mode != VXB_POOL_FUSED_NONE) {
       return set_error(VXB_EINVAL, "conv3d: bad pool_mode %d", d->pool_mode);
     }
+    if (d->head_cout) {
+      const vxb_tensor &h = d->head_out;
+      if ((rc = check_view(&h, "conv3d.head_out"))) return rc;
+      if (d->head_cout < 0 || d->head_cout > 4 || !d->head_w || !d->head_b)
+        return set_error(VXB_EINVAL, "conv3d: fused head needs 1..4 fmaps, weights and bias");
+      if (h.dtype != VXB_F32 || h.blocked || h.n != d->out.n || h.c != d->head_cout ||
+          h.x != d->out.x || h.y != d->out.y || h.z != d->out.z)
+        return set_error(VXB_EINVAL,
+                         "conv3d.head_out must be an fp32 standard view (n, head_cout, ox, oy, oz)");
+      if (d->head_act < 0 || d->head_act > 3 || d->pool_mode != VXB_POOL_FUSED_NONE)
+        return set_error(VXB_EINVAL, "conv3d: bad head activation / head with pooling");
+      a.head_w = d->head_w;
+      a.head_b = d->head_b;
+      a.head_cout = d->head_cout;
+      a.head_act = d->head_act;
+      a.head_alpha = d->head_alpha;
+      a.head_out = to_epi(h);
+    }
     return run_tc(a, s);
   }
   if (d->pool_mode != VXB_POOL_FUSED_NONE)
     return set_error(VXB_EUNSUPPORTED, "fused pooling needs the tensor-core conv path");
+  if (d->head_cout)
+    return set_error(VXB_EUNSUPPORTED, "a fused head needs the tensor-core conv path");
   if (two) return set_error(VXB_EUNSUPPORTED, "direct conv path takes a single input");
   DirectParams p;
   memset(&p, 0, sizeof(p));

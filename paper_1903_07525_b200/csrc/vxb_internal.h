@@ -27,6 +27,11 @@ struct TcParams {
   int ox, oy, oz;              // output extents
   int tiles_x, tiles_y, tiles_z;
   int n_tiles, reps, total_tiles;
+  // fast division of tile indices: q = (t * m) >> 40 with m = ceil(2^40 / d)
+  // for d = spatial_pad, tiles_z, tiles_y, tiles_x, nb, n_tiles (exact while
+  // t * d < 2^40, checked on the host); replaces six runtime integer
+  // divisions per tile in every epilogue warp
+  unsigned long long dm[6];
   int spatial_real, spatial_pad;  // tiles per (rep, ntile); padded to the cluster size
   int cluster;                    // 1, or 2 = CTA pair sharing B via TMA multicast
   int pair;                       // cta_group::2 MMA (M = 256), each CTA holds half of B
@@ -81,6 +86,11 @@ struct TcParams {
   // fused 1x2x2 max pool of the stored output (VXB_POOL_FUSED_MAX122)
   int pool, pool_oy, pool_oz;
   EpiView pool_out;
+  // fused 1x1x1 head (vxb_conv_desc.head_*): head_out = act(head_b + head_w . y)
+  const float *head_w, *head_b;
+  int head_cout, head_act;
+  float head_alpha;
+  EpiView head_out;
   unsigned long long *dbg;     // optional per-tile phase timestamps (VXB_TC_DEBUG)
   int dbg_mode;                // VXB_TC_DBGMODE (timing experiments, wrong results): 1 no
                                // epilogue, 2 no A loads, 4 no B loads, 8 no MMAs (resident B),

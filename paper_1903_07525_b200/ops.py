@@ -94,12 +94,32 @@ def pack_conv(kernel, bias, *, stride=(1, 1, 1), base_scale=None, cin_split=None
                       cin0, cin1, cout, k, stride, path, prec)
 
 
+@dataclass
+class Head:
+    """A 1x1x1 conv fused into the producing conv's epilogue (vxb_conv_desc
+    head_*): w (cout_h, cin) and b on the device, its fused activation."""
+    w: object
+    b: object
+    cout: int
+    act: tuple = None
+
+
+def make_head(kernel, bias, fused_act=None, device=None) -> Head:
+    w = np.asarray(kernel, np.float32)
+    cout = int(w.shape[0])
+    return Head(device_vector(w.reshape(-1), device=device), device_vector(bias, cout, device),
+                cout, fused_act)
+
+
 def conv3d(x: DTensor, pk: PackedConv, out: DTensor, *, pad=(0, 0, 0), base: DTensor = None,
            fused_act=None, x2: DTensor = None, off=(0, 0, 0), off2=(0, 0, 0),
-           pool_out: DTensor = None, stream=None) -> None:
+           pool_out: DTensor = None, head: Head = None, head_out: DTensor = None,
+           stream=None) -> None:
     """Fused conv step (kernels_cy.conv3d -> _kernels.conv3d, _kernels.pyx:44-179).
     ``pool_out`` (n, cout, x, y/2, z/2): also write the 1x2x2 max pool of the
-    stored output (the following MaxPool step, ops.py:63-86, fused)."""
+    stored output (the following MaxPool step, ops.py:63-86, fused).
+    ``head`` / ``head_out``: the network's next 1x1x1 conv computed in this
+    conv's epilogue into the fp32 NCDHW ``head_out`` (``out`` is not written)."""
     L = _lib.lib()
     d = _lib.VxbConvDesc()
     d.in0 = x.vxb()
@@ -121,6 +141,12 @@ def conv3d(x: DTensor, pk: PackedConv, out: DTensor, *, pad=(0, 0, 0), base: DTe
     if pool_out is not None:
         d.pool_mode = 1
         d.pool_out = pool_out.vxb()
+    if head is not None:
+        d.head_w = head.w.data_ptr()
+        d.head_b = head.b.data_ptr()
+        d.head_cout = head.cout
+        d.head_act, d.head_alpha = _act(head.act)
+        d.head_out = head_out.vxb()
     _lib.check(L.vxb_conv3d(ctypes.byref(d), stream or current_stream_handle()), "vxb_conv3d")
 
 

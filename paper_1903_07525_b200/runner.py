@@ -70,7 +70,7 @@ class PlanRunner:
     """Executes one ExecutionPlan on one B200; reusable, deterministic."""
 
     def __init__(self, plan, backend=None, *, device=None, use_graph=True, fuse_concat=True,
-                 fuse_pool=False, fuse_input=False, probe=None):
+                 fuse_pool=False, fuse_input=False, fuse_head=True, probe=None):
         torch = _torch()
         from .backend import resolve_device_backend
         self.backend = resolve_device_backend(backend)
@@ -88,6 +88,8 @@ class PlanRunner:
         self.fuse_concat = fuse_concat and self.precision == "bf16"
         self.fuse_pool = fuse_pool and self.precision == "bf16"
         self.fuse_input = fuse_input
+        self.fuse_head = fuse_head and self.precision in ("bf16", "x3") and \
+            os.environ.get("VXB_FUSE_HEAD", "1") == "1"
         self._conv_path = _lib.PATH_DIRECT if self.precision == "fp32" else 0
         self.stream = torch.cuda.Stream(device=self.device)
         # independent input packs (set by PlanBatch while it captures).  A
@@ -176,6 +178,8 @@ class PlanRunner:
             self._fuse_mergecrop()
         if self.fuse_pool:
             self._fuse_maxpool()
+        if self.fuse_head:
+            self._fuse_head()
 
     def _fuse_mergecrop(self):
         """Zero-copy MergeCrop: a conv whose only input is a MergeCrop of two
@@ -204,6 +208,47 @@ class PlanRunner:
             m.readers = 0
             info["x"] = None
             drop.add(src)
+        if drop:
+            self._ops = [op for i, op in enumerate(self._ops) if i not in drop]
+
+    def _fuse_head(self):
+        """The network's 1x1x1 output conv (<= 4 fmaps, e.g. the U-nets'
+        3-fmap head + sigmoid) computed in the epilogue of the conv that
+        produces its only input (vxb_conv_desc.head_*): that conv's activated
+        output is never stored, the head writes the fp32 network output
+        (SURVEY §8f rank 3).  The reference runs the head as its own conv
+        step over the stored tensor (executor.py:134-164)."""
+        producers = {id(info["out"]): i for i, (_, _, info) in enumerate(self._ops)}
+        out_names = {id(v): n for n, v in self._out_values.items()}
+        drop = set()
+        for i, (kind, st, info) in enumerate(self._ops):
+            if kind is not LayerKind.CONVOLUTION or st.additive or "segments" in info:
+                continue
+            k = self.plan.weights.tensor(st.name, ROLE_KERNEL).shape
+            if tuple(k[2:]) != (1, 1, 1) or k[0] > 4 or any(info["pad"]):
+                continue
+            if tuple(st.params.get("stride", (1, 1, 1))) != (1, 1, 1):
+                continue
+            hout = info["out"]
+            if out_names.get(id(hout)) is None or hout.readers != 1:
+                continue
+            v = info["x"]
+            j = producers.get(id(v))
+            if j is None or v.readers != 1:
+                continue
+            pkind, pst, pinfo = self._ops[j]
+            if pkind is not LayerKind.CONVOLUTION or "pool_out" in pinfo or "head" in pinfo:
+                continue
+            if tuple(pst.params.get("stride", (1, 1, 1))) != (1, 1, 1):
+                continue
+            pk = self.plan.weights.tensor(pst.name, ROLE_KERNEL).shape
+            L = _lib.lib()
+            if L.vxb_conv_select(pk[1], pk[0], _lib.i3(pk[2:]), _lib.i3((1, 1, 1))) != \
+                    _lib.PATH_TC:
+                continue
+            pinfo["head"] = (st, hout)
+            v.readers = 0
+            drop.add(i)
         if drop:
             self._ops = [op for i, op in enumerate(self._ops) if i not in drop]
 
@@ -266,6 +311,8 @@ class PlanRunner:
             last.setdefault(id(info["out"]), i)
             if "pool_out" in info:
                 last.setdefault(id(info["pool_out"]), i)
+            if "head" in info:
+                last.setdefault(id(info["head"][1]), i)
         for v in self._out_values.values():
             last[id(v)] = len(self._ops)
         slots, free = [], []
@@ -293,6 +340,9 @@ class PlanRunner:
             if "pool_out" in info:
                 info["pool_out"].slot = grab(info["pool_out"])
                 live.append(info["pool_out"])
+            if "head" in info:
+                info["head"][1].slot = grab(info["head"][1])
+                live.append(info["head"][1])
             keep = []
             for v in live:
                 if last.get(id(v), -1) <= i:
@@ -385,6 +435,15 @@ class PlanRunner:
                 scale = st.base_scale if st.additive else None
                 kern = w.tensor(st.name, ROLE_KERNEL)
                 stride = tuple(st.params.get("stride", (1, 1, 1)))
+                hd = hout = None
+                if "head" in info:       # fused 1x1x1 output conv (_fuse_head)
+                    hst, hval = info["head"]
+                    hname = fused_out[id(hval)]
+                    hk = np.asarray(w.tensor(hst.name, ROLE_KERNEL), np.float32)
+                    hd = K.make_head(hk.reshape(hk.shape[0], hk.shape[1]),
+                                     w.tensor(hst.name, ROLE_BIAS), hst.fused_act, device=dev)
+                    hout = standard(self._out_std[hname])
+                    self._fused_outputs.add(hname)
                 if "segments" in info:
                     a, b, oa, ob = info["segments"]
                     pk = K.pack_conv(kern, w.tensor(st.name, ROLE_BIAS), stride=stride,
@@ -392,9 +451,9 @@ class PlanRunner:
                                      out_shape=tuple(info["out"].dims[2:]), device=dev)
                     pool = info["pool_out"].dt if "pool_out" in info else None
                     calls.append(lambda a=a.dt, b=b.dt, pk=pk, out=out, base=base, oa=oa, ob=ob,
-                                 act=st.fused_act, pool=pool:
+                                 act=st.fused_act, pool=pool, hd=hd, hout=hout:
                                  K.conv3d(a, pk, out, base=base, fused_act=act, x2=b, off=oa,
-                                          off2=ob, pool_out=pool))
+                                          off2=ob, pool_out=pool, head=hd, head_out=hout))
                 elif id(info) in self._zwin:
                     xz, kz, pz = self._zwin[id(info)]
                     # w'(co, l, dx, dy, 0) = w(co, 0, dx, dy, l)
@@ -406,9 +465,9 @@ class PlanRunner:
                     pool = info["pool_out"].dt if "pool_out" in info else None
                     calls.append(lambda x=xz, pk=pk, out=out, base=base,
                                  pad=(info["pad"][0], info["pad"][1], 0), act=st.fused_act,
-                                 pool=pool:
+                                 pool=pool, hd=hd, hout=hout:
                                  K.conv3d(x, pk, out, pad=pad, base=base, fused_act=act,
-                                          pool_out=pool))
+                                          pool_out=pool, head=hd, head_out=hout))
                 else:
                     pk = K.pack_conv(kern, w.tensor(st.name, ROLE_BIAS), stride=stride,
                                      base_scale=scale, path=self._conv_path,
@@ -419,9 +478,9 @@ class PlanRunner:
                         raise ExecutionError("fused fp32 input needs the tensor-core conv path")
                     pool = info["pool_out"].dt if "pool_out" in info else None
                     calls.append(lambda x=x, pk=pk, out=out, base=base,
-                                 pad=info["pad"], act=st.fused_act, pool=pool:
+                                 pad=info["pad"], act=st.fused_act, pool=pool, hd=hd, hout=hout:
                                  K.conv3d(x, pk, out, pad=pad, base=base, fused_act=act,
-                                          pool_out=pool))
+                                          pool_out=pool, head=hd, head_out=hout))
             elif kind is LayerKind.DECONVOLUTION:
                 base = info["base"].dt if "base" in info else None
                 scale = st.base_scale if st.additive else None

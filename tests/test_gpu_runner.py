@@ -329,3 +329,27 @@ def test_all_ops_network_matches_oracle(backend):
         e_mx, e_l2 = R.normalized_error(got, emu)
         assert e_mx < 3e-2 and e_l2 < 1.5e-2, (e_mx, e_l2)
         assert mx < 5e-2 and l2 < 2e-2, (mx, l2)
+
+
+@pytest.mark.parametrize("cfg", [4, 5])
+@pytest.mark.parametrize("backend", ["b200", "b200-x3"])
+def test_fused_head_matches_unfused(cfg, backend):
+    """The 1x1x1 output conv fused into the previous conv's epilogue
+    (vxb_conv_desc.head_*) reads that conv's fp32 activations instead of
+    their stored (bf16 / split) copy: one launch fewer, same network."""
+    spec, store = _small(cfg)
+    plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
+    lo, hi = C.input_range(cfg)
+    x = C.make_input(spec, 3, lo, hi)
+    fused = P.PlanRunner(plan, backend=backend)
+    plain = P.PlanRunner(plan, backend=backend, fuse_head=False)
+    assert fused.launches == plain.launches - 1
+    (n, a), = fused.run(x).items()
+    b = plain.run(x)[n]
+    ref = R.ref_run(spec, store, x)[n]
+    mx, l2 = R.normalized_error(a, ref)
+    if backend == "b200-x3":
+        assert mx < X3_NET_TOL[cfg], mx
+    else:
+        assert R.normalized_error(a, b)[0] < 2e-2
+        assert mx < {4: 3e-2, 5: 4e-2}[cfg] and l2 < 2.5e-2, (mx, l2)

@@ -31,7 +31,7 @@ def test_header_symbols_all_bound_and_exported():
     L = _lib.lib()
     for s in syms:
         assert hasattr(L, s)
-    assert L.vxb_abi_version() == _lib.ABI_VERSION == 4
+    assert L.vxb_abi_version() == _lib.ABI_VERSION == 5
 
 
 def test_host_packing_sizes_and_selection():

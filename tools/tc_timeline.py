@@ -26,16 +26,21 @@ for case in os.environ.get("CASES", "8:333,16:333,32:333").split(","):
     if os.environ.get("F32IN"):
         x = D.standard(torch.randn((1, c) + spatial, device=dev))
     out = D.empty_blocked(1, cout, spatial)
+    base = None
+    if os.environ.get("BASE") == "1":        # residual operand (the c2 convs of config 5)
+        base = D.empty_blocked(1, cout, spatial)
+        base.t.copy_(torch.randn(base.t.shape, device=dev).to(torch.bfloat16))
     w = (np.random.default_rng(0).standard_normal((cout, c) + k) * 0.05).astype(np.float32)
-    pk = K.pack_conv(w, np.zeros(cout, np.float32))
+    pk = K.pack_conv(w, np.zeros(cout, np.float32),
+                     base_scale=np.ones(cout, np.float32) if base is not None else None)
     pad = tuple(v // 2 for v in k)
     for _ in range(3):
-        K.conv3d(x, pk, out, pad=pad, fused_act=FA)
+        K.conv3d(x, pk, out, pad=pad, fused_act=FA, base=base)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(10):
-        K.conv3d(x, pk, out, pad=pad, fused_act=FA)
+        K.conv3d(x, pk, out, pad=pad, fused_act=FA, base=base)
     e1.record()
     torch.cuda.synchronize()
     ev_us = e0.elapsed_time(e1) / 10 * 1e3
