@@ -208,29 +208,15 @@ def statistics_mean(v):
 
 def gather_volume(dt, mine, grid, dev, dist, rank, world):
     """Rank 0 receives every rank's output slab into one device volume over
-    NCCL (point-to-point); max-over-ranks device time in ms."""
+    NCCL (tiling.gather_volume, point-to-point); max-over-ranks device time
+    in ms."""
     import torch
     from paper_1903_07525_b200 import tiling
     _sync_barrier(dev, dist)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     cs = torch.cuda.current_stream(dev)
     e0.record(cs)
-    if rank == 0:
-        full = torch.empty((1, dt.out_fmaps) + tuple(grid.volume_out), dtype=torch.float32,
-                           device=dev)
-        for r in range(world):
-            tiles = [grid.tiles[i] for i in tiling.partition(len(grid.tiles), world, r)]
-            _, _, olo, ohi = dt.slab_bounds(tiles)
-            win = (slice(None), slice(None)) + tuple(slice(a, b) for a, b in zip(olo, ohi))
-            if r == 0:
-                full[win].copy_(dt.out_slab)
-            else:
-                buf = torch.empty((1, dt.out_fmaps) + tuple(b - a for a, b in zip(olo, ohi)),
-                                  dtype=torch.float32, device=dev)
-                dist.recv(buf, src=r)
-                full[win].copy_(buf)
-    else:
-        dist.send(dt.out_slab.contiguous(), dst=0)
+    tiling.gather_volume(dt.out_slab, grid, rank, world, dist)
     e1.record(cs)
     torch.cuda.synchronize(dev)
     return _max_over_ranks(e0.elapsed_time(e1), dev, dist)

@@ -140,6 +140,61 @@ def partition(n_tiles: int, parts: int, rank: int) -> range:
     return range(lo, hi)
 
 
+def slab_bounds(grid: TileGrid, tiles):
+    """(in_lo, in_hi, out_lo, out_hi) of the input slab a block of tiles
+    reads and of the output region it writes (bounding boxes)."""
+    lo = [min(t.in_lo[d] for t in tiles) for d in range(3)]
+    hi = [max(t.in_lo[d] + grid.patch_in[d] for t in tiles) for d in range(3)]
+    olo = [min(t.out_lo[d] for t in tiles) for d in range(3)]
+    ohi = [max(t.out_lo[d] + t.keep_hi[d] - t.keep_lo[d] for t in tiles) for d in range(3)]
+    return lo, hi, olo, ohi
+
+
+def rank_tiles(grid: TileGrid, world: int, rank: int):
+    """The contiguous block of tiles rank ``rank`` of ``world`` runs."""
+    return [grid.tiles[i] for i in partition(len(grid.tiles), world, rank)]
+
+
+def gather_volume(out_slab, grid: TileGrid, rank: int, world: int, dist, full=None):
+    """Assemble the output volume on rank 0 from every rank's output slab
+    (the region ``slab_bounds(rank_tiles(...))`` of each rank) over
+    torch.distributed point-to-point: NCCL between GPUs, or gloo (host
+    tensors).  Each tile's kept window is copied out of its owner's slab, so
+    any partition assembles every output voxel exactly once, also when a
+    rank's block is not whole x-rows and its bounding box holds voxels it
+    never wrote.  Returns the (batch, fmaps, X, Y, Z) volume on rank 0 (in
+    ``full`` when given), None elsewhere.  This is the only exchange of a
+    multi-GPU run (patches are independent)."""
+    import torch
+    host_only = dist.get_backend() == "gloo"
+    if rank != 0:
+        mine = out_slab.contiguous()
+        dist.send(mine.cpu() if host_only else mine, dst=0)
+        return None
+    if full is None:
+        full = torch.empty(tuple(out_slab.shape[:2]) + tuple(grid.volume_out),
+                           dtype=out_slab.dtype, device=out_slab.device)
+    for r in range(world):
+        tiles = rank_tiles(grid, world, r)
+        if not tiles:
+            continue
+        _, _, olo, ohi = slab_bounds(grid, tiles)
+        if r == 0:
+            src = out_slab
+        else:
+            shape = tuple(out_slab.shape[:2]) + tuple(b - a for a, b in zip(olo, ohi))
+            buf = torch.empty(shape, dtype=out_slab.dtype,
+                              device="cpu" if host_only else out_slab.device)
+            dist.recv(buf, src=r)
+            src = buf.to(full.device)
+        for t in tiles:
+            win = tuple(slice(o - l, o - l + (e - a)) for o, l, a, e in
+                        zip(t.out_lo, olo, t.keep_lo, t.keep_hi))
+            full[(slice(None), slice(None)) + t.out_window].copy_(
+                src[(slice(None), slice(None)) + win])
+    return full
+
+
 class DeviceTiler:
     """Runs blocks of tiles of one grid on one GPU.
 
@@ -193,11 +248,7 @@ class DeviceTiler:
 
     # ------------------------------------------------------------ geometry
     def slab_bounds(self, tiles):
-        lo = [min(t.in_lo[d] for t in tiles) for d in range(3)]
-        hi = [max(t.in_lo[d] + self.grid.patch_in[d] for t in tiles) for d in range(3)]
-        olo = [min(t.out_lo[d] for t in tiles) for d in range(3)]
-        ohi = [max(t.out_lo[d] + t.keep_hi[d] - t.keep_lo[d] for t in tiles) for d in range(3)]
-        return lo, hi, olo, ohi
+        return slab_bounds(self.grid, tiles)
 
     @staticmethod
     def rows(tiles):
@@ -387,10 +438,12 @@ _TILER_CACHE: dict = {}
 _TILER_LOCK = threading.Lock()
 
 
-def device_tiler(plan, grid: TileGrid, device, backend=None) -> DeviceTiler:
-    """A cached DeviceTiler per (plan, grid, device, backend, batching knobs):
-    repeated run_tiled calls reuse bound runners and captured graphs."""
-    key = (id(plan), grid.patch_in, grid.volume_in, grid.overlap, str(device), repr(backend),
+def device_tiler(plan, grid: TileGrid, device, backend=None, slot=0) -> DeviceTiler:
+    """A cached DeviceTiler per (plan, grid, device, worker slot, backend,
+    batching knobs): repeated run_tiled calls reuse bound runners and
+    captured graphs; two workers on the same device get separate tilers."""
+    key = (id(plan), grid.patch_in, grid.volume_in, grid.overlap, str(device), int(slot),
+           repr(backend),
            os.environ.get("VOXPLAN_PATCH_BATCH", "4"), os.environ.get("VOXPLAN_STREAMS", "2"))
     with _TILER_LOCK:
         hit = _TILER_CACHE.get(key)
@@ -445,7 +498,7 @@ def run_tiled(plan, volume, *, overlap=None, backend=None, workers=None, grid=No
         try:
             if not blocks[r]:
                 return
-            dt = device_tiler(plan, grid, devices[r], backend)
+            dt = device_tiler(plan, grid, devices[r], backend, slot=r)
             dt.run_host(volume, out, blocks[r])
         except Exception as exc:  # surfaced below
             errors.append(exc)

@@ -200,3 +200,58 @@ def test_two_rank_tile_partition_gloo():
         p.join(timeout=60)
     assert total == 128 * 1024 * 1024
     assert mx == 2.0
+
+
+def _gather_main(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = tiling.plan_tiles((22, 30, 27), (8, 12, 11), (6, 10, 9), (4, 4, 4))
+    mine = tiling.rank_tiles(g, world, rank)
+    lo, hi, olo, ohi = tiling.slab_bounds(g, mine)
+    slab = torch.full((1, 2) + tuple(b - a for a, b in zip(olo, ohi)), float("nan"),
+                      dtype=torch.float64)
+    for t in mine:        # what a tile's run would write: a code of the global voxel
+        for d in range(3):
+            assert lo[d] <= t.in_lo[d] and t.in_lo[d] + g.patch_in[d] <= hi[d]
+        w = [np.arange(o, o + (e - a)) for o, a, e in zip(t.out_lo, t.keep_lo, t.keep_hi)]
+        code = (w[0][:, None, None] * 10000 + w[1][None, :, None] * 100 + w[2][None, None, :])
+        loc = tuple(slice(o - l, o - l + len(v)) for o, l, v in zip(t.out_lo, olo, w))
+        for c in range(2):
+            slab[(0, c) + loc] = torch.from_numpy(code + c * 1e6)
+    full = tiling.gather_volume(slab, g, rank, world, dist)
+    if rank == 0:
+        q.put(full.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gather_volume_gloo_assembles_exactly_once(world):
+    """Ranks own contiguous tile blocks (split mid x-row for these grids);
+    rank 0's gather must place every tile's kept window, never a neighbour's
+    unwritten bounding-box voxels (tiling.gather_volume)."""
+    import multiprocessing as mp
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gather_main, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    full = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = tiling.plan_tiles((22, 30, 27), (8, 12, 11), (6, 10, 9), (4, 4, 4))
+    assert len(g.tiles) % world != 0 or any(
+        len({t.in_lo[0] for t in tiling.rank_tiles(g, world, r)}) > 1 for r in range(world))
+    X, Y, Z = g.volume_out
+    want = (np.arange(X)[:, None, None] * 10000 + np.arange(Y)[None, :, None] * 100
+            + np.arange(Z)[None, None, :])
+    assert full.shape == (1, 2, X, Y, Z)
+    assert not np.isnan(full).any()
+    np.testing.assert_array_equal(full[0, 0], want)
+    np.testing.assert_array_equal(full[0, 1], want + 1e6)
