@@ -1145,43 +1145,91 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
         // fused 1x1x1 head: this warp takes whole slices (every column item
         // of a slice), so each thread holds all fmaps of its voxel; the
         // activated values feed head_cout dot products and are never stored
+        // Items run slice-major per warp (every column item of a slice in a
+        // row, so the head sums stay in registers) through the same software
+        // pipeline as the plain epilogue: the TMEM load of the next item and
+        // the residual loads two items ahead are in flight while an item is
+        // finished.
+        const EpiView &hv = p.head_out;
+        float hsum[4] = {0.f, 0.f, 0.f, 0.f};
+        auto adv = [&](int &s_, int &c_) {
+          if (++c_ == col_items) {
+            c_ = 0;
+            s_ += NSUB;
+          }
+        };
+        auto head_item = [&](int s_, int c_, const uint32_t (&rv)[16], const float (&bq)[16]) {
+          const int col = tc.nt * p.nt + c_ * 16;
+#pragma unroll
+          for (int i4 = 0; i4 < 4; ++i4) {
+            const float4 b4 = *reinterpret_cast<const float4 *>(s_bias + col + 4 * i4);
+            const float4 c4 = *reinterpret_cast<const float4 *>(s_scale + col + 4 * i4);
+            const float bb[4] = {b4.x, b4.y, b4.z, b4.w}, sc[4] = {c4.x, c4.y, c4.z, c4.w};
+            float r[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int i = 4 * i4 + e;
+              r[e] = __uint_as_float(rv[i]) + bb[e];
+              if (BASE) r[e] = fmaf(sc[e], bq[i], r[e]);
+              if (act == VXB_ACT_RELU) r[e] = fmaxf(r[e], 0.f);
+              else if (act == VXB_ACT_ELU) r[e] = fast_elu(r[e], p.alpha);
+              else if (act == VXB_ACT_SIGMOID) r[e] = fast_sigmoid(r[e]);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 h4 = *reinterpret_cast<const float4 *>(s_head + j * cpad + col + 4 * i4);
+              hsum[j] = fmaf(r[0], h4.x, hsum[j]);
+              hsum[j] = fmaf(r[1], h4.y, hsum[j]);
+              hsum[j] = fmaf(r[2], h4.z, hsum[j]);
+              hsum[j] = fmaf(r[3], h4.w, hsum[j]);
+            }
+          }
+          if (c_ == col_items - 1) {
+            const int x = sc0 + s_;
+            if (yz_ok && x < slim) {
+              float *op = static_cast<float *>(hv.data) + tc.b * hv.s[0] + rc * hv.s[ra_dim] +
+                          z * hv.s[4] + x * hv.s[sl_dim];
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                if (j < p.head_cout)
+                  op[j * hv.s[1]] = apply_act(hsum[j] + p.head_b[j], p.head_act, p.head_alpha);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) hsum[j] = 0.f;
+          }
+        };
+        uint32_t ra[16], rb[16];
+        uint4 qa[2], qb[2];
+        float bq[16];
+        int s0 = sub, c0 = 0, s1 = sub, c1 = 0;   // items A (s0, c0) and B (s1, c1)
+        adv(s1, c1);
+        if (braw) {
+          if (s0 < p.bx) base_issue(s0 * col_items + c0, qa);
+          if (s1 < p.bx) base_issue(s1 * col_items + c1, qb);
+        }
         mbar_wait_sleep(&t_full[acc], ((p.acc_stages == 2 ? (it >> 1) : it) & 1));
         tc_fence_after();
-        const EpiView &hv = p.head_out;
-        for (int s = sub; s < p.bx; s += NSUB) {
-          float hsum[4] = {0.f, 0.f, 0.f, 0.f};
-          const int x = sc0 + s;
-          for (int ci = 0; ci < col_items; ++ci) {
-            const int item = s * col_items + ci;
-            uint32_t rv[16];
-            tmem_ld16_issue(taddr_of(item), rv);
-            float bq[16];
-            if (BASE) {
-              uint4 qd[2];
-              if (braw) base_issue(item, qd);
-              base_get(item, qd, bq);
-            }
-            tmem_wait_ld16(rv);
-            const int col = tc.nt * p.nt + ci * 16;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              float r = __uint_as_float(rv[i]) + s_bias[col + i];
-              if (BASE) r = fmaf(s_scale[col + i], bq[i], r);
-              if (act == VXB_ACT_RELU) r = fmaxf(r, 0.f);
-              else if (act == VXB_ACT_ELU) r = fast_elu(r, p.alpha);
-              else if (act == VXB_ACT_SIGMOID) r = fast_sigmoid(r);
-#pragma unroll
-              for (int j = 0; j < 4; ++j) hsum[j] = fmaf(r, s_head[j * cpad + col + i], hsum[j]);
-            }
-          }
-          if (yz_ok && x < slim) {
-            float *op = static_cast<float *>(hv.data) + tc.b * hv.s[0] + rc * hv.s[ra_dim] +
-                        z * hv.s[4] + x * hv.s[sl_dim];
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (j < p.head_cout) op[j * hv.s[1]] = apply_act(hsum[j] + p.head_b[j], p.head_act,
-                                                               p.head_alpha);
-          }
+        if (s0 < p.bx) tmem_ld16_issue(taddr_of(s0 * col_items + c0), ra);
+        while (s0 < p.bx) {
+          tmem_wait_ld16(ra);
+          if (s1 < p.bx) tmem_ld16_issue(taddr_of(s1 * col_items + c1), rb);
+          if (BASE) base_get(s0 * col_items + c0, qa, bq);
+          head_item(s0, c0, ra, bq);
+          int s2 = s1, c2 = c1;                      // next A
+          adv(s2, c2);
+          if (braw && s2 < p.bx) base_issue(s2 * col_items + c2, qa);
+          if (s1 >= p.bx) break;
+          tmem_wait_ld16(rb);
+          if (s2 < p.bx) tmem_ld16_issue(taddr_of(s2 * col_items + c2), ra);
+          if (BASE) base_get(s1 * col_items + c1, qb, bq);
+          head_item(s1, c1, rb, bq);
+          int s3 = s2, c3 = c2;                      // next B
+          adv(s3, c3);
+          if (braw && s3 < p.bx) base_issue(s3 * col_items + c3, qb);
+          s0 = s2;
+          c0 = c2;
+          s1 = s3;
+          c1 = c3;
         }
         tc_fence_before();
         __syncwarp();

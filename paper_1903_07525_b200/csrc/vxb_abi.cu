@@ -286,8 +286,8 @@ static int tc_tmem_cols(int bx, int nt, int acc, bool fold_pair) {
 // can_pair: the conv may run as CTA pairs (pair_mode 1: always, 2: only with
 // streamed weights); fold_pair: it is a folded conv that pairs (TMEM layout)
 static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, long long other_tiles,
-                        int sms, int reps, int reserved, bool can_pair, int pair_mode,
-                        bool fold_pair, TcConfig &c) {
+                        int sms, int reps, int reserved, bool f32in, bool can_pair,
+                        int pair_mode, bool fold_pair, TcConfig &c) {
   // room for bias/scale/barriers, plus the fp32-input staging ring if any
   const int budget = 227 * 1024 - 6144 - reserved;
   c.acc = env_int("VXB_TC_ACC", 2);
@@ -326,7 +326,7 @@ static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, lon
   }
   const int slab = L.slab;
   // fp32-input convs buffer their input in the staging ring: two A stages
-  int na_cap = reserved ? std::max(2, std::min(4, env_int("VXB_TC_F32IN_NA", 2)))
+  int na_cap = f32in ? std::max(2, std::min(4, env_int("VXB_TC_F32IN_NA", 2)))
                         : std::max(2, std::min(6, env_int("VXB_TC_NA", 3)));
   for (;;) {
     const int sx = L.fold == 2 ? TILE_Y : c.bx, sy = L.fold == 2 ? c.bx : TILE_Y;
@@ -558,7 +558,7 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
   // a fused head keeps its weights in smem: 4 rows x the padded fmaps
   const int head_smem = a.head_cout ? 4 * L.n_tiles * L.nt * 4 : 0;
   int rc = tc_configure(L, a.k, slice_y ? a.oy : a.ox, other_tiles, sms, a.reps,
-                        stg_bytes + head_smem, can_pair && !(fold_pair && a.head_cout), pair_env,
+                        stg_bytes + head_smem, f32in, can_pair && !(fold_pair && a.head_cout), pair_env,
                         fold_pair && !a.head_cout, c);
   if (rc) return rc;
   TcParams p;
