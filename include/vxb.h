@@ -191,6 +191,10 @@ int vxb_conv_select(int cin, int cout, const int k[3], const int stride[3]);
  * reference makes once per bind (kernels_cy.py:22-27 lane-kernel cache). */
 int vxb_conv_select_shape(int cin, int cout, const int k[3], const int stride[3],
                           const int out_xyz[3]);
+/* as vxb_conv_select_shape for a launch over `batch` volumes of that extent
+ * (the N-tile split counts the tiles of every batch entry) */
+int vxb_conv_select_shape_b(int cin, int cout, const int k[3], const int stride[3],
+                            const int out_xyz[3], int batch);
 /* bytes of the packed weight image for a conv of this geometry */
 size_t vxb_conv_weights_bytes(int cin, int cout, const int k[3], const int stride[3],
                               int path);

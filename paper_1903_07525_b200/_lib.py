@@ -109,6 +109,7 @@ SIGNATURES = [
     ("vxb_debug_read", c_size_t, [c_void_p, c_size_t]),
     ("vxb_conv_select", c_int, [c_int, c_int, I3, I3]),
     ("vxb_conv_select_shape", c_int, [c_int, c_int, I3, I3, I3]),
+    ("vxb_conv_select_shape_b", c_int, [c_int, c_int, I3, I3, I3, c_int]),
     ("vxb_conv_weights_bytes", c_size_t, [c_int, c_int, I3, I3, c_int]),
     ("vxb_conv_pack_weights", c_int, [c_void_p, c_int, c_int, I3, I3, c_int, c_void_p, c_size_t]),
     ("vxb_conv_weights_bytes2", c_size_t, [c_int, c_int, c_int, I3, I3, c_int]),

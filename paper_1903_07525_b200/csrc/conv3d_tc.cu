@@ -259,9 +259,19 @@ __host__ __device__ constexpr int tc_threads(bool f32in) {
   return 96 + 32 * epi_warps(f32in) + (f32in ? 32 * CVT_WARPS : 0);
 }
 
+// Lean epilogue (bf16 blocked output, optional bf16 blocked residual): per
+// 16-column item of a tile, the element offsets of its two 8-fmap halves
+// relative to the thread's row in slice 0 of the tile (output and residual)
+// and its first channel within the N tile, built once per CTA.
+struct LeanEnt {
+  long long o0, o1, b0, b1;
+  int ch, pad;
+};
+constexpr int LEAN_TAB = 16;   // nt <= 256: <= 16 column items
+
 // Byte offsets inside the dynamic smem block (all derivable from p).
 struct SmemMap {
-  uint32_t a, b, stg, bias, scale, head, bars;
+  uint32_t a, b, stg, bias, scale, head, ltab, bars;
 };
 __host__ __device__ inline SmemMap smem_map(const TcParams &p) {
   SmemMap m;
@@ -272,7 +282,8 @@ __host__ __device__ inline SmemMap smem_map(const TcParams &p) {
   const uint32_t cpad = p.n_tiles * p.nt;
   m.scale = m.bias + cpad * 4;
   m.head = m.scale + cpad * 4;                 // fused head weights [head_cout][cpad]
-  m.bars = (m.head + (p.head_cout > 0 ? 4 * cpad * 4 : 0) + 15) & ~15u;
+  m.ltab = (m.head + (p.head_cout > 0 ? 4 * cpad * 4 : 0) + 15) & ~15u;
+  m.bars = m.ltab + (p.lean ? LEAN_TAB * sizeof(LeanEnt) : 0);
   return m;
 }
 
@@ -491,7 +502,7 @@ __device__ __forceinline__ void mma_group_fold_pair(
 }
 
 template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN, bool POOL = false,
-          bool HEAD = false>
+          bool HEAD = false, bool LEAN = false>
 __global__ void __maxnreg__(VXB_TC_MAXNREG)
     conv3d_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -544,10 +555,39 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
     }
   const int cpad = p.n_tiles * p.nt;
   for (int c = threadIdx.x; c < cpad; c += blockDim.x) {
-    const int cr = p.rep_n ? c % p.rep_n : c;   // taps in N: column -> channel of its tap
+    // taps in N: column -> channel of its tap (z-pair order: see TcParams::zpair)
+    int cr = c;
+    if (p.rep_n) {
+      const int rem = p.zpair ? c % (2 * p.rep_n) : c % p.rep_n;
+      cr = p.zpair ? ((rem >> 4) << 3) + (rem & 7) : rem;
+    }
     s_bias[c] = cr < p.cout ? p.bias[cr] : 0.f;
     s_scale[c] = (cr < p.cout && p.scale) ? p.scale[cr] : 1.f;
   }
+  LeanEnt *ltab = reinterpret_cast<LeanEnt *>(smem + sm.ltab);
+  if (LEAN)
+    for (int ci = threadIdx.x; ci < (p.nt >> 4); ci += blockDim.x) {
+      const int cc = ci << 4;
+      int rep = 0, ch = cc;
+      if (p.zpair) {
+        const int rp = cc / (2 * p.rep_n), rem = cc - rp * 2 * p.rep_n;
+        rep = 2 * rp;
+        ch = (rem >> 4) << 3;
+      } else if (p.rep_n) {
+        rep = cc / p.rep_n;
+        ch = cc - rep * p.rep_n;
+      }
+      const long long oc = static_cast<long long>(ch >> 3) * p.out.s[1];
+      const long long bc = static_cast<long long>(ch >> 3) * p.base.s[1];
+      LeanEnt e;
+      e.o0 = (p.rep_n ? p.out_rep_off[rep] : 0) + oc;
+      e.o1 = p.zpair ? p.out_rep_off[rep + 1] + oc : e.o0 + p.out.s[1];
+      e.b0 = (p.rep_n ? p.base_rep_off[rep] : 0) + bc;
+      e.b1 = p.zpair ? p.base_rep_off[rep + 1] + bc : e.b0 + p.base.s[1];
+      e.ch = ch;
+      e.pad = 0;
+      ltab[ci] = e;
+    }
   if (HEAD)
     for (int i = threadIdx.x; i < 4 * cpad; i += blockDim.x) {
       const int j = i / cpad, c = i - j * cpad;
@@ -967,8 +1007,14 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       const long long orow = tc.b * ov.s[0] + rc * ov.s[ra_dim] + z * ov.s[4];
       const long long brow = tc.b * bvw.s[0] + rc * bvw.s[ra_dim] + z * bvw.s[4];
       // item column -> (replica, first channel of the item)
+      // (z-pair order: rep is the item's dz = 0 tap, its second half is rep + 1
+      // at the same channels)
       auto item_rep = [&](int cc, int &rep, int &ch) {
-        if (p.rep_n) {
+        if (p.zpair) {
+          const int rp = cc / (2 * p.rep_n), rem = cc - rp * 2 * p.rep_n;
+          rep = 2 * rp;
+          ch = (rem >> 4) << 3;
+        } else if (p.rep_n) {
           rep = cc / p.rep_n;
           ch = cc - rep * p.rep_n;
         } else {
@@ -978,6 +1024,19 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       };
       const uint32_t tbase =
           tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * acc_stride + p.slice0_col;
+      // lean epilogue: this thread's row in slice 0 of the tile (N tile and
+      // tile replica included); items add the slice and their LeanEnt offsets
+      const int nt0 = tc.nt * p.nt;
+      __nv_bfloat16 *lo_row = nullptr;
+      const __nv_bfloat16 *lb_row = nullptr;
+      if constexpr (LEAN) {
+        lo_row = static_cast<__nv_bfloat16 *>(ov.data) + orow +
+                 (p.rep_n ? 0 : p.out_rep_off[tc.rep]) + sc0 * ov.s[sl_dim] + (nt0 >> 3) * ov.s[1];
+        if (BASE)
+          lb_row = static_cast<const __nv_bfloat16 *>(bvw.data) + brow +
+                   (p.rep_n ? 0 : p.base_rep_off[tc.rep]) + sc0 * bvw.s[sl_dim] +
+                   (nt0 >> 3) * bvw.s[1];
+      }
 
       auto taddr_of = [&](int item) {
         int s, cc;
@@ -988,6 +1047,23 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       // ahead (the first ones before the accumulator is even ready); other
       // layouts are read at use
       auto base_issue = [&](int item, uint4 (&d)[2]) {
+        if constexpr (LEAN) {
+          int s, cc;
+          split_item(item, s, cc);
+          const LeanEnt &e = ltab[cc >> 4];
+          const int c0 = nt0 + e.ch, c1 = p.zpair ? c0 : c0 + 8;
+          d[0] = d[1] = make_uint4(0u, 0u, 0u, 0u);
+          if (yz_ok && sc0 + s < slim) {
+            const __nv_bfloat16 *q = lb_row + s * bvw.s[sl_dim];
+            if (p.zpair_v8) {
+              if (c0 < p.cout) ld_nc_v8(q + e.b0, d[0], d[1]);
+            } else {
+              if (c0 < p.cout) d[0] = __ldg(reinterpret_cast<const uint4 *>(q + e.b0));
+              if (c1 < p.cout) d[1] = __ldg(reinterpret_cast<const uint4 *>(q + e.b1));
+            }
+          }
+          return;
+        }
         int s, cc, rep, ch;
         split_item(item, s, cc);
         item_rep(cc, rep, ch);
@@ -995,6 +1071,21 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
         const bool ok = yz_ok && x < slim;
         const __nv_bfloat16 *bp = static_cast<const __nv_bfloat16 *>(bvw.data) + brow +
                                   p.base_rep_off[rep] + x * bvw.s[sl_dim];
+        if (p.zpair) {
+          // both halves: the same chunk at dz = 0 and dz = 1 (adjacent rows)
+          d[0] = d[1] = make_uint4(0u, 0u, 0u, 0u);
+          if (ok && ch < p.cout) {
+            const __nv_bfloat16 *q = bp + (ch >> 3) * bvw.s[1];
+            if (p.zpair_v8) {
+              ld_nc_v8(q, d[0], d[1]);
+            } else {
+              d[0] = __ldg(reinterpret_cast<const uint4 *>(q));
+              d[1] = __ldg(reinterpret_cast<const uint4 *>(q + p.base_rep_off[rep + 1] -
+                                                              p.base_rep_off[rep]));
+            }
+          }
+          return;
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c0 = ch + h * 8;
@@ -1024,9 +1115,10 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           float t8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          const int c0 = ch + h * 8;
+          const int c0 = p.zpair ? ch : ch + h * 8;
+          const int rp = p.zpair ? rep + h : rep;
           if (ok && c0 < p.cout)
-            load8(bvw, brow + p.base_rep_off[rep] + x * bvw.s[sl_dim] +
+            load8(bvw, brow + p.base_rep_off[rp] + x * bvw.s[sl_dim] +
                            (bvw.blocked ? (c0 >> 3) * bvw.s[1] : c0 * bvw.s[1]),
                   bvw.blocked, t8);
 #pragma unroll
@@ -1034,16 +1126,64 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
         }
       };
       auto finish = [&](int item, const uint32_t (&rv)[16], const float (&bv)[16]) {
+        if constexpr (LEAN) {
+          // bias (+ scale . residual), activation, bf16 pack, two 16-byte
+          // stores (or one 32-byte store for z-paired deconv taps)
+          int s, cc;
+          split_item(item, s, cc);
+          const LeanEnt &e = ltab[cc >> 4];
+          const int c0 = nt0 + e.ch, c1 = p.zpair ? c0 : c0 + 8;
+          const int col = nt0 + cc;
+          uint32_t w[8];
+#pragma unroll
+          for (int i4 = 0; i4 < 4; ++i4) {
+            const float4 b4 = *reinterpret_cast<const float4 *>(s_bias + col + 4 * i4);
+            float r[4] = {__uint_as_float(rv[4 * i4]) + b4.x, __uint_as_float(rv[4 * i4 + 1]) + b4.y,
+                          __uint_as_float(rv[4 * i4 + 2]) + b4.z,
+                          __uint_as_float(rv[4 * i4 + 3]) + b4.w};
+            if (BASE) {
+              const float4 c4 = *reinterpret_cast<const float4 *>(s_scale + col + 4 * i4);
+              r[0] = fmaf(c4.x, bv[4 * i4], r[0]);
+              r[1] = fmaf(c4.y, bv[4 * i4 + 1], r[1]);
+              r[2] = fmaf(c4.z, bv[4 * i4 + 2], r[2]);
+              r[3] = fmaf(c4.w, bv[4 * i4 + 3], r[3]);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if (ACT == VXB_ACT_RELU) r[i] = fmaxf(r[i], 0.f);
+              else if (ACT == VXB_ACT_ELU) r[i] = fast_elu(r[i], p.alpha);
+            }
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(r[0], r[1]);
+            __nv_bfloat162 h1 = __floats2bfloat162_rn(r[2], r[3]);
+            w[2 * i4] = *reinterpret_cast<uint32_t *>(&h0);
+            w[2 * i4 + 1] = *reinterpret_cast<uint32_t *>(&h1);
+          }
+          if (yz_ok && sc0 + s < slim) {
+            __nv_bfloat16 *o = lo_row + s * ov.s[sl_dim];
+            if (p.zpair_v8) {
+              if (c0 < p.cout) st_v8(o + e.o0, w);
+            } else {
+              if (c0 < p.cout)
+                *reinterpret_cast<uint4 *>(o + e.o0) = make_uint4(w[0], w[1], w[2], w[3]);
+              if (c1 < p.cout)
+                *reinterpret_cast<uint4 *>(o + e.o1) = make_uint4(w[4], w[5], w[6], w[7]);
+            }
+          }
+          return;
+        }
         int s, cc, rep, ch;
         split_item(item, s, cc);
         item_rep(cc, rep, ch);
         const int x = sc0 + s;
         const bool valid = yz_ok && x < slim;   // stores only; all lanes run the math
-        const long long obase = orow + p.out_rep_off[rep] + x * ov.s[sl_dim];
+        const long long obase0 = orow + p.out_rep_off[rep] + x * ov.s[sl_dim];
+        uint32_t zp_w[8];                       // z-pair: both halves, one 32-byte store
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int c0 = ch + h * 8;                       // output channel
+          const int c0 = p.zpair ? ch : ch + h * 8;        // output channel
           const int col = tc.nt * p.nt + cc + h * 8;       // bias / scale column
+          const long long obase =
+              p.zpair && h ? orow + p.out_rep_off[rep + 1] + x * ov.s[sl_dim] : obase0;
           if (c0 >= p.cout) break;
           const int nvalid = min(8, p.cout - c0);
           const float4 b0 = *reinterpret_cast<const float4 *>(s_bias + col);
@@ -1116,7 +1256,15 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
                                          (c0 >> 3) * pv.s[1]) = make_uint4(w[0], w[1], w[2], w[3]);
             }
           } else if (FASTOUT) {
-            if (ov.blocked) {
+            if (p.zpair_v8) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(r[2 * i], r[2 * i + 1]);
+                zp_w[4 * h + i] = *reinterpret_cast<uint32_t *>(&h2);
+              }
+              if (h == 1 && valid)
+                st_v8(static_cast<__nv_bfloat16 *>(ov.data) + obase0 + (c0 >> 3) * ov.s[1], zp_w);
+            } else if (ov.blocked) {
               if (valid && !(p.dbg_mode & 512)) {
                 if (ov.dtype == VXB_BF16X2)
                   store8_split(ov, obase + (c0 >> 3) * ov.s[1], r);
@@ -1297,10 +1445,10 @@ size_t tc_smem_bytes(const TcParams &p) {
 }
 
 template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN = false, bool POOL = false,
-          bool HEAD = false>
+          bool HEAD = false, bool LEAN = false>
 static int launch_variant(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t stream,
                           size_t smem) {
-  auto kern = conv3d_tc_kernel<ACT, FASTOUT, BASE, PAIR, F32IN, POOL, HEAD>;
+  auto kern = conv3d_tc_kernel<ACT, FASTOUT, BASE, PAIR, F32IN, POOL, HEAD, LEAN>;
   if (int rc = ensure_smem_attr(kern, 232448, "cudaFuncSetAttribute(conv3d_tc)")) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1371,6 +1519,23 @@ static int launch_act(const TcParams &p, const TcMaps &maps, int grid, cudaStrea
   if (!fast) {
     if (PAIR) return set_error(VXB_EUNSUPPORTED, "pair mode needs a blocked bf16 output");
     return launch_variant<-1, false, BASE, false>(p, maps, grid, s, smem);
+  }
+  if (p.lean) {
+    // bf16 blocked output (and residual): the lean epilogue (tc_lean_ok)
+    switch (p.act) {
+      case VXB_ACT_RELU:
+        return launch_variant<VXB_ACT_RELU, true, BASE, PAIR, false, false, false, true>(p, maps,
+                                                                                          grid, s,
+                                                                                          smem);
+      case VXB_ACT_ELU:
+        return launch_variant<VXB_ACT_ELU, true, BASE, PAIR, false, false, false, true>(p, maps,
+                                                                                         grid, s,
+                                                                                         smem);
+      default:
+        return launch_variant<VXB_ACT_NONE, true, BASE, PAIR, false, false, false, true>(p, maps,
+                                                                                          grid, s,
+                                                                                          smem);
+    }
   }
   switch (p.act) {
     case VXB_ACT_RELU:

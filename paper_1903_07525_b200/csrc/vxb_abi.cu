@@ -475,6 +475,7 @@ struct TcLaunch {
   int ox, oy, oz, nb;
   int reps;
   int rep_n;        // > 0: the reps ride in N (rep_n columns each), one tile computes all
+  int zpair;        // rep_n layout with the dz = 0 / 1 taps interleaved per 8-fmap chunk
   long long out_rep_off[MAX_REPS], base_rep_off[MAX_REPS];
   EpiView out, base;
   int has_base;
@@ -705,6 +706,22 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
     p.base_rep_off[r] = a.base_rep_off[r];
   }
   p.rep_n = a.rep_n;
+  p.zpair = a.zpair;
+  if (a.zpair) {
+    // 32-byte stores / residual loads need the dz = 0 row 32-byte aligned:
+    // every offset of a dz = 0 row is a multiple of 16 elements
+    auto al32 = [&](const EpiView &v, const long long *roff) {
+      if (!v.data) return true;
+      if (v.dtype != VXB_BF16 || !v.blocked || (reinterpret_cast<uintptr_t>(v.data) & 31)) return false;
+      for (int i = 0; i < 5; ++i)
+        if (i != 4 && v.s[i] % 16) return false;
+      if (v.s[4] != 16) return false;
+      for (int r = 0; r < a.reps; r += 2)
+        if (roff[r] % 16 || roff[r + 1] != roff[r] + 8) return false;
+      return true;
+    };
+    p.zpair_v8 = al32(a.out, a.out_rep_off) && (!a.has_base || al32(a.base, a.base_rep_off));
+  }
   (void)rep_offsets;
   p.head_w = a.head_w;
   p.head_b = a.head_b;
@@ -715,6 +732,12 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
   p.cout = a.cout;
   p.act = a.act;
   p.alpha = a.alpha;
+  // lean epilogue (conv3d_tc.cu LeanEnt): the common bf16 blocked case
+  p.lean = env_int("VXB_TC_LEAN", 1) && !f32in && !p.pool && !a.head_cout &&
+           a.out.dtype == VXB_BF16 && a.out.blocked &&
+           (!a.has_base || (a.base.dtype == VXB_BF16 && a.base.blocked)) &&
+           (a.act == VXB_ACT_NONE || a.act == VXB_ACT_RELU || a.act == VXB_ACT_ELU) &&
+           L.nt <= 256;
   p.dbg_mode = env_int("VXB_TC_DBGMODE", 0);
   if (env_int("VXB_TC_DEBUG", 0)) {
     if (!g_dbg) {
@@ -807,6 +830,11 @@ static int device_sms_or(int fallback) {
 
 int vxb_conv_select_shape(int cin, int cout, const int k[3], const int stride[3],
                           const int out_xyz[3]) {
+  return vxb_conv_select_shape_b(cin, cout, k, stride, out_xyz, 1);
+}
+
+int vxb_conv_select_shape_b(int cin, int cout, const int k[3], const int stride[3],
+                            const int out_xyz[3], int batch) {
   int path = vxb_conv_select(cin, cout, k, stride);
   if (path != VXB_PATH_TC || !out_xyz) return path;
   const TcLayout L = tc_layout(cin, 0, cout, k);
@@ -818,8 +846,13 @@ int vxb_conv_select_shape(int cin, int cout, const int k[3], const int stride[3]
   // re-reads the (small, L2-resident) input.  Take the widest N tile that
   // gives one tile per SM.
   const int sms = std::max(1, device_sms_or(148));
+  // (all batch entries count: a rebatched plan runs several patches per
+  // launch.  The N split never changes a result -- every output column
+  // accumulates the same K steps in the same order -- so batch-1 and
+  // batch-B runs stay bit-identical; config 5 at 12 patches per launch:
+  // 80 -> 80 3x3x3 unsplit 24 us vs 45 us in N tiles of 32, tools/conv_sweep.py)
   const long long sp = static_cast<long long>(out_xyz[0]) * ceil_div(out_xyz[1], TILE_Y) *
-                       ceil_div(out_xyz[2], TILE_Z);
+                       ceil_div(out_xyz[2], TILE_Z) * std::max(1, batch);
   if (sp * L.n_tiles >= sms) return path;
   if (L.npad > 128) {
     // wide layers (CTA-pair MMAs when unsplit): the widest split that fills
@@ -1154,6 +1187,16 @@ static int deconv_rep_n(int cout, const int k[3], const int stride[3], int path)
   return ntr;
 }
 
+// z-pair column order for taps in N with a z stride of 2 (config 5's 1x2x2
+// deconvs): column n of tap r, fmap co is
+//   (r / 2) * 2 rn + (co / 8) * 16 + (r % 2) * 8 + co % 8,
+// so a 16-column epilogue item holds one 8-fmap chunk at dz = 0 and dz = 1,
+// whose outputs are adjacent 16-byte rows (one 32-byte store instead of two
+// half-sector writes 32 bytes apart)
+static bool deconv_zpair(int rep_n, const int k[3], const int stride[3]) {
+  return rep_n > 0 && k[2] == 2 && stride[2] == 2 && env_int("VXB_DECONV_ZPAIR", 1);
+}
+
 // K segments of a tensor-core deconv's 1x1x1 GEMM: the input fmaps, or the
 // two x3 segments over a split input
 static void deconv_segments(int cin, int prec, int &c0, int &c1) {
@@ -1205,8 +1248,14 @@ int vxb_deconv_pack_weights3(const float *w, int cin, int cout, const int k[3],
     // column co' = tap * rn + co, taps in (dx, dy, dz) order
     const int reps = k[0] * k[1] * k[2];
     TcLayout L = tc_layout(c0, c1, reps * rn, one);
+    const bool zp = deconv_zpair(rn, k, stride);
     auto wtap = [&](int cop, int ci, int, int, int) {
-      const int r = cop / rn, co = cop - r * rn;
+      int r = cop / rn, co = cop - r * rn;
+      if (zp) {
+        const int rp = cop / (2 * rn), rem = cop - rp * 2 * rn;
+        r = 2 * rp + ((rem >> 3) & 1);
+        co = ((rem >> 4) << 3) + (rem & 7);
+      }
       if (co >= cout) return 0.f;
       const int dz = r % k[2], dy = (r / k[2]) % k[1], dx = r / (k[2] * k[1]);
       return wk(co, ci, dx, dy, dz);
@@ -1276,6 +1325,7 @@ int vxb_deconv3d(const vxb_deconv_desc *d, void *stream) {
     a.nb = d->in.n;
     a.reps = d->k[0] * d->k[1] * d->k[2];
     a.rep_n = deconv_rep_n(d->cout, d->k, d->stride, d->path);
+    a.zpair = deconv_zpair(a.rep_n, d->k, d->stride);
     a.out = to_epi(d->out);
     for (int i = 0; i < 3; ++i) a.out.s[2 + i] = d->out.s[2 + i] * d->stride[i];
     a.has_base = additive;

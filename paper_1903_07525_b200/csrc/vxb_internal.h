@@ -80,6 +80,12 @@ struct TcParams {
   EpiView out, base;
   long long out_rep_off[MAX_REPS], base_rep_off[MAX_REPS];
   int rep_n;                   // deconv taps in N: columns per tap (0 = taps are tile replicas)
+  int zpair;                   // taps in N with z-stride 2: the dz = 0 / 1 taps of each 8-fmap
+                               // chunk are adjacent 8-column halves of one 16-column item
+                               // (their output rows are adjacent: one 32-byte store)
+  int zpair_v8;                // zpair outputs (and residuals) moved as 32-byte accesses
+  int lean;                    // lean epilogue: bf16 blocked output, bf16 blocked residual if
+                               // any, act none / relu / elu, no pooling / head / fp32 input
   int cout, act;
   float alpha;
   int has_base;

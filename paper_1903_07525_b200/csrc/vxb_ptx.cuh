@@ -563,3 +563,19 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
 }
 
 }  // namespace vxb
+
+// 32-byte global accesses (sm_100: LDG/STG .256); the address must be
+// 32-byte aligned
+namespace vxb {
+__device__ __forceinline__ void ld_nc_v8(const void *p, uint4 &a, uint4 &b) {
+  asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z),
+                 "=r"(b.w)
+               : "l"(p));
+}
+__device__ __forceinline__ void st_v8(void *p, const uint32_t (&w)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w[0]), "r"(w[1]),
+               "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
+}
+}  // namespace vxb

@@ -58,10 +58,11 @@ PRECISIONS = {"bf16": _lib.PREC_BF16, "x3": _lib.PREC_X3}
 
 
 def pack_conv(kernel, bias, *, stride=(1, 1, 1), base_scale=None, cin_split=None,
-              path=0, out_shape=None, device=None, precision="bf16") -> PackedConv:
+              path=0, out_shape=None, batch=1, device=None, precision="bf16") -> PackedConv:
     """Pack a standard (cout, cin, kx, ky, kz) fp32 kernel bank for vxb_conv3d.
     ``out_shape`` (x, y, z) of the output, when known, lets the library pick
-    the tile layout (vxb_conv_select_shape).  ``precision="x3"`` packs for a
+    the tile layout (vxb_conv_select_shape_b, ``batch`` volumes per launch).
+    ``precision="x3"`` packs for a
     split-bf16 input: bf16(W) against its hi and lo planes and
     bf16(W - bf16(W)) against hi (VXB_PREC_X3)."""
     import torch
@@ -76,8 +77,8 @@ def pack_conv(kernel, bias, *, stride=(1, 1, 1), base_scale=None, cin_split=None
     stride = tuple(int(s) for s in stride)
     if path == 0:
         if out_shape is not None:
-            path = L.vxb_conv_select_shape(cin, cout, _lib.i3(k), _lib.i3(stride),
-                                           _lib.i3(tuple(out_shape)))
+            path = L.vxb_conv_select_shape_b(cin, cout, _lib.i3(k), _lib.i3(stride),
+                                             _lib.i3(tuple(out_shape)), int(batch))
         else:
             path = L.vxb_conv_select(cin, cout, _lib.i3(k), _lib.i3(stride))
     if cin1 and path not in _lib.TC_PATHS:

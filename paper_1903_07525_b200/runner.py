@@ -448,7 +448,7 @@ class PlanRunner:
                     a, b, oa, ob = info["segments"]
                     pk = K.pack_conv(kern, w.tensor(st.name, ROLE_BIAS), stride=stride,
                                      base_scale=scale, cin_split=a.dims[1],
-                                     out_shape=tuple(info["out"].dims[2:]), device=dev)
+                                     out_shape=tuple(info["out"].dims[2:]), batch=int(info["out"].dims[0]), device=dev)
                     pool = info["pool_out"].dt if "pool_out" in info else None
                     calls.append(lambda a=a.dt, b=b.dt, pk=pk, out=out, base=base, oa=oa, ob=ob,
                                  act=st.fused_act, pool=pool, hd=hd, hout=hout:
@@ -460,7 +460,7 @@ class PlanRunner:
                     kz_w = np.ascontiguousarray(
                         np.transpose(np.asarray(kern, np.float32)[:, 0], (0, 3, 1, 2))[..., None])
                     pk = K.pack_conv(kz_w, w.tensor(st.name, ROLE_BIAS), stride=stride,
-                                     base_scale=scale, out_shape=tuple(info["out"].dims[2:]),
+                                     base_scale=scale, out_shape=tuple(info["out"].dims[2:]), batch=int(info["out"].dims[0]),
                                      device=dev, precision=self._prec)
                     pool = info["pool_out"].dt if "pool_out" in info else None
                     calls.append(lambda x=xz, pk=pk, out=out, base=base,
@@ -471,7 +471,7 @@ class PlanRunner:
                 else:
                     pk = K.pack_conv(kern, w.tensor(st.name, ROLE_BIAS), stride=stride,
                                      base_scale=scale, path=self._conv_path,
-                                     out_shape=tuple(info["out"].dims[2:]), device=dev,
+                                     out_shape=tuple(info["out"].dims[2:]), batch=int(info["out"].dims[0]), device=dev,
                                      precision=self._prec)
                     x = fused_in.get(id(info), info["x"].dt)
                     if id(info) in fused_in and pk.path not in _lib.TC_PATHS:

@@ -92,6 +92,10 @@ def test_host_packing_sizes_and_selection():
         (_lib.PATH_TC_N128, _lib.PATH_TC_N64)
     assert L.vxb_conv_select_shape(80, 80, k3, s1, _lib.i3((18, 12, 12))) in \
         (_lib.PATH_TC_N64, _lib.PATH_TC_N32, _lib.PATH_TC_N16)
+    # ... unless a launch covers enough batch entries (rebatched patches)
+    assert L.vxb_conv_select_shape_b(80, 80, k3, s1, _lib.i3((18, 12, 12)), 1) == \
+        L.vxb_conv_select_shape(80, 80, k3, s1, _lib.i3((18, 12, 12)))
+    assert L.vxb_conv_select_shape_b(80, 80, k3, s1, _lib.i3((18, 12, 12)), 12) == _lib.PATH_TC
     assert L.vxb_conv_select_shape(128, 128, k3, s1, _lib.i3((32, 128, 128))) == _lib.PATH_TC
     assert L.vxb_conv_weights_bytes(768, 256, k3, s1, _lib.PATH_TC_N64) == \
         L.vxb_conv_weights_bytes(768, 256, k3, s1, _lib.PATH_TC)

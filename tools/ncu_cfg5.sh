@@ -9,3 +9,12 @@ while [ $# -ge 2 ]; do
     -s $1 -c 1 -o $OUT/ncu_$2 -f python tools/cfg5_patch.py > /dev/null 2>&1; echo "full $2 rc=$?"
   shift 2
 done
+# text summaries (the reports themselves can exceed gpurun's 64 MiB return limit)
+for f in $OUT/*.ncu-rep; do
+  b=${f%.ncu-rep}
+  ncu -i $f --page details --csv > $b.details.csv 2>/dev/null
+  ncu -i $f --page raw --csv > $b.raw.csv 2>/dev/null
+  ncu -i $f --page source --csv --print-source cuda > $b.src_cuda.csv 2>/dev/null
+  ncu -i $f --page source --csv --print-source sass > $b.src_sass.csv 2>/dev/null
+  [ -n "${KEEP_REP:-}" ] || rm -f $f
+done
