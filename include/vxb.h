@@ -181,6 +181,11 @@ int vxb_device_sms(void);
  * timestamps (ns, [cta][tile<64][8]) of its last launch; copies up to count */
 size_t vxb_debug_read(unsigned long long *host, size_t count);
 
+/* launches from the calling host thread use programmatic dependent launch
+ * (mode 1), plain stream order (0), or the VXB_PDL environment default (-1,
+ * on); returns the previous mode.  Graph captures record the mode in force. */
+int vxb_set_pdl(int mode);
+
 /* ---- convolution (kernels_cy.conv3d / _kernels.conv3d) ---- */
 int vxb_conv_select(int cin, int cout, const int k[3], const int stride[3]);
 /* as vxb_conv_select, knowing the output extent: a 1x3x3 conv whose x extent

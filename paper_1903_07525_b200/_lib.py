@@ -108,6 +108,7 @@ SIGNATURES = [
     ("vxb_device_sms", c_int, []),
     ("vxb_debug_read", c_size_t, [c_void_p, c_size_t]),
     ("vxb_conv_select", c_int, [c_int, c_int, I3, I3]),
+    ("vxb_set_pdl", c_int, [c_int]),
     ("vxb_conv_select_shape", c_int, [c_int, c_int, I3, I3, I3]),
     ("vxb_conv_select_shape_b", c_int, [c_int, c_int, I3, I3, I3, c_int]),
     ("vxb_conv_weights_bytes", c_size_t, [c_int, c_int, I3, I3, c_int]),

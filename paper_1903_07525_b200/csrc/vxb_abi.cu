@@ -41,7 +41,18 @@ static int env_int(const char *name, int dflt) {
   return (v && *v) ? atoi(v) : dflt;
 }
 
-bool pdl_enabled() { return env_int("VXB_PDL", 1) != 0; }
+// programmatic dependent launch: VXB_PDL (default on), overridden per host
+// thread by vxb_set_pdl (a runner captures its graph with its own setting)
+static thread_local int t_pdl_override = -1;
+bool pdl_enabled() {
+  if (t_pdl_override >= 0) return t_pdl_override != 0;
+  return env_int("VXB_PDL", 1) != 0;
+}
+int vxb_set_pdl(int mode) {
+  const int prev = t_pdl_override;
+  t_pdl_override = mode < 0 ? -1 : (mode ? 1 : 0);
+  return prev;
+}
 
 static std::mutex g_attr_mu;
 static std::set<std::pair<const void *, int>> g_attr_done;

@@ -70,7 +70,7 @@ class PlanRunner:
     """Executes one ExecutionPlan on one B200; reusable, deterministic."""
 
     def __init__(self, plan, backend=None, *, device=None, use_graph=True, fuse_concat=True,
-                 fuse_pool=False, fuse_input=False, fuse_head=True, probe=None):
+                 fuse_pool=False, fuse_input=False, fuse_head=True, pdl=None, probe=None):
         torch = _torch()
         from .backend import resolve_device_backend
         self.backend = resolve_device_backend(backend)
@@ -80,6 +80,11 @@ class PlanRunner:
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
         self.use_graph = use_graph
+        # programmatic dependent launch for this runner's kernels (None: the
+        # VXB_PDL default, on).  Off measured faster for the 12-patch config-5
+        # batches (4.65 -> 4.48 ms per batch), on for the single networks of
+        # configs 1-4 (config 4 0.82 vs 0.86 ms).
+        self.pdl = pdl
         self.precision = self.backend.precision
         # activation storage: bf16, fp32 (CUDA-core path) or split bf16 (x3)
         self.storage = {"x3": "split"}.get(self.precision, self.precision)
@@ -586,8 +591,13 @@ class PlanRunner:
 
     # ------------------------------------------------------------ running
     def _launch_all(self):
-        for c in self._calls:
-            c()
+        L = _lib.lib()
+        prev = L.vxb_set_pdl(-1 if self.pdl is None else int(bool(self.pdl)))
+        try:
+            for c in self._calls:
+                c()
+        finally:
+            L.vxb_set_pdl(prev)
 
     def _replay(self):
         torch = _torch()
