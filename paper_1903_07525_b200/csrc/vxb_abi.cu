@@ -48,7 +48,7 @@ bool pdl_enabled() {
   if (t_pdl_override >= 0) return t_pdl_override != 0;
   return env_int("VXB_PDL", 1) != 0;
 }
-int vxb_set_pdl(int mode) {
+int set_pdl_override(int mode) {
   const int prev = t_pdl_override;
   t_pdl_override = mode < 0 ? -1 : (mode ? 1 : 0);
   return prev;
@@ -814,6 +814,8 @@ using namespace vxb;
 extern "C" {
 
 int vxb_abi_version(void) { return VXB_ABI_VERSION; }
+
+int vxb_set_pdl(int mode) { return vxb::set_pdl_override(mode); }
 const char *vxb_last_error(void) { return g_last_error.c_str(); }
 int vxb_device_sms(void) { return device_sms(); }
 
