@@ -14,7 +14,8 @@ from .backend import (BACKEND_ENV, Backend, available_backends, compiled_availab
 from .errors import (CycleError, DanglingReferenceError, DuplicateTopError, ExecutionError,
                      FormatError, LayoutError, ModelError, ParseError, PlanError, ShapeError,
                      TileError, UnknownLayerError, VoxplanError)
-from .formats import WeightStore, read_volume, read_weights, write_volume, write_weights
+from .formats import (WeightStore, create_volume, open_volume, read_volume, read_weights,
+                      write_volume, write_weights)
 from .ir import PassReport, build_ir, optimize
 from .netspec import LayerKind, LayerSpec, NetworkSpec
 from .plan import (DEFAULT_PATCH_EXTENT, DEFAULT_SIMD_WIDTH, ExecutionPlan, compile_network,
@@ -29,9 +30,9 @@ def __getattr__(name):
     if name in ("PlanRunner", "PlanBatch", "execute"):
         from . import runner
         return getattr(runner, name)
-    if name == "run_tiled":
-        from .tiling import run_tiled
-        return run_tiled
+    if name in ("run_tiled", "run_tiled_file"):
+        from . import tiling
+        return getattr(tiling, name)
     if name in ("ConvInvocation", "SubImageTask"):
         from . import kernels_b200
         return getattr(kernels_b200, name)
@@ -48,6 +49,7 @@ __all__ = [
     "SubImageTask", "TileError", "TileGrid", "UnknownLayerError", "VoxplanError", "WeightStore",
     "available_backends", "build_ir", "compile_network", "compiled_available", "dump_plan",
     "execute", "get_backend", "grid_for", "optimize", "parse_network", "parse_plan",
-    "plan_tiles", "print_network", "read_plan", "read_volume", "read_weights", "run_tiled",
+    "plan_tiles", "print_network", "read_plan", "read_volume", "open_volume", "create_volume", "read_weights", "run_tiled",
+    "run_tiled_file",
     "validate_shapes", "write_plan", "write_volume", "write_weights", "__version__",
 ]

@@ -55,7 +55,8 @@ def pinned_empty(shape) -> np.ndarray:
 
 def is_pinned(a: np.ndarray) -> bool:
     import torch
-    return (isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous
+    return (isinstance(a, np.ndarray) and not isinstance(a, np.memmap) and
+            a.dtype == np.float32 and a.flags.c_contiguous and a.flags.writeable
             and torch.from_numpy(a).is_pinned())
 
 

@@ -520,3 +520,26 @@ def run_tiled(plan, volume, *, overlap=None, backend=None, workers=None, grid=No
     if errors:
         raise errors[0]
     return out
+
+
+def run_tiled_file(plan, in_path, out_path, *, overlap=None, backend=None, workers=None,
+                   devices=None, grid=None):
+    """File to file: stream a PZNV volume through ``run_tiled`` into a new PZNV
+    file (formats.open_volume / create_volume memory maps: input rows are
+    paged in and output rows written back while the GPU works on the
+    neighbouring rows; neither volume is ever held in host memory as a
+    whole).  The output file is byte-identical to
+    ``write_volume(out_path, run_tiled(plan, read_volume(in_path)))``."""
+    from .formats import create_volume, open_volume
+    vol = open_volume(in_path)
+    _, _, out_dims = _plan_io(plan)
+    if grid is None:
+        grid = grid_for(plan, vol.shape[2:], overlap)
+    out = create_volume(out_path, tuple(out_dims[:2]) + tuple(grid.volume_out))
+    try:
+        run_tiled(plan, vol, overlap=overlap, backend=backend, workers=workers, grid=grid,
+                  devices=devices, out=out)
+        out.flush()
+    finally:
+        del out, vol
+    return out_path

@@ -95,6 +95,31 @@ def test_volume_round_trip(tmp_path, rng):
         formats.read_volume(tmp_path / "v.pznv")
 
 
+def test_streamed_volume_files_match_read_write(tmp_path, rng):
+    """open_volume / create_volume (memory-mapped PZNV, the streamed run_tiled
+    path) read and write exactly the bytes of read_volume / write_volume."""
+    x = rng.standard_normal((2, 3, 5, 4, 6)).astype(np.float32)
+    formats.write_volume(tmp_path / "a.pznv", x)
+    m = formats.open_volume(tmp_path / "a.pznv")
+    assert m.shape == x.shape
+    np.testing.assert_array_equal(np.asarray(m), x)
+    out = formats.create_volume(tmp_path / "b.pznv", x.shape)
+    out[:, :, 2:] = x[:, :, 2:]          # written in two row blocks, like run_host
+    out[:, :, :2] = x[:, :, :2]
+    out.flush()
+    del out
+    assert (tmp_path / "a.pznv").read_bytes() == (tmp_path / "b.pznv").read_bytes()
+    with open(tmp_path / "a.pznv", "ab") as fh:
+        fh.write(b"\0")
+    with pytest.raises(FormatError):
+        formats.open_volume(tmp_path / "a.pznv")
+    (tmp_path / "c.pznv").write_bytes((tmp_path / "b.pznv").read_bytes()[:-4])
+    with pytest.raises(FormatError):
+        formats.open_volume(tmp_path / "c.pznv")
+    with pytest.raises(FormatError):
+        formats.create_volume(tmp_path / "d.pznv", (1, 2, 3))
+
+
 def test_empty_weight_store_is_12_bytes():
     # test_formats.py:63-68 (the code and tests win over SPEC's 13)
     assert len(formats.dump_weights(formats.WeightStore())) == 12

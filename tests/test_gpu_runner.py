@@ -226,6 +226,40 @@ def test_patch_batching_bit_identical(batch, monkeypatch):
     np.testing.assert_array_equal(got, want)
 
 
+def test_patch_batching_with_batch_aware_n_split(monkeypatch):
+    """At 12 patches per launch the 80-fmap level keeps its fmaps in one N tile
+    (vxb_conv_select_shape_b counts every batch entry's tiles) while a
+    single-patch run splits them into N tiles of 32: the split never changes
+    a result, so the outputs stay bit-identical."""
+    from paper_1903_07525_b200 import _lib
+    L = _lib.lib()
+    k3, s1 = _lib.i3((3, 3, 3)), _lib.i3((1, 1, 1))
+    assert L.vxb_conv_select_shape_b(80, 80, k3, s1, _lib.i3((4, 12, 12)), 1) != \
+        L.vxb_conv_select_shape_b(80, 80, k3, s1, _lib.i3((4, 12, 12)), 12)
+    spec, store = C.config5(patch=(4, 24, 24), feats=(16, 80))
+    plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
+    vol = np.random.default_rng(3).uniform(0, 1, (1, 1, 8, 72, 48)).astype(np.float32)
+    grid = P.grid_for(plan, vol.shape[2:], overlap=0)
+    assert len(grid.tiles) == 12
+    monkeypatch.setenv("VOXPLAN_PATCH_BATCH", "1")
+    want = P.run_tiled(plan, vol, grid=grid)
+    monkeypatch.setenv("VOXPLAN_PATCH_BATCH", "12")
+    got = P.run_tiled(plan, vol, grid=grid)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_run_tiled_file_streams_pznv(tmp_path):
+    """run_tiled_file (memory-mapped PZNV in and out, formats.py:45-74 byte
+    layout) writes exactly write_volume(run_tiled(read_volume(...)))."""
+    spec, store = C.config5(patch=(4, 32, 32), feats=(8, 12, 16))
+    plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
+    vol = np.random.default_rng(2).uniform(0, 1, (1, 1, 9, 80, 70)).astype(np.float32)
+    P.write_volume(tmp_path / "in.pznv", vol)
+    P.run_tiled_file(plan, tmp_path / "in.pznv", tmp_path / "out.pznv", overlap=0)
+    P.write_volume(tmp_path / "want.pznv", P.run_tiled(plan, vol, overlap=0))
+    assert (tmp_path / "out.pznv").read_bytes() == (tmp_path / "want.pznv").read_bytes()
+
+
 def test_rebatched_plan_equals_per_volume_runs():
     """plan.rebatch on a U-net with pooling, deconv, crop + concat: entry b
     of the batched run equals the batch-1 run on volume b, bit for bit."""
