@@ -223,14 +223,19 @@ class DeviceTiler:
         self.torch = torch
         self.grid = grid
         self.device = torch.device(device)
-        n = int(streams if streams is not None else os.environ.get("VOXPLAN_STREAMS", "2"))
+        n = int(streams if streams is not None else os.environ.get("VOXPLAN_STREAMS", "1"))
         # patches per launch: the deep U-net levels of several patches share
         # one kernel (their few output tiles alone leave most SMs idle).
         # Config-5 volume, 2 streams: 1 -> 170.6 ms, 2 -> 149.9, 3 -> 138.4,
         # 4 -> 131.5, 6 -> 127.1, 8 -> 124.1, 12 -> 123.5, 16 -> 123.1 ms
         # (tools/sweep_batch.sh; one stream is ~1 % slower at every batch).
         # 12 divides the 36 tiles of a config-5 x-row, so the streamed
-        # run_host (row by row) never runs a short, padded batch.
+        # run_host (row by row) never runs a short, padded batch.  Runner
+        # streams: with the lean epilogue and no PDL inside the batches, one
+        # stream measured 116.2 ms vs 116.9 ms for two (the persistent convs
+        # fill every SM, so a second stream only interleaves), and a single
+        # stream keeps the in-step kernel timing free of the other stream's
+        # work.
         self.batch = max(1, int(batch if batch is not None else
                                 os.environ.get("VOXPLAN_PATCH_BATCH", "12")))
         self.vol_batch = int(plan.inputs[0][2][0])
@@ -450,7 +455,7 @@ def device_tiler(plan, grid: TileGrid, device, backend=None, slot=0) -> DeviceTi
     captured graphs; two workers on the same device get separate tilers."""
     key = (id(plan), grid.patch_in, grid.volume_in, grid.overlap, str(device), int(slot),
            repr(backend),
-           os.environ.get("VOXPLAN_PATCH_BATCH", "12"), os.environ.get("VOXPLAN_STREAMS", "2"))
+           os.environ.get("VOXPLAN_PATCH_BATCH", "12"), os.environ.get("VOXPLAN_STREAMS", "1"))
     with _TILER_LOCK:
         hit = _TILER_CACHE.get(key)
         if hit is not None and hit[0] is plan:
