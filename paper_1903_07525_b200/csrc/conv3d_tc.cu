@@ -269,6 +269,18 @@ struct LeanEnt {
 };
 constexpr int LEAN_TAB = 16;   // nt <= 256: <= 16 column items
 
+// Lean epilogue: per-tile origin computed once by the A producer (which
+// decodes the tile anyway) instead of by all 16 epilogue warps: element
+// offsets of the tile's (row 0, slice 0) in the output and residual views,
+// the tile's row / z / slice origins and its N-tile column.  A ring of
+// TINFO slots, each published with an mbarrier arrive; the producer runs at
+// most na + acc_stages tiles ahead of the epilogue.
+struct TileInfo {
+  long long o_off, b_off;
+  int rc0, z0, sc0, nt0, dummy, pad[3];
+};
+constexpr int TINFO = 16;
+
 // Byte offsets inside the dynamic smem block (all derivable from p).
 struct SmemMap {
   uint32_t a, b, stg, bias, scale, head, ltab, bars;
@@ -283,7 +295,7 @@ __host__ __device__ inline SmemMap smem_map(const TcParams &p) {
   m.scale = m.bias + cpad * 4;
   m.head = m.scale + cpad * 4;                 // fused head weights [head_cout][cpad]
   m.ltab = (m.head + (p.head_cout > 0 ? 4 * cpad * 4 : 0) + 15) & ~15u;
-  m.bars = m.ltab + (p.lean ? LEAN_TAB * sizeof(LeanEnt) : 0);
+  m.bars = m.ltab + (p.lean ? LEAN_TAB * sizeof(LeanEnt) + TINFO * sizeof(TileInfo) : 0);
   return m;
 }
 
@@ -529,7 +541,8 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
   uint64_t *t_empty = t_full + 2;
   uint64_t *stg_full = t_empty + 2;                 // F32IN staging ring
   uint64_t *stg_empty = stg_full + p.n_stg;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(stg_empty + p.n_stg);
+  uint64_t *info_full = stg_empty + p.n_stg;          // lean: TileInfo ring slots
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(stg_empty + p.n_stg + (p.lean ? TINFO : 0));
   uint8_t *stg_buf = smem + sm.stg;
 
   // CTA pairs (cluster 2) walk pairs of tiles in lockstep so they can share
@@ -565,6 +578,7 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
     s_scale[c] = (cr < p.cout && p.scale) ? p.scale[cr] : 1.f;
   }
   LeanEnt *ltab = reinterpret_cast<LeanEnt *>(smem + sm.ltab);
+  TileInfo *tinfo = reinterpret_cast<TileInfo *>(smem + sm.ltab + LEAN_TAB * sizeof(LeanEnt));
   if (LEAN)
     for (int ci = threadIdx.x; ci < (p.nt >> 4); ci += blockDim.x) {
       const int cc = ci << 4;
@@ -616,6 +630,8 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       mbar_init(&t_full[i], 1);
       mbar_init(&t_empty[i], PAIR ? 2 * EPI_WARPS : EPI_WARPS);
     }
+    if (LEAN)
+      for (int i = 0; i < TINFO; ++i) mbar_init(&info_full[i], 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -643,6 +659,26 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       int pit = 0;
       for (int tile = first_tile; tile < p.total_tiles; tile += tile_step, ++pit) {
         TileCoord tc = decode_tile(p, tile);
+        if constexpr (LEAN) {
+          TileInfo ti;
+          const int ra_dim = p.slice_y ? 2 : 3, sl_dim = p.slice_y ? 3 : 2;
+          ti.rc0 = p.slice_y ? tc.x0 : tc.y0;
+          ti.z0 = tc.z0;
+          ti.sc0 = p.slice_y ? tc.y0 : tc.x0;
+          ti.nt0 = tc.nt * p.nt;
+          ti.dummy = tc.dummy;
+          ti.o_off = tc.b * p.out.s[0] + static_cast<long long>(ti.rc0) * p.out.s[ra_dim] +
+                     static_cast<long long>(ti.z0) * p.out.s[4] +
+                     static_cast<long long>(ti.sc0) * p.out.s[sl_dim] +
+                     (p.rep_n ? 0 : p.out_rep_off[tc.rep]) + (ti.nt0 >> 3) * p.out.s[1];
+          ti.b_off = tc.b * p.base.s[0] + static_cast<long long>(ti.rc0) * p.base.s[ra_dim] +
+                     static_cast<long long>(ti.z0) * p.base.s[4] +
+                     static_cast<long long>(ti.sc0) * p.base.s[sl_dim] +
+                     (p.rep_n ? 0 : p.base_rep_off[tc.rep]) + (ti.nt0 >> 3) * p.base.s[1];
+          ti.pad[0] = ti.pad[1] = ti.pad[2] = 0;
+          tinfo[pit & (TINFO - 1)] = ti;
+          mbar_arrive(&info_full[pit & (TINFO - 1)]);   // release: the epilogue acquires
+        }
         for (int g = 0; g < p.n_groups; ++g) {
           GroupInfo gi = group_info(p, g);
           mbar_wait_sleep(&a_empty[a_st], a_ph ^ 1);
@@ -995,17 +1031,47 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
     const int act = ACT >= 0 ? ACT : p.act;
     const bool braw = BASE && bvw.dtype == VXB_BF16 && bvw.blocked;
     int it = 0;
+    const int ra_dim = p.slice_y ? 2 : 3, sl_dim = p.slice_y ? 3 : 2;
+    // lean: this thread's row offset inside a tile (per kernel)
+    const long long ra_oo = LEAN ? ra * ov.s[ra_dim] + zz * ov.s[4] : 0;
+    const long long ra_bo = LEAN && BASE ? ra * bvw.s[ra_dim] + zz * bvw.s[4] : 0;
     for (int tile = first_tile; tile < p.total_tiles; tile += tile_step, ++it) {
-      TileCoord tc = decode_tile(p, tile);
+      TileCoord tc;
+      int rc, z, sc0;
+      bool yz_ok;
+      long long lo_off = 0, lb_off = 0;
+      int nt0;
+      if constexpr (LEAN) {
+        // the producer published this tile's origin (TileInfo ring)
+        const int slot = it & (TINFO - 1);
+        mbar_wait_sleep(&info_full[slot], static_cast<uint32_t>((it / TINFO) & 1));
+        const TileInfo &ti = tinfo[slot];
+        rc = ti.rc0 + ra;
+        z = ti.z0 + zz;
+        sc0 = ti.sc0;
+        nt0 = ti.nt0;
+        yz_ok = rc < (p.slice_y ? p.ox : p.oy) && z < p.oz && !ti.dummy;
+        lo_off = ti.o_off + ra_oo;
+        lb_off = ti.b_off + ra_bo;
+        tc.rep = 0;
+        tc.nt = 0;
+        tc.b = 0;
+        tc.x0 = tc.y0 = tc.z0 = 0;
+        tc.dummy = ti.dummy;
+      } else {
+        tc = decode_tile(p, tile);
+        rc = (p.slice_y ? tc.x0 : tc.y0) + ra;
+        z = tc.z0 + zz;
+        sc0 = p.slice_y ? tc.y0 : tc.x0;
+        yz_ok = rc < (p.slice_y ? p.ox : p.oy) && z < p.oz && !tc.dummy;
+        nt0 = tc.nt * p.nt;
+      }
       const int acc = (it & (p.acc_stages - 1));
-      const int rc = (p.slice_y ? tc.x0 : tc.y0) + ra, z = tc.z0 + zz;
-      const int sc0 = p.slice_y ? tc.y0 : tc.x0, slim = p.slice_y ? p.oy : p.ox;
-      const bool yz_ok = rc < (p.slice_y ? p.ox : p.oy) && z < p.oz && !tc.dummy;
-      const int ra_dim = p.slice_y ? 2 : 3, sl_dim = p.slice_y ? 3 : 2;
+      const int slim = p.slice_y ? p.oy : p.ox;
       // (replica offsets are added per item: with taps in N (rep_n) every
       // 16-column item belongs to one tap)
-      const long long orow = tc.b * ov.s[0] + rc * ov.s[ra_dim] + z * ov.s[4];
-      const long long brow = tc.b * bvw.s[0] + rc * bvw.s[ra_dim] + z * bvw.s[4];
+      const long long orow = LEAN ? 0 : tc.b * ov.s[0] + rc * ov.s[ra_dim] + z * ov.s[4];
+      const long long brow = LEAN ? 0 : tc.b * bvw.s[0] + rc * bvw.s[ra_dim] + z * bvw.s[4];
       // item column -> (replica, first channel of the item)
       // (z-pair order: rep is the item's dz = 0 tap, its second half is rep + 1
       // at the same channels)
@@ -1026,16 +1092,11 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
           tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * acc_stride + p.slice0_col;
       // lean epilogue: this thread's row in slice 0 of the tile (N tile and
       // tile replica included); items add the slice and their LeanEnt offsets
-      const int nt0 = tc.nt * p.nt;
       __nv_bfloat16 *lo_row = nullptr;
       const __nv_bfloat16 *lb_row = nullptr;
       if constexpr (LEAN) {
-        lo_row = static_cast<__nv_bfloat16 *>(ov.data) + orow +
-                 (p.rep_n ? 0 : p.out_rep_off[tc.rep]) + sc0 * ov.s[sl_dim] + (nt0 >> 3) * ov.s[1];
-        if (BASE)
-          lb_row = static_cast<const __nv_bfloat16 *>(bvw.data) + brow +
-                   (p.rep_n ? 0 : p.base_rep_off[tc.rep]) + sc0 * bvw.s[sl_dim] +
-                   (nt0 >> 3) * bvw.s[1];
+        lo_row = static_cast<__nv_bfloat16 *>(ov.data) + lo_off;
+        if (BASE) lb_row = static_cast<const __nv_bfloat16 *>(bvw.data) + lb_off;
       }
 
       auto taddr_of = [&](int item) {
@@ -1440,7 +1501,8 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
 // ---------------------------------------------------------------- host side
 
 size_t tc_smem_bytes(const TcParams &p) {
-  return smem_map(p).bars + (2 * p.na + 2 * p.nb_stages + 4 + 2 * p.n_stg) * sizeof(uint64_t) +
+  return smem_map(p).bars +
+         (2 * p.na + 2 * p.nb_stages + 4 + 2 * p.n_stg + (p.lean ? TINFO : 0)) * sizeof(uint64_t) +
          16;
 }
 
