@@ -266,6 +266,10 @@ int vxb_pad_copy(const vxb_tensor *in, const vxb_tensor *out, const int pads[3],
  * generic strided copy between any two views of the same logical shape,
  * converting dtype; tail lanes of a blocked destination are zeroed. */
 int vxb_copy(const vxb_tensor *src, const vxb_tensor *dst, void *stream);
+/* count (src[i] -> dst[i]) copies of equally shaped fp32 standard views
+ * (z contiguous) in one launch per 16: the patch gather / scatter of tiled
+ * execution (the reference's per-tile numpy slicing, tiling.py:189-237) */
+int vxb_copy_windows(const vxb_tensor *src, const vxb_tensor *dst, int count, void *stream);
 /* vxb_copy with flags.  VXB_COPY_INDEPENDENT: the copy reads nothing the
  * previous kernel in the stream writes and writes nothing it touches (a
  * network-input pack), so it may start beside that kernel instead of after

@@ -744,6 +744,50 @@ int launch_copy(const DView &src, const DView &dst, cudaStream_t s, bool indepen
   return check_cuda(launch_pdl(copy_kernel, grid3(dst, 256), dim3(256), 0, s, src, dst),
                     "copy_kernel");
 }
+// One block row per (window, 256-element span of its z rows): consecutive
+// threads move consecutive z elements (float4 when the window allows), so a
+// warp reads and writes contiguous 512-byte runs of both volumes.
+__global__ void __launch_bounds__(256) copy_windows_kernel(const __grid_constant__ WinBatch b) {
+  pdl_begin();
+  const WinCopy &w = b.w[blockIdx.y];
+  const int zq = w.vec4 ? w.ext[4] >> 2 : w.ext[4];      // z elements (or float4s) per row
+  const long long rows = static_cast<long long>(w.ext[0]) * w.ext[1] * w.ext[2] * w.ext[3];
+  const long long total = rows * zq;
+  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    long long r = e / zq;
+    const int zz = static_cast<int>(e - r * zq);
+    const int y = static_cast<int>(r % w.ext[3]);
+    r /= w.ext[3];
+    const int x = static_cast<int>(r % w.ext[2]);
+    r /= w.ext[2];
+    const int c = static_cast<int>(r % w.ext[1]);
+    const int n = static_cast<int>(r / w.ext[1]);
+    const long long so = n * w.ss[0] + c * w.ss[1] + x * w.ss[2] + y * w.ss[3];
+    const long long d = n * w.ds[0] + c * w.ds[1] + x * w.ds[2] + y * w.ds[3];
+    if (w.vec4)
+      reinterpret_cast<float4 *>(w.dst + d)[zz] =
+          __ldg(reinterpret_cast<const float4 *>(w.src + so) + zz);
+    else
+      w.dst[d + zz] = __ldg(w.src + so + zz);
+  }
+}
+
+int launch_copy_windows(const WinBatch &b, cudaStream_t s) {
+  if (b.count <= 0) return VXB_OK;
+  long long most = 1;
+  for (int i = 0; i < b.count; ++i) {
+    const WinCopy &w = b.w[i];
+    const long long e = static_cast<long long>(w.ext[0]) * w.ext[1] * w.ext[2] * w.ext[3] *
+                        (w.vec4 ? w.ext[4] >> 2 : w.ext[4]);
+    most = std::max(most, e);
+  }
+  // enough blocks per window to cover the SMs a few times over
+  const int bx = static_cast<int>(std::min<long long>((most + 255) / 256, 4096));
+  return check_cuda(launch_pdl(copy_windows_kernel, dim3(bx, b.count), dim3(256), 0, s, b),
+                    "copy_windows_kernel");
+}
+
 int launch_pack_zwin(const DView &src, const DView &dst, int kz, int pz, cudaStream_t s,
                      bool independent) {
   dim3 g((dst.y * ((dst.z + 3) >> 2) + 127) / 128, dst.x, dst.n);

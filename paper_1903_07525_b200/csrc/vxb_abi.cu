@@ -1472,6 +1472,40 @@ int vxb_copy_ex(const vxb_tensor *src, const vxb_tensor *dst, int flags, void *s
                      (flags & VXB_COPY_INDEPENDENT) != 0);
 }
 
+int vxb_copy_windows(const vxb_tensor *src, const vxb_tensor *dst, int count, void *stream) {
+  if (count < 0 || (count > 0 && (!src || !dst)))
+    return set_error(VXB_EINVAL, "copy_windows: bad arguments");
+  for (int base = 0; base < count; base += WIN_MAX) {
+    WinBatch b;
+    memset(&b, 0, sizeof(b));
+    b.count = std::min(WIN_MAX, count - base);
+    for (int i = 0; i < b.count; ++i) {
+      const vxb_tensor &a = src[base + i], &d = dst[base + i];
+      int rc;
+      if ((rc = check_view(&a, "copy_windows.src")) || (rc = check_view(&d, "copy_windows.dst")))
+        return rc;
+      if (a.dtype != VXB_F32 || d.dtype != VXB_F32 || a.blocked || d.blocked || a.s[4] != 1 ||
+          d.s[4] != 1)
+        return set_error(VXB_EINVAL, "copy_windows: fp32 standard views with contiguous z");
+      if ((rc = same_shape(&a, &d, "copy_windows"))) return rc;
+      WinCopy &w = b.w[i];
+      w.src = static_cast<const float *>(a.data);
+      w.dst = static_cast<float *>(d.data);
+      for (int k = 0; k < 4; ++k) {
+        w.ss[k] = a.s[k];
+        w.ds[k] = d.s[k];
+      }
+      w.ext[0] = a.n; w.ext[1] = a.c; w.ext[2] = a.x; w.ext[3] = a.y; w.ext[4] = a.z;
+      bool v4 = a.z % 4 == 0 && !(reinterpret_cast<uintptr_t>(a.data) & 15) &&
+                !(reinterpret_cast<uintptr_t>(d.data) & 15);
+      for (int k = 0; k < 4; ++k) v4 = v4 && a.s[k] % 4 == 0 && d.s[k] % 4 == 0;
+      w.vec4 = v4;
+    }
+    if (int rc = launch_copy_windows(b, as_stream(stream))) return rc;
+  }
+  return VXB_OK;
+}
+
 int vxb_pack_zwin(const vxb_tensor *src, const vxb_tensor *dst, int kz, int pz, int flags,
                   void *stream) {
   int rc;

@@ -144,6 +144,21 @@ struct GatherDeconvParams {
 };
 
 int launch_copy(const DView &src, const DView &dst, cudaStream_t s, bool independent = false);
+// batched window copies (fp32, z contiguous): up to WIN_MAX (src, dst) pairs
+// of equal extents in one launch (DeviceTiler's patch gather / scatter)
+constexpr int WIN_MAX = 16;
+struct WinCopy {
+  const float *src;
+  float *dst;
+  long long ss[4], ds[4];   // n, c, x, y strides (elements); z stride is 1
+  int ext[5];               // n, c, x, y, z
+  int vec4;                 // z extent, pointers and strides allow float4 moves
+};
+struct WinBatch {
+  WinCopy w[WIN_MAX];
+  int count;
+};
+int launch_copy_windows(const WinBatch &b, cudaStream_t s);
 int launch_pack_zwin(const DView &src, const DView &dst, int kz, int pz, cudaStream_t s,
                      bool independent);
 int launch_zero(const DView &dst, cudaStream_t s);

@@ -119,6 +119,21 @@ def null_tensor() -> _lib.VxbTensor:
     return _lib.VxbTensor()
 
 
+def copy_windows(pairs, stream=None) -> None:
+    """vxb_copy_windows: [(src, dst), ...] fp32 (n, c, x, y, z) torch views of
+    equal shapes (z contiguous), moved in one launch per 16 pairs."""
+    if not pairs:
+        return
+    L = _lib.lib()
+    n = len(pairs)
+    srcs, dsts = (_lib.VxbTensor * n)(), (_lib.VxbTensor * n)()
+    for i, (a, b) in enumerate(pairs):
+        srcs[i] = standard(a).vxb()
+        dsts[i] = standard(b).vxb()
+    _lib.check(L.vxb_copy_windows(srcs, dsts, n, stream or current_stream_handle()),
+               "vxb_copy_windows")
+
+
 def copy(src: DTensor, dst: DTensor, stream=None, independent=False) -> None:
     """vxb_copy; ``independent`` (vxb_copy_ex VXB_COPY_INDEPENDENT): the copy
     touches nothing the previous kernel in the stream does, so it may run

@@ -91,6 +91,8 @@ class PlanRunner:
         # weight packing precision of the tensor-core paths
         self._prec = "x3" if self.precision == "x3" else "bf16"
         self.fuse_concat = fuse_concat and self.precision == "bf16"
+        if os.environ.get("VXB_FUSE_POOL") is not None:     # experiments
+            fuse_pool = os.environ["VXB_FUSE_POOL"] == "1"
         self.fuse_pool = fuse_pool and self.precision == "bf16"
         self.fuse_input = fuse_input
         self.fuse_head = fuse_head and self.precision in ("bf16", "x3") and \
@@ -598,6 +600,19 @@ class PlanRunner:
                 c()
         finally:
             L.vxb_set_pdl(prev)
+
+    def ensure_graph(self):
+        """Capture this runner's graph now if it has not been (the first
+        launches also configure the kernels' shared-memory attributes)."""
+        torch = _torch()
+        if self._graph is None and self.use_graph:
+            self._replay()
+            self.stream.synchronize()
+
+    def launch_raw(self):
+        """Launch the network's kernels on the current stream without the
+        graph (for a caller capturing a larger graph around them)."""
+        self._launch_all()
 
     def _replay(self):
         torch = _torch()

@@ -276,8 +276,9 @@ class DeviceTiler:
         return self.runner.launches / self.batch
 
     def launches_for(self, n_tiles: int) -> int:
-        """Kernel launches to run n_tiles (batches of self.batch patches)."""
-        return self.runner.launches * -(-n_tiles // self.batch)
+        """Kernel launches to run n_tiles (batches of self.batch patches): the
+        network plus one gather and one scatter launch per batch."""
+        return (self.runner.launches + 2) * -(-n_tiles // self.batch)
 
     # ------------------------------------------------------------ resident
     def bind_slabs(self, slab, lo, out_slab, olo):
@@ -301,26 +302,82 @@ class DeviceTiler:
 
     def run(self, tiles):
         """Run the tiles from the bound input slab into the bound output slab
-        (enqueued; the current stream is made to wait for all of them)."""
+        (enqueued; the current stream is made to wait for all of them).  With
+        one runner the whole tile list -- every batch's patch gather, network
+        and kept-window scatter -- replays as one CUDA graph, captured on the
+        first call for this (tile list, slab pair)."""
         torch = self.torch
         with torch.cuda.device(self.device):
             cur = torch.cuda.current_stream(self.device)
             for r in self.runners:
                 r.stream.wait_stream(cur)       # slab / output slab are ready
-            self._enqueue(tiles, self.slab, self.lo, self.out_slab, self.olo)
+            g = self._volume_graph(tiles, self.slab, self.lo, self.out_slab, self.olo)
+            if g is not None:
+                with torch.cuda.stream(self.runner.stream):
+                    g.replay()
+            else:
+                self._enqueue(tiles, self.slab, self.lo, self.out_slab, self.olo)
             for r in self.runners:
                 cur.wait_stream(r.stream)
 
-    def _enqueue(self, tiles, slab, lo, out_slab, olo, start=0):
-        """Enqueue the tiles' batches on the runner streams (round robin from
-        runner `start`); returns the next runner index."""
+    def _volume_graph(self, tiles, slab, lo, out_slab, olo):
+        """One CUDA graph over every batch of ``tiles`` (single runner only;
+        cached per tile list and slab pointers, VOXPLAN_VOLUME_GRAPH=0 off)."""
         torch = self.torch
+        if len(self.runners) != 1 or os.environ.get("VOXPLAN_VOLUME_GRAPH", "1") != "1":
+            return None
+        # keyed by the tiles' geometry relative to the slabs, so the rows of
+        # the streamed run_host (same layout, two ring slots) share graphs
+        geo = tuple((tuple(a - l for a, l in zip(t.in_lo, lo)),
+                     tuple(o - l for o, l in zip(t.out_lo, olo)),
+                     tuple(t.keep_lo), tuple(t.keep_hi)) for t in tiles)
+        key = (geo, slab.data_ptr(), out_slab.data_ptr(), tuple(slab.shape), tuple(slab.stride()),
+               tuple(out_slab.shape), tuple(out_slab.stride()))
+        cache = self.__dict__.setdefault("_vgraphs", {})
+        g = cache.get(key)
+        if g is None:
+            r = self.runner
+            r.ensure_graph()                     # kernels configured, pool bound
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=r.stream, capture_error_mode="thread_local"):
+                self._enqueue(tiles, slab, lo, out_slab, olo, raw=True)
+            if len(cache) >= 8:
+                cache.pop(next(iter(cache)))
+            cache[key] = g
+        return g
+
+    def _windows(self, group, slab, lo, out_slab, olo, xin, res):
+        """(gather, scatter) window pairs of one patch batch."""
         pin = self.grid.patch_in
+        whole = self.vol_batch > 1
+        gather, scatter = [], []
+        for b in range(self.batch):
+            t = group[min(b, len(group) - 1)]   # a short last group repeats
+            src = tuple(slice(a - l, a - l + p) for a, l, p in zip(t.in_lo, lo, pin))
+            dst_b = slice(None) if whole else slice(b, b + 1)
+            gather.append((slab[(slice(None), slice(None)) + src], xin[dst_b]))
+        for b, t in enumerate(group):
+            dst = tuple(slice(o - l, o - l + (e - a)) for o, l, a, e in
+                        zip(t.out_lo, olo, t.keep_lo, t.keep_hi))
+            src_b = slice(None) if whole else slice(b, b + 1)
+            scatter.append((res[(src_b, slice(None)) + t.local_window],
+                            out_slab[(slice(None), slice(None)) + dst]))
+        return gather, scatter
+
+    def _enqueue(self, tiles, slab, lo, out_slab, olo, start=0, raw=False):
+        """Enqueue the tiles' batches on the runner streams (round robin from
+        runner `start`); returns the next runner index.  Each batch: one
+        gather launch (the patches' input windows into the runner's input
+        buffer), the network, one scatter launch (kept windows into the
+        output slab).  ``raw``: launch the network's kernels directly (inside
+        a capture of the whole volume) instead of replaying its graph."""
+        from .device import copy_windows, current_stream_handle
+        torch = self.torch
         B = self.batch
         # rebatched plans (volume batch 1) stack B patches along the batch
         # axis; a plan whose own batch is > 1 runs one patch of the whole
         # volume batch per launch (B == 1)
-        whole = self.vol_batch > 1
         groups = [tiles[i:i + B] for i in range(0, len(tiles), B)]
         k = start
         nocopy = os.environ.get("VOXPLAN_DEBUG_NOCOPY") == "1"   # timing experiments only
@@ -328,20 +385,17 @@ class DeviceTiler:
             r = self.runners[k % len(self.runners)]
             k += 1
             xin = r._in_std[self.in_name]
+            res = next(iter(r._out_std.values()))
+            gather, scatter = self._windows(group, slab, lo, out_slab, olo, xin, res)
             with torch.cuda.stream(r.stream):
-                for b in range(0 if nocopy else B):
-                    t = group[min(b, len(group) - 1)]   # a short last group repeats
-                    src = tuple(slice(a - l, a - l + p) for a, l, p in zip(t.in_lo, lo, pin))
-                    dst_b = slice(None) if whole else slice(b, b + 1)
-                    xin[dst_b].copy_(slab[(slice(None), slice(None)) + src])
-            res = next(iter(r.run_on_stream({self.in_name: xin}).values()))
-            with torch.cuda.stream(r.stream):
-                for b, t in enumerate([] if nocopy else group):
-                    dst = tuple(slice(o - l, o - l + (e - a)) for o, l, a, e in
-                                zip(t.out_lo, olo, t.keep_lo, t.keep_hi))
-                    src_b = slice(None) if whole else slice(b, b + 1)
-                    out_slab[(slice(None), slice(None)) + dst].copy_(
-                        res[(src_b, slice(None)) + t.local_window])
+                if not nocopy:
+                    copy_windows(gather, current_stream_handle())
+                if raw:
+                    r.launch_raw()
+                else:
+                    r.run_on_stream({self.in_name: xin})
+                if not nocopy:
+                    copy_windows(scatter, current_stream_handle())
         return k
 
     # ------------------------------------------------------------ streamed
@@ -416,7 +470,12 @@ class DeviceTiler:
                     r.stream.wait_event(up)
                     if ev_out[slot] is not None:
                         r.stream.wait_event(ev_out[slot])
-                k = self._enqueue(row, xin, lo, yout, olo, start=k)
+                g = self._volume_graph(row, xin, lo, yout, olo)
+                if g is not None:
+                    with torch.cuda.stream(self.runner.stream):
+                        g.replay()
+                else:
+                    k = self._enqueue(row, xin, lo, yout, olo, start=k)
                 done = []
                 for r in self.runners:
                     e = torch.cuda.Event()
