@@ -1195,29 +1195,29 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
           const LeanEnt &e = ltab[cc >> 4];
           const int c0 = nt0 + e.ch, c1 = p.zpair ? c0 : c0 + 8;
           const int col = nt0 + cc;
+          // (packed pairs: FADD2 / FFMA2 / FMUL2 for the bias, the residual and
+          // the exponent's scaling -- bit-identical to the scalar forms)
           uint32_t w[8];
 #pragma unroll
-          for (int i4 = 0; i4 < 4; ++i4) {
-            const float4 b4 = *reinterpret_cast<const float4 *>(s_bias + col + 4 * i4);
-            float r[4] = {__uint_as_float(rv[4 * i4]) + b4.x, __uint_as_float(rv[4 * i4 + 1]) + b4.y,
-                          __uint_as_float(rv[4 * i4 + 2]) + b4.z,
-                          __uint_as_float(rv[4 * i4 + 3]) + b4.w};
+          for (int i2 = 0; i2 < 8; ++i2) {
+            const float2 b2 = *reinterpret_cast<const float2 *>(s_bias + col + 2 * i2);
+            float2 r = fadd2(make_float2(__uint_as_float(rv[2 * i2]), __uint_as_float(rv[2 * i2 + 1])),
+                             b2);
             if (BASE) {
-              const float4 c4 = *reinterpret_cast<const float4 *>(s_scale + col + 4 * i4);
-              r[0] = fmaf(c4.x, bv[4 * i4], r[0]);
-              r[1] = fmaf(c4.y, bv[4 * i4 + 1], r[1]);
-              r[2] = fmaf(c4.z, bv[4 * i4 + 2], r[2]);
-              r[3] = fmaf(c4.w, bv[4 * i4 + 3], r[3]);
+              const float2 c2 = *reinterpret_cast<const float2 *>(s_scale + col + 2 * i2);
+              r = ffma2(c2, make_float2(bv[2 * i2], bv[2 * i2 + 1]), r);
             }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              if (ACT == VXB_ACT_RELU) r[i] = fmaxf(r[i], 0.f);
-              else if (ACT == VXB_ACT_ELU) r[i] = fast_elu(r[i], p.alpha);
+            if (ACT == VXB_ACT_RELU) {
+              r.x = fmaxf(r.x, 0.f);
+              r.y = fmaxf(r.y, 0.f);
+            } else if (ACT == VXB_ACT_ELU) {
+              const float2 t = fmul2(r, make_float2(1.4426950408889634f, 1.4426950408889634f));
+              const float ex = ex2_ftz(t.x), ey = ex2_ftz(t.y);
+              r.x = r.x > 0.f ? r.x : fmaf(p.alpha, ex, -p.alpha);
+              r.y = r.y > 0.f ? r.y : fmaf(p.alpha, ey, -p.alpha);
             }
-            __nv_bfloat162 h0 = __floats2bfloat162_rn(r[0], r[1]);
-            __nv_bfloat162 h1 = __floats2bfloat162_rn(r[2], r[3]);
-            w[2 * i4] = *reinterpret_cast<uint32_t *>(&h0);
-            w[2 * i4 + 1] = *reinterpret_cast<uint32_t *>(&h1);
+            __nv_bfloat162 h = __floats2bfloat162_rn(r.x, r.y);
+            w[i2] = *reinterpret_cast<uint32_t *>(&h);
           }
           if (yz_ok && sc0 + s < slim) {
             __nv_bfloat16 *o = lo_row + s * ov.s[sl_dim];
@@ -1360,37 +1360,50 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
         // the residual loads two items ahead are in flight while an item is
         // finished.
         const EpiView &hv = p.head_out;
-        float hsum[4] = {0.f, 0.f, 0.f, 0.f};
         auto adv = [&](int &s_, int &c_) {
           if (++c_ == col_items) {
             c_ = 0;
             s_ += NSUB;
           }
         };
+        // head sums as even / odd channel pairs (FFMA2), folded at the store
+        float2 hs2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                         make_float2(0.f, 0.f)};
         auto head_item = [&](int s_, int c_, const uint32_t (&rv)[16], const float (&bq)[16]) {
           const int col = tc.nt * p.nt + c_ * 16;
 #pragma unroll
           for (int i4 = 0; i4 < 4; ++i4) {
             const float4 b4 = *reinterpret_cast<const float4 *>(s_bias + col + 4 * i4);
-            const float4 c4 = *reinterpret_cast<const float4 *>(s_scale + col + 4 * i4);
-            const float bb[4] = {b4.x, b4.y, b4.z, b4.w}, sc[4] = {c4.x, c4.y, c4.z, c4.w};
-            float r[4];
+            float2 r[2] = {fadd2(make_float2(__uint_as_float(rv[4 * i4]), __uint_as_float(rv[4 * i4 + 1])),
+                                 make_float2(b4.x, b4.y)),
+                           fadd2(make_float2(__uint_as_float(rv[4 * i4 + 2]),
+                                             __uint_as_float(rv[4 * i4 + 3])),
+                                 make_float2(b4.z, b4.w))};
+            if (BASE) {
+              const float4 c4 = *reinterpret_cast<const float4 *>(s_scale + col + 4 * i4);
+              r[0] = ffma2(make_float2(c4.x, c4.y), make_float2(bq[4 * i4], bq[4 * i4 + 1]), r[0]);
+              r[1] = ffma2(make_float2(c4.z, c4.w), make_float2(bq[4 * i4 + 2], bq[4 * i4 + 3]), r[1]);
+            }
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int i = 4 * i4 + e;
-              r[e] = __uint_as_float(rv[i]) + bb[e];
-              if (BASE) r[e] = fmaf(sc[e], bq[i], r[e]);
-              if (act == VXB_ACT_RELU) r[e] = fmaxf(r[e], 0.f);
-              else if (act == VXB_ACT_ELU) r[e] = fast_elu(r[e], p.alpha);
-              else if (act == VXB_ACT_SIGMOID) r[e] = fast_sigmoid(r[e]);
+            for (int h = 0; h < 2; ++h) {
+              if (act == VXB_ACT_RELU) {
+                r[h].x = fmaxf(r[h].x, 0.f);
+                r[h].y = fmaxf(r[h].y, 0.f);
+              } else if (act == VXB_ACT_ELU) {
+                const float2 t = fmul2(r[h], make_float2(1.4426950408889634f, 1.4426950408889634f));
+                const float ex = ex2_ftz(t.x), ey = ex2_ftz(t.y);
+                r[h].x = r[h].x > 0.f ? r[h].x : fmaf(p.alpha, ex, -p.alpha);
+                r[h].y = r[h].y > 0.f ? r[h].y : fmaf(p.alpha, ey, -p.alpha);
+              } else if (act == VXB_ACT_SIGMOID) {
+                r[h].x = fast_sigmoid(r[h].x);
+                r[h].y = fast_sigmoid(r[h].y);
+              }
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const float4 h4 = *reinterpret_cast<const float4 *>(s_head + j * cpad + col + 4 * i4);
-              hsum[j] = fmaf(r[0], h4.x, hsum[j]);
-              hsum[j] = fmaf(r[1], h4.y, hsum[j]);
-              hsum[j] = fmaf(r[2], h4.z, hsum[j]);
-              hsum[j] = fmaf(r[3], h4.w, hsum[j]);
+              const float4 hw = *reinterpret_cast<const float4 *>(s_head + j * cpad + col + 4 * i4);
+              hs2[j] = ffma2(r[0], make_float2(hw.x, hw.y), hs2[j]);
+              hs2[j] = ffma2(r[1], make_float2(hw.z, hw.w), hs2[j]);
             }
           }
           if (c_ == col_items - 1) {
@@ -1401,10 +1414,11 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
 #pragma unroll
               for (int j = 0; j < 4; ++j)
                 if (j < p.head_cout)
-                  op[j * hv.s[1]] = apply_act(hsum[j] + p.head_b[j], p.head_act, p.head_alpha);
+                  op[j * hv.s[1]] =
+                      apply_act(hs2[j].x + hs2[j].y + p.head_b[j], p.head_act, p.head_alpha);
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) hsum[j] = 0.f;
+            for (int j = 0; j < 4; ++j) hs2[j] = make_float2(0.f, 0.f);
           }
         };
         uint32_t ra[16], rb[16];
