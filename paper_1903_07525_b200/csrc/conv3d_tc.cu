@@ -283,7 +283,7 @@ constexpr int TINFO = 16;
 
 // Byte offsets inside the dynamic smem block (all derivable from p).
 struct SmemMap {
-  uint32_t a, b, stg, bias, scale, head, ltab, bars;
+  uint32_t a, b, stg, bias, scale, head, hpart, ltab, bars;
 };
 __host__ __device__ inline SmemMap smem_map(const TcParams &p) {
   SmemMap m;
@@ -294,7 +294,9 @@ __host__ __device__ inline SmemMap smem_map(const TcParams &p) {
   const uint32_t cpad = p.n_tiles * p.nt;
   m.scale = m.bias + cpad * 4;
   m.head = m.scale + cpad * 4;                 // fused head weights [head_cout][cpad]
-  m.ltab = (m.head + (p.head_cout > 0 ? 4 * cpad * 4 : 0) + 15) & ~15u;
+  // fused head: per-row partial dot products of every column item [item][row]
+  m.hpart = (m.head + (p.head_cout > 0 ? 4 * cpad * 4 : 0) + 15) & ~15u;
+  m.ltab = m.hpart + (p.head_cout > 0 ? p.bx * (p.nt >> 4) * 128 * 16 : 0);
   m.bars = m.ltab + (p.lean ? LEAN_TAB * sizeof(LeanEnt) + TINFO * sizeof(TileInfo) : 0);
   return m;
 }
@@ -1351,26 +1353,24 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       };
 
       if constexpr (HEAD) {
-        // fused 1x1x1 head: this warp takes whole slices (every column item
-        // of a slice), so each thread holds all fmaps of its voxel; the
-        // activated values feed head_cout dot products and are never stored
-        // Items run slice-major per warp (every column item of a slice in a
-        // row, so the head sums stay in registers) through the same software
-        // pipeline as the plain epilogue: the TMEM load of the next item and
-        // the residual loads two items ahead are in flight while an item is
-        // finished.
+        // Fused 1x1x1 head.  (1) Column items run balanced over the epilogue
+        // warps through the plain epilogue's pipeline (TMEM load of the next
+        // item and residual loads two items ahead in flight); each item's
+        // activated values feed head_cout partial dot products over its 16
+        // fmaps (even / odd fmap pairs, FFMA2), written to smem as one float4
+        // per row.  (2) After a barrier of the epilogue warps, the warps owning
+        // a slice fold its items' partials in column order, add the head bias,
+        // activate and store the fp32 network output; a second barrier frees
+        // the partials for the next tile.  The activated values are never
+        // stored.
         const EpiView &hv = p.head_out;
-        auto adv = [&](int &s_, int &c_) {
-          if (++c_ == col_items) {
-            c_ = 0;
-            s_ += NSUB;
-          }
-        };
-        // head sums as even / odd channel pairs (FFMA2), folded at the store
-        float2 hs2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                         make_float2(0.f, 0.f)};
-        auto head_item = [&](int s_, int c_, const uint32_t (&rv)[16], const float (&bq)[16]) {
-          const int col = tc.nt * p.nt + c_ * 16;
+        float4 *hpart = reinterpret_cast<float4 *>(smem + sm.hpart);   // [slice][item][row]
+        auto head_item = [&](int item, const uint32_t (&rv)[16], const float (&bq)[16]) {
+          int s_, cc;
+          split_item(item, s_, cc);
+          const int col = tc.nt * p.nt + cc;
+          float2 hs2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                           make_float2(0.f, 0.f)};
 #pragma unroll
           for (int i4 = 0; i4 < 4; ++i4) {
             const float4 b4 = *reinterpret_cast<const float4 *>(s_bias + col + 4 * i4);
@@ -1406,57 +1406,61 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
               hs2[j] = ffma2(r[1], make_float2(hw.z, hw.w), hs2[j]);
             }
           }
-          if (c_ == col_items - 1) {
-            const int x = sc0 + s_;
-            if (yz_ok && x < slim) {
-              float *op = static_cast<float *>(hv.data) + tc.b * hv.s[0] + rc * hv.s[ra_dim] +
-                          z * hv.s[4] + x * hv.s[sl_dim];
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                if (j < p.head_cout)
-                  op[j * hv.s[1]] =
-                      apply_act(hs2[j].x + hs2[j].y + p.head_b[j], p.head_act, p.head_alpha);
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) hs2[j] = make_float2(0.f, 0.f);
-          }
+          hpart[item * 128 + row] = make_float4(hs2[0].x + hs2[0].y, hs2[1].x + hs2[1].y,
+                                                hs2[2].x + hs2[2].y, hs2[3].x + hs2[3].y);
         };
         uint32_t ra[16], rb[16];
         uint4 qa[2], qb[2];
         float bq[16];
-        int s0 = sub, c0 = 0, s1 = sub, c1 = 0;   // items A (s0, c0) and B (s1, c1)
-        adv(s1, c1);
+        int item = sub;
         if (braw) {
-          if (s0 < p.bx) base_issue(s0 * col_items + c0, qa);
-          if (s1 < p.bx) base_issue(s1 * col_items + c1, qb);
+          if (item < items) base_issue(item, qa);
+          if (item + NSUB < items) base_issue(item + NSUB, qb);
         }
         mbar_wait_sleep(&t_full[acc], ((p.acc_stages == 2 ? (it >> 1) : it) & 1));
         tc_fence_after();
-        if (s0 < p.bx) tmem_ld16_issue(taddr_of(s0 * col_items + c0), ra);
-        while (s0 < p.bx) {
+        if (item < items) tmem_ld16_issue(taddr_of(item), ra);
+        while (item < items) {
+          const int nxt = item + NSUB;
           tmem_wait_ld16(ra);
-          if (s1 < p.bx) tmem_ld16_issue(taddr_of(s1 * col_items + c1), rb);
-          if (BASE) base_get(s0 * col_items + c0, qa, bq);
-          head_item(s0, c0, ra, bq);
-          int s2 = s1, c2 = c1;                      // next A
-          adv(s2, c2);
-          if (braw && s2 < p.bx) base_issue(s2 * col_items + c2, qa);
-          if (s1 >= p.bx) break;
+          if (nxt < items) tmem_ld16_issue(taddr_of(nxt), rb);
+          if (BASE) base_get(item, qa, bq);
+          head_item(item, ra, bq);
+          if (braw && item + 2 * NSUB < items) base_issue(item + 2 * NSUB, qa);
+          if (nxt >= items) break;
+          const int nn = nxt + NSUB;
           tmem_wait_ld16(rb);
-          if (s2 < p.bx) tmem_ld16_issue(taddr_of(s2 * col_items + c2), ra);
-          if (BASE) base_get(s1 * col_items + c1, qb, bq);
-          head_item(s1, c1, rb, bq);
-          int s3 = s2, c3 = c2;                      // next B
-          adv(s3, c3);
-          if (braw && s3 < p.bx) base_issue(s3 * col_items + c3, qb);
-          s0 = s2;
-          c0 = c2;
-          s1 = s3;
-          c1 = c3;
+          if (nn < items) tmem_ld16_issue(taddr_of(nn), ra);
+          if (BASE) base_get(nxt, qb, bq);
+          head_item(nxt, rb, bq);
+          if (braw && nxt + 2 * NSUB < items) base_issue(nxt + 2 * NSUB, qb);
+          item = nn;
         }
+        // the accumulator stage is free for the next tile's MMAs
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&t_empty[acc]);
+        named_bar_sync(1, EPI_WARPS * 32);
+        for (int s_ = sub; s_ < p.bx; s_ += NSUB) {
+          float hsum[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int c_ = 0; c_ < col_items; ++c_) {
+            const float4 v = hpart[(s_ * col_items + c_) * 128 + row];
+            hsum[0] += v.x;
+            hsum[1] += v.y;
+            hsum[2] += v.z;
+            hsum[3] += v.w;
+          }
+          const int x = sc0 + s_;
+          if (yz_ok && x < slim) {
+            float *op = static_cast<float *>(hv.data) + tc.b * hv.s[0] + rc * hv.s[ra_dim] +
+                        z * hv.s[4] + x * hv.s[sl_dim];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (j < p.head_cout)
+                op[j * hv.s[1]] = apply_act(hsum[j] + p.head_b[j], p.head_act, p.head_alpha);
+          }
+        }
+        named_bar_sync(1, EPI_WARPS * 32);   // partials free for the next tile
         continue;
       }
       uint32_t ra[16], rb[16];

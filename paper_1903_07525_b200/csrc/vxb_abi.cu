@@ -567,8 +567,9 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
   const bool can_pair = (!L.fold || fold_pair) && !a.pool && !a.head_cout && spatial_min >= 2 &&
                         L.nt % 16 == 0 && L.nt / 8 <= 256 && out_ok &&
                         (pair_env == 1 || pair_env == 2);
-  // a fused head keeps its weights in smem: 4 rows x the padded fmaps
-  const int head_smem = a.head_cout ? 4 * L.n_tiles * L.nt * 4 : 0;
+  // a fused head keeps its weights in smem (4 rows x the padded fmaps) and
+  // one float4 partial per row and column item of a tile (<= 8 slices)
+  const int head_smem = a.head_cout ? 4 * L.n_tiles * L.nt * 4 + 8 * (L.nt / 16) * 128 * 16 : 0;
   int rc = tc_configure(L, a.k, slice_y ? a.oy : a.ox, other_tiles, sms, a.reps,
                         stg_bytes + head_smem, f32in, can_pair && !(fold_pair && a.head_cout), pair_env,
                         fold_pair && !a.head_cout, c);

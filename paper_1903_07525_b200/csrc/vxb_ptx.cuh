@@ -608,3 +608,10 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   return r;
 }
 }  // namespace vxb
+
+namespace vxb {
+// named barrier among `count` threads (warps of one role), id >= 1
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+}  // namespace vxb
