@@ -226,18 +226,22 @@ class DeviceTiler:
         n = int(streams if streams is not None else os.environ.get("VOXPLAN_STREAMS", "1"))
         # patches per launch: the deep U-net levels of several patches share
         # one kernel (their few output tiles alone leave most SMs idle).
-        # Config-5 volume, 2 streams: 1 -> 170.6 ms, 2 -> 149.9, 3 -> 138.4,
-        # 4 -> 131.5, 6 -> 127.1, 8 -> 124.1, 12 -> 123.5, 16 -> 123.1 ms
-        # (tools/sweep_batch.sh; one stream is ~1 % slower at every batch).
-        # 12 divides the 36 tiles of a config-5 x-row, so the streamed
-        # run_host (row by row) never runs a short, padded batch.  Runner
+        # Config-5 volume (round 1 kernels, 2 streams): 1 -> 170.6 ms,
+        # 4 -> 131.5, 8 -> 124.1, 12 -> 123.5, 16 -> 123.1 ms; with the round-2
+        # epilogues (1 stream): 12 -> 111.3, 18 -> 109.8, 24 -> 108.8,
+        # 36 -> 108.4, 72 -> 106.9, 96 -> 106.5 ms (tools/ab_bench5.sh).  36
+        # is one x-row of config 5's (8,6,6) tile grid, the largest batch the
+        # streamed run_host (row by row) can form without padding.  Runner
         # streams: with the lean epilogue and no PDL inside the batches, one
         # stream measured 116.2 ms vs 116.9 ms for two (the persistent convs
         # fill every SM, so a second stream only interleaves), and a single
         # stream keeps the in-step kernel timing free of the other stream's
         # work.
         self.batch = max(1, int(batch if batch is not None else
-                                os.environ.get("VOXPLAN_PATCH_BATCH", "12")))
+                                os.environ.get("VOXPLAN_PATCH_BATCH", "36")))
+        if batch is None:
+            # never more than one x-row of this grid (no padded batches)
+            self.batch = min(self.batch, max(len(r) for r in self.rows(list(grid.tiles))))
         self.vol_batch = int(plan.inputs[0][2][0])
         if self.vol_batch != 1:
             self.batch = 1                 # the volume's own batch already fills the plan
@@ -514,7 +518,7 @@ def device_tiler(plan, grid: TileGrid, device, backend=None, slot=0) -> DeviceTi
     captured graphs; two workers on the same device get separate tilers."""
     key = (id(plan), grid.patch_in, grid.volume_in, grid.overlap, str(device), int(slot),
            repr(backend),
-           os.environ.get("VOXPLAN_PATCH_BATCH", "12"), os.environ.get("VOXPLAN_STREAMS", "1"))
+           os.environ.get("VOXPLAN_PATCH_BATCH", "36"), os.environ.get("VOXPLAN_STREAMS", "1"))
     with _TILER_LOCK:
         hit = _TILER_CACHE.get(key)
         if hit is not None and hit[0] is plan:

@@ -238,7 +238,7 @@ def test_patch_batching_with_batch_aware_n_split(monkeypatch):
         L.vxb_conv_select_shape_b(80, 80, k3, s1, _lib.i3((4, 12, 12)), 12)
     spec, store = C.config5(patch=(4, 24, 24), feats=(16, 80))
     plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
-    vol = np.random.default_rng(3).uniform(0, 1, (1, 1, 8, 72, 48)).astype(np.float32)
+    vol = np.random.default_rng(3).uniform(0, 1, (1, 1, 4, 72, 96)).astype(np.float32)
     grid = P.grid_for(plan, vol.shape[2:], overlap=0)
     assert len(grid.tiles) == 12
     monkeypatch.setenv("VOXPLAN_PATCH_BATCH", "1")
