@@ -276,8 +276,8 @@ constexpr int LEAN_TAB = 16;   // nt <= 256: <= 16 column items
 // TINFO slots, each published with an mbarrier arrive; the producer runs at
 // most na + acc_stages tiles ahead of the epilogue.
 struct TileInfo {
-  long long o_off, b_off;
-  int rc0, z0, sc0, nt0, dummy, pad[3];
+  long long o_off, b_off, p_off;   // output, residual, fused-pool view offsets
+  int rc0, z0, sc0, nt0, dummy, pad[5];
 };
 constexpr int TINFO = 16;
 
@@ -677,7 +677,13 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
                      static_cast<long long>(ti.z0) * p.base.s[4] +
                      static_cast<long long>(ti.sc0) * p.base.s[sl_dim] +
                      (p.rep_n ? 0 : p.base_rep_off[tc.rep]) + (ti.nt0 >> 3) * p.base.s[1];
-          ti.pad[0] = ti.pad[1] = ti.pad[2] = 0;
+          ti.p_off = 0;
+          if (p.pool)   // the pooled tile origin (tiles start at even y, z)
+            ti.p_off = tc.b * p.pool_out.s[0] + static_cast<long long>(ti.sc0) * p.pool_out.s[2] +
+                       static_cast<long long>(ti.rc0 >> 1) * p.pool_out.s[3] +
+                       static_cast<long long>(ti.z0 >> 1) * p.pool_out.s[4] +
+                       (ti.nt0 >> 3) * p.pool_out.s[1];
+          for (int i = 0; i < 5; ++i) ti.pad[i] = 0;
           tinfo[pit & (TINFO - 1)] = ti;
           mbar_arrive(&info_full[pit & (TINFO - 1)]);   // release: the epilogue acquires
         }
@@ -1037,11 +1043,13 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
     // lean: this thread's row offset inside a tile (per kernel)
     const long long ra_oo = LEAN ? ra * ov.s[ra_dim] + zz * ov.s[4] : 0;
     const long long ra_bo = LEAN && BASE ? ra * bvw.s[ra_dim] + zz * bvw.s[4] : 0;
+    // lean + fused pool: lanes with (y, z) both even store the 2x2 max
+    const long long ra_po = LEAN ? (ra >> 1) * p.pool_out.s[3] + (zz >> 1) * p.pool_out.s[4] : 0;
     for (int tile = first_tile; tile < p.total_tiles; tile += tile_step, ++it) {
       TileCoord tc;
       int rc, z, sc0;
       bool yz_ok;
-      long long lo_off = 0, lb_off = 0;
+      long long lo_off = 0, lb_off = 0, lp_off = 0;
       int nt0;
       if constexpr (LEAN) {
         // the producer published this tile's origin (TileInfo ring)
@@ -1055,6 +1063,7 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
         yz_ok = rc < (p.slice_y ? p.ox : p.oy) && z < p.oz && !ti.dummy;
         lo_off = ti.o_off + ra_oo;
         lb_off = ti.b_off + ra_bo;
+        lp_off = ti.p_off + ra_po;
         tc.rep = 0;
         tc.nt = 0;
         tc.b = 0;
@@ -1220,6 +1229,31 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
             }
             __nv_bfloat162 h = __floats2bfloat162_rn(r.x, r.y);
             w[i2] = *reinterpret_cast<uint32_t *>(&h);
+          }
+          if (p.pool) {
+            // MaxPool 1x2x2 / 1x2x2 of the stored values (ops.py:63-86):
+            // rows (y, z) (y, z+1) (y+1, z) (y+1, z+1) are lanes l, l+1,
+            // l+8, l+9; packed-bf16 max, NaN-propagating like np.maximum
+            uint32_t m[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const uint32_t t1 = __shfl_down_sync(0xffffffffu, w[i], 1);
+              const uint32_t t2 = __shfl_down_sync(0xffffffffu, w[i], 8);
+              const uint32_t t3 = __shfl_down_sync(0xffffffffu, w[i], 9);
+              __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162 *>(&w[i]);
+              a = __hmax2_nan(a, *reinterpret_cast<const __nv_bfloat162 *>(&t1));
+              a = __hmax2_nan(a, *reinterpret_cast<const __nv_bfloat162 *>(&t2));
+              a = __hmax2_nan(a, *reinterpret_cast<const __nv_bfloat162 *>(&t3));
+              m[i] = *reinterpret_cast<uint32_t *>(&a);
+            }
+            if ((lane & 9) == 0 && sc0 + s < slim && !tc.dummy && (rc >> 1) < p.pool_oy &&
+                (z >> 1) < p.pool_oz) {
+              __nv_bfloat16 *pp = static_cast<__nv_bfloat16 *>(p.pool_out.data) + lp_off +
+                                  s * p.pool_out.s[2] + (e.ch >> 3) * p.pool_out.s[1];
+              if (c0 < p.cout) *reinterpret_cast<uint4 *>(pp) = make_uint4(m[0], m[1], m[2], m[3]);
+              if (c0 + 8 < p.cout)
+                *reinterpret_cast<uint4 *>(pp + p.pool_out.s[1]) = make_uint4(m[4], m[5], m[6], m[7]);
+            }
           }
           if (yz_ok && sc0 + s < slim) {
             __nv_bfloat16 *o = lo_row + s * ov.s[sl_dim];
@@ -1582,7 +1616,7 @@ static int launch_act(const TcParams &p, const TcMaps &maps, int grid, cudaStrea
                        "fused head: single-CTA tiles, one N tile, no fp32 input / pooling");
     return launch_variant<-1, true, BASE, false, false, false, true>(p, maps, grid, s, smem);
   }
-  if (p.pool) {
+  if (p.pool && !p.lean) {
     if (PAIR || p.f32in || p.out.dtype != VXB_BF16 || !p.out.blocked ||
         p.pool_out.dtype != VXB_BF16 || !p.pool_out.blocked)
       return set_error(VXB_EUNSUPPORTED,

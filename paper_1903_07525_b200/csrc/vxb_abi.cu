@@ -745,7 +745,8 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
   p.act = a.act;
   p.alpha = a.alpha;
   // lean epilogue (conv3d_tc.cu LeanEnt): the common bf16 blocked case
-  p.lean = env_int("VXB_TC_LEAN", 1) && !f32in && !p.pool && !a.head_cout &&
+  p.lean = env_int("VXB_TC_LEAN", 1) && !f32in && !a.head_cout &&
+           (!p.pool || (!p.pair && a.pool_out.dtype == VXB_BF16 && a.pool_out.blocked)) &&
            a.out.dtype == VXB_BF16 && a.out.blocked &&
            (!a.has_base || (a.base.dtype == VXB_BF16 && a.base.blocked)) &&
            (a.act == VXB_ACT_NONE || a.act == VXB_ACT_RELU || a.act == VXB_ACT_ELU) &&

@@ -70,7 +70,7 @@ class PlanRunner:
     """Executes one ExecutionPlan on one B200; reusable, deterministic."""
 
     def __init__(self, plan, backend=None, *, device=None, use_graph=True, fuse_concat=True,
-                 fuse_pool=False, fuse_input=False, fuse_head=True, pdl=None, probe=None):
+                 fuse_pool=True, fuse_input=False, fuse_head=True, pdl=None, probe=None):
         torch = _torch()
         from .backend import resolve_device_backend
         self.backend = resolve_device_backend(backend)
@@ -264,9 +264,9 @@ class PlanRunner:
         tensor-core conv that produces its input: the conv
         writes its output and the pooled output; the pool step disappears.
         Only x-sliced conv tiles (3-deep x kernels, 1x1x1) pool over their
-        (y, z) rows.  Opt-in (fuse_pool=True): measured on config 5 the extra
-        epilogue work (shuffles + second store) costs as much as the HBM-bound
-        pool kernel it replaces, and the pool kernel overlaps via PDL."""
+        (y, z) rows.  On by default since the lean epilogue carries it (round
+        1's generic pooled epilogue cost as much as the HBM-bound pool kernel
+        it replaced); bit-identical to the pool kernel either way."""
         producers = {id(info["out"]): i for i, (_, _, info) in enumerate(self._ops)}
         drop = set()
         for i, (kind, st, info) in enumerate(self._ops):
