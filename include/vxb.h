@@ -270,6 +270,11 @@ int vxb_copy(const vxb_tensor *src, const vxb_tensor *dst, void *stream);
  * (z contiguous) in one launch per 16: the patch gather / scatter of tiled
  * execution (the reference's per-tile numpy slicing, tiling.py:189-237) */
 int vxb_copy_windows(const vxb_tensor *src, const vxb_tensor *dst, int count, void *stream);
+/* vxb_pack_zwin over a batch whose entry b is read from window src[b]
+ * (1-channel fp32 views into one volume): the patch gather of a tiled run
+ * fused into the network's input pack; count == dst->n <= 64 */
+int vxb_pack_zwin_windows(const vxb_tensor *src, int count, const vxb_tensor *dst, int kz, int pz,
+                          void *stream);
 /* vxb_copy with flags.  VXB_COPY_INDEPENDENT: the copy reads nothing the
  * previous kernel in the stream writes and writes nothing it touches (a
  * network-input pack), so it may start beside that kernel instead of after

@@ -136,6 +136,7 @@ SIGNATURES = [
     ("vxb_pad_copy", c_int, [TP, TP, I3, c_void_p]),
     ("vxb_copy", c_int, [TP, TP, c_void_p]),
     ("vxb_copy_windows", c_int, [TP, TP, c_int, c_void_p]),
+    ("vxb_pack_zwin_windows", c_int, [TP, c_int, TP, c_int, c_int, c_void_p]),
     ("vxb_copy_ex", c_int, [TP, TP, c_int, c_void_p]),
     ("vxb_pack_zwin", c_int, [TP, TP, c_int, c_int, c_int, c_void_p]),
     ("vxb_zero", c_int, [TP, c_void_p]),

@@ -638,16 +638,19 @@ __global__ void pack_std_f32_indep_kernel(DView src, DView dst, int trigger) {
 // kernel over kz "channels" (w'(co, l, dx, dy, 0) = w(co, 0, dx, dy, l)):
 // half the K steps of the 1-channel conv, whose 8-lane chunks were 7/8
 // padding.  Each thread writes 4 consecutive z (4 x 16-byte chunks).
-template <bool INDEP>
-__global__ void pack_zwin_kernel(DView src, DView dst, int kz, int pz, int trigger) {
+template <bool INDEP, bool WIN = false>
+__global__ void pack_zwin_kernel(DView src, DView dst, int kz, int pz, int trigger,
+                                 const __grid_constant__ ZwinWindows win) {
   if (!INDEP) pdl_begin();
   else if (trigger) pdl_trigger();
   const int zq = (dst.z + 3) >> 2;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= dst.y * zq) return;
   const int y = i / zq, z0 = (i - y * zq) * 4, x = blockIdx.y, b = blockIdx.z;
-  const float *row = static_cast<const float *>(src.data) + b * src.s[0] + x * src.s[2] +
-                     y * src.s[3];
+  // WIN: batch entry b reads its own window of one source volume (the
+  // patches of a tiled run, gathered while packing)
+  const float *row = static_cast<const float *>(src.data) + (WIN ? win.off[b] : b * src.s[0]) +
+                     x * src.s[2] + y * src.s[3];
   float v[4 + 8 - 1];
 #pragma unroll
   for (int j = 0; j < 11; ++j) {
@@ -791,12 +794,22 @@ int launch_copy_windows(const WinBatch &b, cudaStream_t s) {
 int launch_pack_zwin(const DView &src, const DView &dst, int kz, int pz, cudaStream_t s,
                      bool independent) {
   dim3 g((dst.y * ((dst.z + 3) >> 2) + 127) / 128, dst.x, dst.n);
+  ZwinWindows none;
+  none.off[0] = 0;
   if (independent)
     return check_cuda(launch_pdl_prio(pack_zwin_kernel<true>, g, dim3(128), 0, s, true, src, dst,
-                                      kz, pz, pack_trigger()),
+                                      kz, pz, pack_trigger(), none),
                       "pack_zwin_kernel");
-  return check_cuda(launch_pdl(pack_zwin_kernel<false>, g, dim3(128), 0, s, src, dst, kz, pz, 0),
-                    "pack_zwin_kernel");
+  return check_cuda(
+      launch_pdl(pack_zwin_kernel<false>, g, dim3(128), 0, s, src, dst, kz, pz, 0, none),
+      "pack_zwin_kernel");
+}
+int launch_pack_zwin_windows(const DView &src, const ZwinWindows &w, const DView &dst, int kz,
+                             int pz, cudaStream_t s) {
+  dim3 g((dst.y * ((dst.z + 3) >> 2) + 127) / 128, dst.x, dst.n);
+  return check_cuda(
+      launch_pdl(pack_zwin_kernel<false, true>, g, dim3(128), 0, s, src, dst, kz, pz, 0, w),
+      "pack_zwin_kernel");
 }
 int launch_zero(const DView &dst, cudaStream_t s) {
   return check_cuda(launch_pdl(zero_kernel, grid3(dst, 256), dim3(256), 0, s, dst), "zero_kernel");

@@ -1527,6 +1527,34 @@ int vxb_pack_zwin(const vxb_tensor *src, const vxb_tensor *dst, int kz, int pz, 
                           (flags & VXB_COPY_INDEPENDENT) != 0);
 }
 
+int vxb_pack_zwin_windows(const vxb_tensor *src, int count, const vxb_tensor *dst, int kz, int pz,
+                          void *stream) {
+  int rc;
+  if (!src || !dst || count < 1 || count > ZWIN_MAX || count != dst->n)
+    return set_error(VXB_EINVAL, "pack_zwin_windows: need 1..%d windows, one per dst entry",
+                     ZWIN_MAX);
+  if ((rc = check_view(dst, "pack_zwin_windows.dst"))) return rc;
+  ZwinWindows w;
+  memset(&w, 0, sizeof(w));
+  for (int b = 0; b < count; ++b) {
+    const vxb_tensor &a = src[b];
+    if ((rc = check_view(&a, "pack_zwin_windows.src"))) return rc;
+    if (a.blocked || a.dtype != VXB_F32 || a.c != 1 || a.n != 1 || a.x != src[0].x ||
+        a.y != src[0].y || a.z != src[0].z)
+      return set_error(VXB_EINVAL, "pack_zwin_windows: 1-channel fp32 windows of one shape");
+    for (int i = 2; i < 5; ++i)
+      if (a.s[i] != src[0].s[i])
+        return set_error(VXB_EINVAL, "pack_zwin_windows: windows of one volume (same strides)");
+    w.off[b] = (static_cast<const char *>(a.data) - static_cast<const char *>(src[0].data)) /
+               static_cast<long long>(sizeof(float));
+  }
+  if (!dst->blocked || (dst->dtype != VXB_BF16 && dst->dtype != VXB_BF16X2) || dst->c != kz ||
+      kz < 1 || kz > 8 || pz < 0 || dst->x != src[0].x || dst->y != src[0].y ||
+      dst->z != src[0].z + 2 * pz - kz + 1)
+    return set_error(VXB_EINVAL, "pack_zwin_windows: destination shape");
+  return launch_pack_zwin_windows(to_dview(src[0]), w, to_dview(*dst), kz, pz, as_stream(stream));
+}
+
 int vxb_zero(const vxb_tensor *t, void *stream) {
   int rc;
   if ((rc = check_view(t, "zero"))) return rc;

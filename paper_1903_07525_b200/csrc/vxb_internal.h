@@ -159,6 +159,14 @@ struct WinBatch {
   int count;
 };
 int launch_copy_windows(const WinBatch &b, cudaStream_t s);
+// z-window pack reading one window per batch entry (element offsets into a
+// source volume that shares the view's strides)
+constexpr int ZWIN_MAX = 64;
+struct ZwinWindows {
+  long long off[ZWIN_MAX];
+};
+int launch_pack_zwin_windows(const DView &src, const ZwinWindows &w, const DView &dst, int kz,
+                             int pz, cudaStream_t s);
 int launch_pack_zwin(const DView &src, const DView &dst, int kz, int pz, cudaStream_t s,
                      bool independent);
 int launch_zero(const DView &dst, cudaStream_t s);

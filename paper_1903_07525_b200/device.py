@@ -148,6 +148,20 @@ def copy(src: DTensor, dst: DTensor, stream=None, independent=False) -> None:
         _lib.check(L.vxb_copy(ctypes.byref(s), ctypes.byref(d), h), "vxb_copy")
 
 
+def pack_zwin_windows(windows, dst: DTensor, kz: int, pz: int, stream=None) -> None:
+    """vxb_pack_zwin_windows: batch entry b of ``dst`` packed from the fp32
+    (1, 1, x, y, z) torch view ``windows[b]`` (windows of one volume)."""
+    L = _lib.lib()
+    n = len(windows)
+    srcs = (_lib.VxbTensor * n)()
+    for i, w in enumerate(windows):
+        srcs[i] = standard(w).vxb()
+    d = dst.vxb()
+    _lib.check(L.vxb_pack_zwin_windows(srcs, n, ctypes.byref(d), int(kz), int(pz),
+                                       stream or current_stream_handle()),
+               "vxb_pack_zwin_windows")
+
+
 def pack_zwin(src: DTensor, dst: DTensor, kz: int, pz: int, stream=None,
               independent=False) -> None:
     """vxb_pack_zwin: z-window pack of a 1-channel fp32 input (lane l = z tap l)."""

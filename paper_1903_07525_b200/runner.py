@@ -94,6 +94,8 @@ class PlanRunner:
         if os.environ.get("VXB_FUSE_POOL") is not None:     # experiments
             fuse_pool = os.environ["VXB_FUSE_POOL"] == "1"
         self.fuse_pool = fuse_pool and self.precision == "bf16"
+        if os.environ.get("VXB_FUSE_INPUT") is not None:    # experiments
+            fuse_input = os.environ["VXB_FUSE_INPUT"] == "1"
         self.fuse_input = fuse_input
         self.fuse_head = fuse_head and self.precision in ("bf16", "x3") and \
             os.environ.get("VXB_FUSE_HEAD", "1") == "1"
@@ -397,6 +399,7 @@ class PlanRunner:
                 readers.setdefault(id(info["x"]), []).append((st, info))
         fused_in = {}
         self._zwin = {}       # id(conv info) -> (z-window input tensor, kz, pz)
+        self.zwin_input = None
         for name, v in self._in_values.items():
             rs = readers.get(id(v), [])
             if v.readers == 1 and len(rs) == 1 and self._f32in_ok(name, *rs[0]):
@@ -408,6 +411,7 @@ class PlanRunner:
                 # single-channel input: z taps packed into the chunk lanes
                 xz, kz, pz = zw
                 self._zwin[id(rs[0][1])] = zw
+                self.zwin_input = (name, xz, kz, pz)     # DeviceTiler fuses its gather here
                 calls.append(lambda s=src, d=xz, kz=kz, pz=pz, f=self._indep_flag:
                              _pack_zwin(s, d, kz, pz, independent=f[0]))
                 continue
@@ -609,10 +613,20 @@ class PlanRunner:
             self._replay()
             self.stream.synchronize()
 
-    def launch_raw(self):
+    def launch_raw(self, skip_inputs=False):
         """Launch the network's kernels on the current stream without the
-        graph (for a caller capturing a larger graph around them)."""
-        self._launch_all()
+        graph (for a caller capturing a larger graph around them);
+        ``skip_inputs``: the caller has packed the network inputs itself."""
+        if not skip_inputs:
+            self._launch_all()
+            return
+        L = _lib.lib()
+        prev = L.vxb_set_pdl(-1 if self.pdl is None else int(bool(self.pdl)))
+        try:
+            for c in self._calls[self._n_in_calls:]:
+                c()
+        finally:
+            L.vxb_set_pdl(prev)
 
     def _replay(self):
         torch = _torch()

@@ -376,7 +376,7 @@ class DeviceTiler:
         buffer), the network, one scatter launch (kept windows into the
         output slab).  ``raw``: launch the network's kernels directly (inside
         a capture of the whole volume) instead of replaying its graph."""
-        from .device import copy_windows, current_stream_handle
+        from .device import copy_windows, current_stream_handle, pack_zwin_windows
         torch = self.torch
         B = self.batch
         # rebatched plans (volume batch 1) stack B patches along the batch
@@ -391,12 +391,22 @@ class DeviceTiler:
             xin = r._in_std[self.in_name]
             res = next(iter(r._out_std.values()))
             gather, scatter = self._windows(group, slab, lo, out_slab, olo, xin, res)
+            # inside the volume graph, a z-window network input is packed
+            # straight from the slab windows (the gather fused into the pack)
+            zw = r.zwin_input if (raw and r._n_in_calls == 1 and not nocopy and
+                                  self.vol_batch == 1) else None
+            if zw is not None and zw[0] != self.in_name:
+                zw = None
             with torch.cuda.stream(r.stream):
-                if not nocopy:
+                if zw is not None:
+                    pack_zwin_windows([src for src, _ in gather], zw[1], zw[2], zw[3],
+                                      current_stream_handle())
+                    r.launch_raw(skip_inputs=True)
+                elif not nocopy:
                     copy_windows(gather, current_stream_handle())
-                if raw:
+                if raw and zw is None:
                     r.launch_raw()
-                else:
+                elif not raw:
                     r.run_on_stream({self.in_name: xin})
                 if not nocopy:
                     copy_windows(scatter, current_stream_handle())
