@@ -298,9 +298,10 @@ static int tc_tmem_cols(int bx, int nt, int acc, bool fold_pair) {
 // streamed weights); fold_pair: it is a folded conv that pairs (TMEM layout)
 static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, long long other_tiles,
                         int sms, int reps, int reserved, bool f32in, bool can_pair,
-                        int pair_mode, bool fold_pair, TcConfig &c) {
+                        int pair_mode, bool fold_pair, TcConfig &c, int reserved_per_slice = 0) {
   // room for bias/scale/barriers, plus the fp32-input staging ring if any
-  const int budget = 227 * 1024 - 6144 - reserved;
+  // (and per-slice epilogue scratch: the fused head's partials)
+  const int budget0 = 227 * 1024 - 6144 - reserved;
   c.acc = env_int("VXB_TC_ACC", 2);
   if (c.acc != 1 && c.acc != 2) c.acc = 2;
   int bx_cap = env_int("VXB_TC_BX", 8);
@@ -340,6 +341,7 @@ static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, lon
   int na_cap = f32in ? std::max(2, std::min(4, env_int("VXB_TC_F32IN_NA", 2)))
                         : std::max(2, std::min(6, env_int("VXB_TC_NA", 3)));
   for (;;) {
+    const int budget = budget0 - c.bx * reserved_per_slice;
     const int sx = L.fold == 2 ? TILE_Y : c.bx, sy = L.fold == 2 ? c.bx : TILE_Y;
     const int hx = sx + k[0] - 1, hy = sy + k[1] - 1, hz = TILE_Z + k[2] - 1;
     c.chunk_bytes = hx * hy * hz * 16;
@@ -569,10 +571,11 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
                         (pair_env == 1 || pair_env == 2);
   // a fused head keeps its weights in smem (4 rows x the padded fmaps) and
   // one float4 partial per row and column item of a tile (<= 8 slices)
-  const int head_smem = a.head_cout ? 4 * L.n_tiles * L.nt * 4 + 8 * (L.nt / 16) * 128 * 16 : 0;
+  const int head_smem = a.head_cout ? 4 * L.n_tiles * L.nt * 4 + 16 : 0;
+  const int head_slice = a.head_cout ? (L.nt / 16) * 128 * 16 : 0;
   int rc = tc_configure(L, a.k, slice_y ? a.oy : a.ox, other_tiles, sms, a.reps,
                         stg_bytes + head_smem, f32in, can_pair && !(fold_pair && a.head_cout), pair_env,
-                        fold_pair && !a.head_cout, c);
+                        fold_pair && !a.head_cout, c, head_slice);
   if (rc) return rc;
   TcParams p;
   memset(&p, 0, sizeof(p));
