@@ -608,3 +608,39 @@ def test_deconv_random_shapes_match_oracle(seed):
         want = R.activation(want, act)
     mx, l2 = R.normalized_error(got, want)
     assert mx < BF16_TOL and l2 < 3e-3, (cin, cout, k, stride, n, sp, act, use_base, mx, l2)
+
+
+@pytest.mark.parametrize("seed", range(_FUZZ_N))
+def test_conv_fused_pool_random_shapes(seed):
+    """Seeded random convs with the 1x2x2 max pool fused into the lean
+    epilogue (odd and even y / z extents, batch 1-2, residual, activations):
+    the stored output equals the unfused conv and the pooled output equals
+    the pool kernel on it, bit for bit (ops.py:63-86)."""
+    import torch
+    D, K = _dev()
+    rng = np.random.default_rng(3000 + seed)
+    cin = int(rng.choice([3, 8, 16, 28, 36, 48, 64]))
+    cout = int(rng.choice([8, 16, 28, 36, 48, 64, 80]))
+    k = [(3, 3, 3), (1, 1, 1)][int(rng.integers(2))]
+    pad = tuple(v // 2 for v in k)
+    n = int(rng.integers(1, 3))
+    sp = tuple(int(v) for v in rng.integers([2, 6, 6], [10, 41, 41]))
+    act = [None, "relu", "elu"][int(rng.integers(3))]
+    use_base = bool(rng.integers(2))
+    x = D.to_device_blocked(rng.uniform(-1, 1, (n, cin) + sp).astype(np.float32))
+    w = (rng.standard_normal((cout, cin) + k) * np.sqrt(2.0 / (cin * np.prod(k)))).astype(np.float32)
+    b = (rng.standard_normal(cout) * 0.1).astype(np.float32)
+    base = D.to_device_blocked(rng.uniform(-1, 1, (n, cout) + sp).astype(np.float32)) \
+        if use_base else None
+    scale = rng.uniform(0.5, 1.5, cout).astype(np.float32) if use_base else None
+    pk = K.pack_conv(w, b, base_scale=scale, out_shape=sp)
+    fa = (act, 1.0) if act else None
+    psp = (sp[0], sp[1] // 2, sp[2] // 2)
+    out, ref_out = D.empty_blocked(n, cout, sp), D.empty_blocked(n, cout, sp)
+    pooled, ref_pooled = D.empty_blocked(n, cout, psp), D.empty_blocked(n, cout, psp)
+    K.conv3d(x, pk, out, pad=pad, base=base, fused_act=fa, pool_out=pooled)
+    K.conv3d(x, pk, ref_out, pad=pad, base=base, fused_act=fa)
+    K.pool3d(ref_out, ref_pooled, (1, 2, 2), (1, 2, 2), "max")
+    torch.cuda.synchronize()
+    assert torch.equal(out.t, ref_out.t), (cin, cout, k, n, sp, act, use_base)
+    assert torch.equal(pooled.t, ref_pooled.t), (cin, cout, k, n, sp, act, use_base)
