@@ -249,7 +249,8 @@ class DeviceTiler:
         with torch.cuda.device(self.device):
             # no programmatic dependent launch inside the patch batches
             # (PlanRunner.pdl: 116.9 vs 118.7 ms for the config-5 volume)
-            self.runners = [PlanRunner(bplan, backend=backend, device=self.device, pdl=False,
+            pdl = os.environ.get("VOXPLAN_PDL", "0") == "1"
+            self.runners = [PlanRunner(bplan, backend=backend, device=self.device, pdl=pdl,
                                        probe=probe if i == 0 else None)
                             for i in range(max(1, n))]
             self.copy_in = torch.cuda.Stream(device=self.device)
