@@ -569,16 +569,6 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       for (int i = threadIdx.x; i < 32; i += blockDim.x) reinterpret_cast<uint32_t *>(g)[i] = 0u;
     }
   const int cpad = p.n_tiles * p.nt;
-  for (int c = threadIdx.x; c < cpad; c += blockDim.x) {
-    // taps in N: column -> channel of its tap (z-pair order: see TcParams::zpair)
-    int cr = c;
-    if (p.rep_n) {
-      const int rem = p.zpair ? c % (2 * p.rep_n) : c % p.rep_n;
-      cr = p.zpair ? ((rem >> 4) << 3) + (rem & 7) : rem;
-    }
-    s_bias[c] = cr < p.cout ? p.bias[cr] : 0.f;
-    s_scale[c] = (cr < p.cout && p.scale) ? p.scale[cr] : 1.f;
-  }
   LeanEnt *ltab = reinterpret_cast<LeanEnt *>(smem + sm.ltab);
   TileInfo *tinfo = reinterpret_cast<TileInfo *>(smem + sm.ltab + LEAN_TAB * sizeof(LeanEnt));
   if (LEAN)
@@ -603,11 +593,6 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       e.ch = ch;
       e.pad = 0;
       ltab[ci] = e;
-    }
-  if (HEAD)
-    for (int i = threadIdx.x; i < 4 * cpad; i += blockDim.x) {
-      const int j = i / cpad, c = i - j * cpad;
-      s_head[i] = (j < p.head_cout && c < p.cout) ? p.head_w[j * p.cout + c] : 0.f;
     }
   fence_proxy_async_smem();
 
@@ -1020,6 +1005,28 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
     // Work item = (slice, 16 accumulator columns).  The TMEM load of item k+1
     // and the residual loads of items k+1, k+2 are in flight while item k is
     // finished (software pipeline).
+    // per-fmap epilogue vectors (bias, residual scale, head weights) are
+    // staged by the epilogue warps only, after the CTA-wide setup, so their
+    // global-memory latency overlaps the first tile's loads and MMAs
+    {
+      const int et = threadIdx.x - 96;
+      for (int c = et; c < cpad; c += 32 * EPI_WARPS) {
+        // taps in N: column -> channel of its tap (z-pair order: see TcParams::zpair)
+        int cr = c;
+        if (p.rep_n) {
+          const int rem = p.zpair ? c % (2 * p.rep_n) : c % p.rep_n;
+          cr = p.zpair ? ((rem >> 4) << 3) + (rem & 7) : rem;
+        }
+        s_bias[c] = cr < p.cout ? p.bias[cr] : 0.f;
+        s_scale[c] = (cr < p.cout && p.scale) ? p.scale[cr] : 1.f;
+      }
+      if (HEAD)
+        for (int i = et; i < 4 * cpad; i += 32 * EPI_WARPS) {
+          const int j = i / cpad, c = i - j * cpad;
+          s_head[i] = (j < p.head_cout && c < p.cout) ? p.head_w[j * p.cout + c] : 0.f;
+        }
+      named_bar_sync(2, 32 * EPI_WARPS);
+    }
     const int q = warp & 3;                   // TMEM lane quarter this warp may access
     const int sub = (warp - 3) >> 2;          // which share of the work items
     constexpr int NSUB = EPI_WARPS / 4;
