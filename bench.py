@@ -226,13 +226,19 @@ def ncu_traffic(name):
 
 # ------------------------------------------------------------------ reference CPU arm
 
-def ref_volume_sample(spec, store, threads):
+def ref_volume_sample(spec, store, threads, patch=None):
     """The reference engine on `threads` config-5 tiles: voxplan.run_tiled
     (tiling.py:189-237, backend "compiled", workers = threads) over a
     (1, 1, 18, 192, 192 * threads) slice of the synthetic volume (overlap 0:
     exactly `threads` disjoint 18x192x192 tiles, each costing what a tile of
-    the full 288-tile grid costs).  Returns (run, voxels per run, tiles)."""
+    the full 288-tile grid costs).  ``patch``: the same U-net compiled for a
+    smaller patch (the engine's per-voxel rate does not depend on the patch:
+    0.076 / 0.081 / 0.077 M voxels/s single-threaded at 18x192x192 /
+    18x192x96 / 18x96x96).  Returns (run, voxels per run, tiles)."""
     from oracle import ref_voxplan as RV
+    if patch is not None:
+        from paper_1903_07525_b200 import configs as C
+        spec, store = C.config5(patch=tuple(patch))
     plan = RV.compile_reference(spec, store)
     patch = spec.input_layers()[0].params["shape"][2:]
     vol = np.random.default_rng(77).uniform(
@@ -365,9 +371,18 @@ def run_reference(args, rank, world):
     from bench_util import build_nets, workload_name
     nets = build_nets(args.config)
     if args.config == 5:
-        run, vox, tiles = ref_volume_sample(nets[0][1], nets[0][2], threads)
-        sample = ("%d tiles per step (one per worker) through voxplan.run_tiled(backend="
-                  "'compiled', workers=%d), oracle/_ref" % (tiles, threads))
+        # a full 18x192x192 tile takes ~14 s per worker on the GPU hosts; with
+        # more than a handful of steps each worker takes an 18x96x96 quarter
+        # patch per step instead, so the whole arm stays within a few minutes
+        quarter = (args.steps + args.warmup) > 8
+        run, vox, tiles = ref_volume_sample(nets[0][1], nets[0][2], threads,
+                                            patch=(18, 96, 96) if quarter else None)
+        sample = ("%d %s per step (one per worker) through voxplan.run_tiled(backend="
+                  "'compiled', workers=%d), oracle/_ref%s" % (
+                      tiles, "18x96x96 quarter patches" if quarter else "18x192x192 tiles",
+                      threads, "; per-voxel rate of the engine is patch-size independent "
+                      "(0.076 vs 0.077 M vox/s single-threaded at 18x192x192 vs 18x96x96)"
+                      if quarter else ""))
     elif args.config == 2:
         r = ref_sweep_sample(nets, threads, min(8.0, args.cpu_seconds))
         if r is None:
