@@ -387,3 +387,19 @@ def test_fused_head_matches_unfused(cfg, backend):
     else:
         assert R.normalized_error(a, b)[0] < 2e-2
         assert mx < {4: 3e-2, 5: 4e-2}[cfg] and l2 < 2.5e-2, (mx, l2)
+
+
+def test_run_tiled_volume_batch_2():
+    """A plan whose own batch is 2 tiles a (2, 1, x, y, z) volume (tiling.py:
+    189-237 accepts any plan batch): every batch entry equals the batch-1
+    plan tiled over that entry alone, bit for bit."""
+    from paper_1903_07525_b200.plan import rebatch
+    spec, store = C.config5(patch=(4, 32, 32), feats=(8, 12, 16))
+    plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
+    plan2 = rebatch(plan, 2)
+    vol = np.random.default_rng(5).uniform(0, 1, (2, 1, 7, 80, 70)).astype(np.float32)
+    got = P.run_tiled(plan2, vol, overlap=0)
+    assert got.shape[0] == 2
+    for b in range(2):
+        want = P.run_tiled(plan, vol[b:b + 1], overlap=0)
+        np.testing.assert_array_equal(got[b:b + 1], want)
