@@ -395,7 +395,7 @@ class DeviceTiler:
             # inside the volume graph, a z-window network input is packed
             # straight from the slab windows (the gather fused into the pack)
             zw = r.zwin_input if (raw and r._n_in_calls == 1 and not nocopy and
-                                  self.vol_batch == 1) else None
+                                  self.vol_batch == 1 and B <= 64) else None   # ZWIN_MAX
             if zw is not None and zw[0] != self.in_name:
                 zw = None
             with torch.cuda.stream(r.stream):
