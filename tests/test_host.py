@@ -259,3 +259,39 @@ def test_gather_volume_gloo_assembles_exactly_once(world):
     assert not np.isnan(full).any()
     np.testing.assert_array_equal(full[0, 0], want)
     np.testing.assert_array_equal(full[0, 1], want + 1e6)
+
+
+def test_tiler_windows_and_row_batches():
+    """DeviceTiler's batch geometry on the host (CPU tensors, no CUDA): the
+    gather windows of a batch are exactly each tile's input window of the
+    slab, the scatter windows each tile's kept output window, a short last
+    group repeats its last tile for the gather only, and batches never span
+    more than one x-row of the grid."""
+    import torch
+    grid = tiling.plan_tiles((9, 40, 30), (4, 16, 16), (4, 16, 16), overlap=0)
+    rows = tiling.DeviceTiler.rows(list(grid.tiles))
+    assert sum(len(r) for r in rows) == len(grid.tiles)
+    assert all(len({t.in_lo[0] for t in r}) == 1 for r in rows)
+    dt = object.__new__(tiling.DeviceTiler)      # geometry only: no runners
+    dt.grid, dt.batch, dt.vol_batch = grid, 4, 1
+    vol = torch.arange(9 * 40 * 30, dtype=torch.float32).reshape(1, 1, 9, 40, 30)
+    lo, hi, olo, ohi = tiling.slab_bounds(grid, grid.tiles)
+    slab = vol[(slice(None), slice(None)) + tuple(slice(a, b) for a, b in zip(lo, hi))]
+    out_slab = torch.zeros((1, 2) + tuple(b - a for a, b in zip(olo, ohi)))
+    xin = torch.zeros((4, 1) + tuple(grid.patch_in))
+    res = torch.arange(4 * 2 * int(np.prod(grid.patch_in)), dtype=torch.float32).reshape(
+        (4, 2) + tuple(grid.patch_in))
+    group = list(grid.tiles[:3])                  # short group of 3 in a batch of 4
+    gather, scatter = dt._windows(group, slab, lo, out_slab, olo, xin, res)
+    assert len(gather) == 4 and len(scatter) == 3
+    for b, (src, dst) in enumerate(gather):
+        t = group[min(b, 2)]
+        want = vol[(slice(None), slice(None)) + t.input_window(grid.patch_in)]
+        assert torch.equal(src, want) and dst.shape == want.shape
+    for b, (src, dst) in enumerate(scatter):
+        t = group[b]
+        assert torch.equal(src, res[(slice(b, b + 1), slice(None)) + t.local_window])
+        dst.copy_(src)
+        full = torch.zeros((1, 2, 9, 40, 30))
+        full[(slice(None), slice(None)) + tuple(slice(a, b) for a, b in zip(olo, ohi))] = out_slab
+        assert torch.equal(full[(slice(None), slice(None)) + t.out_window], src)
