@@ -231,47 +231,61 @@ def bench_network(cfg, args, dev, peaks, flush, *, with_cpu, with_e2e, headline=
     import torch
     import paper_1903_07525_b200 as P
     nets = build_nets(cfg)
-    runners, plans = [], []
+    runners, plans, probed = [], [], []
     for name, spec, store, x in nets:
         plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
         plans.append(plan)
-        probe = _dominant(plan)[0] if cfg != 2 else None
-        r = P.PlanRunner(plan, backend="b200", device=dev, probe=probe)
-        xd = r.input_buffers()
-        xd[plan.inputs[0][0]].copy_(torch.from_numpy(x))
+        r = P.PlanRunner(plan, backend="b200", device=dev)
+        r.input_buffers()[plan.inputs[0][0]].copy_(torch.from_numpy(x))
         runners.append(r)
-    batch = None
+        if cfg != 2:
+            # the same plan with external timing events around its dominant
+            # conv: the event nodes split the graph (config 1: 20 -> 35 us per
+            # step), so `value` is timed on the plain runner and the roofline
+            # kernel in a second pass of probed steps
+            rp = P.PlanRunner(plan, backend="b200", device=dev, probe=_dominant(plan)[0])
+            rp.input_buffers()[plan.inputs[0][0]].copy_(torch.from_numpy(x))
+            probed.append(rp)
+    batch = batch_probe = None
     if cfg == 2:
         doms = [(_dominant(p)[1], i) for i, p in enumerate(plans)]
         dom_i = max(doms)[1]
-        batch = P.PlanBatch(runners, probe=dom_i)
+        batch = P.PlanBatch(runners)
+        batch_probe = P.PlanBatch(runners, probe=dom_i)
     steps = args.steps if headline else max(3, min(args.steps, 20))
-    stream = batch.stream if batch is not None else runners[0].stream
     cs = torch.cuda.current_stream(dev)
 
-    def step():
+    def step(with_probe=False):
         if batch is not None:
-            batch.run_device()
+            (batch_probe if with_probe else batch).run_device()
         else:
-            runners[0].run_device(runners[0].input_buffers())
+            r = probed[0] if with_probe else runners[0]
+            r.run_device(r.input_buffers())
 
-    for _ in range(max(3, args.warmup)):
-        step()
-    _sync_barrier(dev, dist)
-    tot, probe = 0.0, []
-    with ClockSampler(dev.index) as clk:
-        for _ in range(steps):
-            flush.fill_(1.0)
-            _sync_barrier(dev, dist)
-            torch.cuda._sleep(200_000)               # keep the window device-bound
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(cs)
-            step()
-            e1.record(cs)
-            torch.cuda.synchronize(dev)
-            tot += e0.elapsed_time(e1)
-            probe.append(batch.probe_ms() if batch is not None else runners[0].probe_ms())
-    del stream
+    def timed(with_probe):
+        for _ in range(max(3, args.warmup)):
+            step(with_probe)
+        _sync_barrier(dev, dist)
+        tot, probe = 0.0, []
+        with ClockSampler(dev.index) as clk:
+            for _ in range(steps):
+                flush.fill_(1.0)
+                _sync_barrier(dev, dist)
+                torch.cuda._sleep(200_000)               # keep the window device-bound
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(cs)
+                step(with_probe)
+                e1.record(cs)
+                torch.cuda.synchronize(dev)
+                tot += e0.elapsed_time(e1)
+                if with_probe:
+                    probe.append(batch_probe.probe_ms() if batch is not None
+                                 else probed[0].probe_ms())
+        return tot, probe, clk
+
+    tot, _, clk = timed(False)
+    tot_probed, probe, _ = timed(True)
     tot = _max_over_ranks(tot, dev, dist)
     ms = tot / steps
     vox = sum(output_voxels(s) for _, s, _, _ in nets)
@@ -289,7 +303,9 @@ def bench_network(cfg, args, dev, peaks, flush, *, with_cpu, with_e2e, headline=
     roof.update({"kernel": "conv3d_tc_kernel (%s/%s)" % (dname, dn), "ms_per_launch": pms,
                  "alg_flops": df, "alg_bytes": db,
                  "timing": "in-step: external CUDA events captured around the launch in the "
-                           "graph, every timed step",
+                           "graph, in a second pass of %d flushed steps (%.4f ms per step with "
+                           "the event nodes; `value` is timed on the same graph without "
+                           "them)" % (steps, tot_probed / steps),
                  "peak_source": peaks["source"] + ", burst", "traffic": ncu_traffic(dname)})
     res = {"value": vox * world / (ms * 1e-3), "unit": "output voxels/s", "ms_per_step": ms,
            "steps": steps, "tflops": flops * world / (ms * 1e-3) / 1e12,
