@@ -315,6 +315,8 @@ def bench_network(cfg, args, dev, peaks, flush, *, with_cpu, with_e2e, headline=
            "gpu_launches": sum(r.launches for r in runners) * steps,
            "clocks": clk.summary(), "parity": _parity("cfg%d" % cfg if cfg != 2 else
                                                       "cfg2_c128_k333", "b200")}
+    if cfg == 2:
+        res["layers"] = sweep_layers(nets, plans, dev, peaks, flush)
     if with_e2e:
         res["e2e"] = e2e_runners(runners, nets, steps, dev, dist, world)
     if with_cpu and cpu_fn is not None:
@@ -329,6 +331,38 @@ def bench_network(cfg, args, dev, peaks, flush, *, with_cpu, with_e2e, headline=
                                      "timed region"}})
         res["metric"] = METRIC
     return res
+
+
+def sweep_layers(nets, plans, dev, peaks, flush, reps=8):
+    """Config 2, layer by layer: each network (input pack + conv) replayed
+    alone after an L2 flush, its conv timed by external events inside the
+    graph; roofline fraction of every layer (tensor or HBM bound)."""
+    import torch
+    import paper_1903_07525_b200 as P
+    out = []
+    cs = torch.cuda.current_stream(dev)
+    for (name, _, _, x), plan in zip(nets, plans):
+        dn, df, db = _dominant(plan)
+        r = P.PlanRunner(plan, backend="b200", device=dev, probe=dn)
+        r.input_buffers()[plan.inputs[0][0]].copy_(torch.from_numpy(x))
+        for _ in range(3):
+            r.run_device(r.input_buffers())
+        torch.cuda.synchronize(dev)
+        t = []
+        for _ in range(reps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize(dev)
+            torch.cuda._sleep(200_000)
+            r.run_device(r.input_buffers())
+            cs.synchronize()
+            torch.cuda.synchronize(dev)
+            t.append(r.probe_ms())
+        ms = float(np.median(t))
+        roof = roof_of(df, db, ms, peaks, "bf16")
+        out.append({"layer": name, "us": ms * 1e3, "bound": roof["bound"],
+                    "achieved": roof["achieved"], "unit": roof["unit"], "frac": roof["frac"]})
+        del r
+    return out
 
 
 def e2e_runners(runners, nets, steps, dev, dist, world):

@@ -913,7 +913,9 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
         switch (p.bx) {
           case 1: tiles(I1{}, K0{}); break;
           case 2: tiles(I2{}, K0{}); break;
+          case 3: tiles(I3{}, K0{}); break;
           case 4: tiles(I4{}, K0{}); break;
+          case 6: tiles(I6{}, K0{}); break;
           default: tiles(I8{}, K0{}); break;
         }
       }
@@ -1033,7 +1035,6 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
     const int row = q * 32 + lane;            // MMA row == TMEM lane
     const int ra = row >> 3, zz = row & 7;    // row-axis offset (y, or x with slice_y), z
     const int col_items = p.nt >> 4;
-    const int items = p.bx * col_items;
     // item -> (slice, column offset) without a division: items < 2^16, so
     // a multiply-high by ceil(2^32 / col_items) is exact
     const uint32_t cmagic = col_items > 1 ? 0xffffffffu / col_items + 1u : 0u;
@@ -1086,6 +1087,10 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       }
       const int acc = (it & (p.acc_stages - 1));
       const int slim = p.slice_y ? p.oy : p.ox;
+      // only the tile's slices inside the output are finished (a last tile
+      // along the slice axis may hold fewer than bx; 18 = 8 + 8 + 2)
+      const int nsv = tc.dummy ? 0 : min(p.bx, slim - sc0);
+      const int items = nsv * col_items;
       // (replica offsets are added per item: with taps in N (rep_n) every
       // 16-column item belongs to one tap)
       const long long orow = LEAN ? 0 : tc.b * ov.s[0] + rc * ov.s[ra_dim] + z * ov.s[4];
@@ -1482,7 +1487,7 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
         __syncwarp();
         if (lane == 0) mbar_arrive(&t_empty[acc]);
         named_bar_sync(1, EPI_WARPS * 32);
-        for (int s_ = sub; s_ < p.bx; s_ += NSUB) {
+        for (int s_ = sub; s_ < nsv; s_ += NSUB) {
           float hsum[4] = {0.f, 0.f, 0.f, 0.f};
           for (int c_ = 0; c_ < col_items; ++c_) {
             const float4 v = hpart[(s_ * col_items + c_) * 128 + row];

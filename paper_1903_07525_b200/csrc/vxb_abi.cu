@@ -316,7 +316,8 @@ static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, lon
   long long best = -1;
   for (int cand : {8, 6, 4, 3, 2, 1}) {
     if (cand > bx_cap || tc_tmem_cols(cand, L.nt, c.acc, fold_pair) > 512) continue;
-    if (!L.fold && (cand & (cand - 1))) continue;   // unfolded tiles: 1, 2, 4, 8
+    // (unfolded tiles of 3 / 6 slices: VXB_TC_UNF36=0 restores 1, 2, 4, 8)
+    if (!L.fold && (cand & (cand - 1)) && !env_int("VXB_TC_UNF36", 1)) continue;
     long long tiles = static_cast<long long>(ceil_div(slice_extent, cand)) * other_tiles;
     if (fold_pair) tiles = (tiles + 1) / 2 * 2;
     const long long waves = (tiles + sms - 1) / sms;

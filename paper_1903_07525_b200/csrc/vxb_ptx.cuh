@@ -495,10 +495,17 @@ __device__ __forceinline__ void umma_step_elect(uint32_t d, uint32_t a_lo, uint3
                                                 uint32_t b_lo, uint32_t b_hi, uint32_t idesc,
                                                 uint32_t accumulate, uint32_t d_inc,
                                                 uint32_t a_inc) {
-  static_assert(BX == 1 || BX == 2 || BX == 4 || BX == 8, "step width");
+  static_assert(BX == 1 || BX == 2 || BX == 3 || BX == 4 || BX == 6 || BX == 8, "step width");
   if (PAIR) {
     if (BX == 1) asm volatile(VXB_UMMA_HEAD VXB_UMMA_2 "}" VXB_UMMA_OPS);
     if (BX == 2) asm volatile(VXB_UMMA_HEAD VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2 "}" VXB_UMMA_OPS);
+    if (BX == 3)
+      asm volatile(VXB_UMMA_HEAD VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2
+                   "}" VXB_UMMA_OPS);
+    if (BX == 6)
+      asm volatile(VXB_UMMA_HEAD VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2
+                       VXB_UMMA_NEXT VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2
+                   "}" VXB_UMMA_OPS);
     if (BX == 4)
       asm volatile(VXB_UMMA_HEAD VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2 VXB_UMMA_NEXT VXB_UMMA_2
                        VXB_UMMA_NEXT VXB_UMMA_2 "}" VXB_UMMA_OPS);
@@ -509,6 +516,13 @@ __device__ __forceinline__ void umma_step_elect(uint32_t d, uint32_t a_lo, uint3
   } else {
     if (BX == 1) asm volatile(VXB_UMMA_HEAD VXB_UMMA_1 "}" VXB_UMMA_OPS);
     if (BX == 2) asm volatile(VXB_UMMA_HEAD VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1 "}" VXB_UMMA_OPS);
+    if (BX == 3)
+      asm volatile(VXB_UMMA_HEAD VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1
+                   "}" VXB_UMMA_OPS);
+    if (BX == 6)
+      asm volatile(VXB_UMMA_HEAD VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1
+                       VXB_UMMA_NEXT VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1
+                   "}" VXB_UMMA_OPS);
     if (BX == 4)
       asm volatile(VXB_UMMA_HEAD VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1 VXB_UMMA_NEXT VXB_UMMA_1
                        VXB_UMMA_NEXT VXB_UMMA_1 "}" VXB_UMMA_OPS);

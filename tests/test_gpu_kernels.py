@@ -155,6 +155,33 @@ def test_fold_tile_widths(bx, k, pad, monkeypatch):
     assert mx < BF16_TOL and l2 < 3e-3, (mx, l2)
 
 
+@pytest.mark.parametrize("bx", ["1", "2", "3", "4", "6", "8"])
+@pytest.mark.parametrize("c,k,pad,sp", [(28, (1, 3, 3), (0, 1, 1), (18, 33, 20)),
+                                        (36, (1, 1, 1), (0, 0, 0), (18, 16, 24)),
+                                        (128, (3, 3, 3), (1, 1, 1), (7, 16, 8))])
+def test_unfolded_tile_widths_bit_identical(bx, c, k, pad, sp, monkeypatch):
+    """Unfolded tiles of 1..8 slices (config 5's 18-deep axis picks 6, three
+    full tiles; 8 leaves a last tile of 2 valid slices whose other slices the
+    epilogue skips): every output slice accumulates the same K steps in the
+    same order, so all widths agree bit for bit and match the oracle."""
+    rng = np.random.default_rng(c)
+    x = rng.uniform(-1, 1, (2, c) + sp).astype(np.float32)
+    w = (rng.standard_normal((c, c) + k) * 0.1).astype(np.float32)
+    b = rng.standard_normal(c).astype(np.float32)
+    base = rng.uniform(-1, 1, (2, c) + sp).astype(np.float32)
+    scale = rng.uniform(0.5, 1.5, c).astype(np.float32)
+    monkeypatch.setenv("VXB_TC_FOLD", "0")
+    monkeypatch.setenv("VXB_TC_BX", bx)
+    got, _ = _conv_bf16(x, w, b, pad, "elu", base, scale)
+    monkeypatch.setenv("VXB_TC_BX", "8")
+    monkeypatch.setenv("VXB_TC_UNF36", "0")        # power-of-two widths only
+    ref, _ = _conv_bf16(x, w, b, pad, "elu", base, scale)
+    assert np.array_equal(got, ref)
+    want = _ref_bf16(x, w, b, pad, "elu", base, scale)
+    mx, l2 = R.normalized_error(got, want)
+    assert mx < BF16_TOL and l2 < 3e-3, (mx, l2)
+
+
 def test_unfolded_path_for_badly_padded_rows():
     """x = 18 makes y-sliced folding pad 14 of 32 rows: select_shape picks the
     unfolded layout, which must match the oracle (and the folded result)."""
