@@ -280,6 +280,7 @@ struct TileInfo {
   int rc0, z0, sc0, nt0, dummy, pad[5];
 };
 constexpr int TINFO = 16;
+static_assert(6 + MAX_ACC < TINFO, "TileInfo ring: the producer runs <= na + acc stages ahead");
 
 // Byte offsets inside the dynamic smem block (all derivable from p).
 struct SmemMap {
@@ -540,8 +541,8 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
   uint64_t *b_full = a_empty + p.na;
   uint64_t *b_empty = b_full + p.nb_stages;
   uint64_t *t_full = b_empty + p.nb_stages;
-  uint64_t *t_empty = t_full + 2;
-  uint64_t *stg_full = t_empty + 2;                 // F32IN staging ring
+  uint64_t *t_empty = t_full + MAX_ACC;
+  uint64_t *stg_full = t_empty + MAX_ACC;           // F32IN staging ring
   uint64_t *stg_empty = stg_full + p.n_stg;
   uint64_t *info_full = stg_empty + p.n_stg;          // lean: TileInfo ring slots
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(stg_empty + p.n_stg + (p.lean ? TINFO : 0));
@@ -613,7 +614,7 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       mbar_init(&b_full[i], 1);
       mbar_init(&b_empty[i], PAIR ? 1 : p.cluster);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < MAX_ACC; ++i) {
       mbar_init(&t_full[i], 1);
       mbar_init(&t_empty[i], PAIR ? 2 * EPI_WARPS : EPI_WARPS);
     }
@@ -831,9 +832,12 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       auto tiles = [&](auto bx_c, auto kind_c) {
         constexpr int BXV = decltype(bx_c)::value;
         constexpr int KIND = decltype(kind_c)::value;   // 0 plain, 1 folded, 2 folded pair
+        // accumulator stage of tile `it`: it % acc_stages, phase (it / acc_stages) & 1
+        int acc = -1, acc_ph = 1;
         for (int it = 0; it < my_tiles; ++it) {
-          const int acc = (it & (p.acc_stages - 1));
-          mbar_wait(&t_empty[acc], (((p.acc_stages == 2 ? (it >> 1) : it) & 1)) ^ 1);
+          if (++acc == p.acc_stages) acc = 0;
+          if (acc == 0) acc_ph ^= 1;
+          mbar_wait(&t_empty[acc], acc_ph ^ 1);
           tc_fence_after();
           const uint32_t d_base = tmem_base + acc * acc_stride;
           uint32_t accumulate = 0, first = 1;
@@ -1047,6 +1051,7 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
     const int act = ACT >= 0 ? ACT : p.act;
     const bool braw = BASE && bvw.dtype == VXB_BF16 && bvw.blocked;
     int it = 0;
+    int acc = -1, acc_ph = 1;   // accumulator stage it % acc_stages and its phase
     const int ra_dim = p.slice_y ? 2 : 3, sl_dim = p.slice_y ? 3 : 2;
     // lean: this thread's row offset inside a tile (per kernel)
     const long long ra_oo = LEAN ? ra * ov.s[ra_dim] + zz * ov.s[4] : 0;
@@ -1085,7 +1090,8 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
         yz_ok = rc < (p.slice_y ? p.ox : p.oy) && z < p.oz && !tc.dummy;
         nt0 = tc.nt * p.nt;
       }
-      const int acc = (it & (p.acc_stages - 1));
+      if (++acc == p.acc_stages) acc = 0;
+      if (acc == 0) acc_ph ^= 1;
       const int slim = p.slice_y ? p.oy : p.ox;
       // only the tile's slices inside the output are finished (a last tile
       // along the slice axis may hold fewer than bx; 18 = 8 + 8 + 2)
@@ -1221,13 +1227,26 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
           // (packed pairs: FADD2 / FFMA2 / FMUL2 for the bias, the residual and
           // the exponent's scaling -- bit-identical to the scalar forms)
           uint32_t w[8];
+          // the per-fmap vectors are read as 16-byte words (all lanes read
+          // the same address): every LDS is a shared-memory wavefront that
+          // competes with the MMAs' operand reads (C28 1x3x3, 18x768x768:
+          // 338 us with eight 8-byte bias reads per item, 297 us with none)
+          float4 bq[4], sq[4];
+#pragma unroll
+          for (int i4 = 0; i4 < 4; ++i4) {
+            bq[i4] = (p.dbg_mode & 2048) ? make_float4(p.alpha, p.alpha, p.alpha, p.alpha)
+                                         : *reinterpret_cast<const float4 *>(s_bias + col + 4 * i4);
+            if (BASE) sq[i4] = *reinterpret_cast<const float4 *>(s_scale + col + 4 * i4);
+          }
 #pragma unroll
           for (int i2 = 0; i2 < 8; ++i2) {
-            const float2 b2 = *reinterpret_cast<const float2 *>(s_bias + col + 2 * i2);
+            const float2 b2 = (i2 & 1) ? make_float2(bq[i2 >> 1].z, bq[i2 >> 1].w)
+                                       : make_float2(bq[i2 >> 1].x, bq[i2 >> 1].y);
             float2 r = fadd2(make_float2(__uint_as_float(rv[2 * i2]), __uint_as_float(rv[2 * i2 + 1])),
                              b2);
             if (BASE) {
-              const float2 c2 = *reinterpret_cast<const float2 *>(s_scale + col + 2 * i2);
+              const float2 c2 = (i2 & 1) ? make_float2(sq[i2 >> 1].z, sq[i2 >> 1].w)
+                                         : make_float2(sq[i2 >> 1].x, sq[i2 >> 1].y);
               r = ffma2(c2, make_float2(bv[2 * i2], bv[2 * i2 + 1]), r);
             }
             if (ACT == VXB_ACT_RELU) {
@@ -1463,7 +1482,7 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
           if (item < items) base_issue(item, qa);
           if (item + NSUB < items) base_issue(item + NSUB, qb);
         }
-        mbar_wait_sleep(&t_full[acc], ((p.acc_stages == 2 ? (it >> 1) : it) & 1));
+        mbar_wait_sleep(&t_full[acc], static_cast<uint32_t>(acc_ph));
         tc_fence_after();
         if (item < items) tmem_ld16_issue(taddr_of(item), ra);
         while (item < items) {
@@ -1517,7 +1536,7 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
         if (item < items) base_issue(item, qa);
         if (item + NSUB < items) base_issue(item + NSUB, qb);
       }
-      mbar_wait_sleep(&t_full[acc], ((p.acc_stages == 2 ? (it >> 1) : it) & 1));
+      mbar_wait_sleep(&t_full[acc], static_cast<uint32_t>(acc_ph));
       if (warp == 3 && lane == 0) dbg_mark(p, it, 3);
       tc_fence_after();
       if (item < items) tmem_ld16_issue(taddr_of(item), ra);
@@ -1566,7 +1585,8 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
 
 size_t tc_smem_bytes(const TcParams &p) {
   return smem_map(p).bars +
-         (2 * p.na + 2 * p.nb_stages + 4 + 2 * p.n_stg + (p.lean ? TINFO : 0)) * sizeof(uint64_t) +
+         (2 * p.na + 2 * p.nb_stages + 2 * MAX_ACC + 2 * p.n_stg + (p.lean ? TINFO : 0)) *
+             sizeof(uint64_t) +
          16;
 }
 

@@ -12,6 +12,9 @@ constexpr int TILE_Y = 16;        // output tile rows along y per 128-row MMA
 constexpr int TILE_Z = 8;         // output tile along z (one 8-row core-matrix group)
 constexpr int SLAB_ROW_BYTES = 32;  // one B row: 16 bf16 of K
 constexpr int MAX_REPS = 8;
+// TMEM accumulator stages: tiles whose MMAs may run ahead of the epilogue
+// (as many as fit in the 512 TMEM columns, see tc_configure)
+constexpr int MAX_ACC = 6;
 
 // Epilogue view of an output / base tensor, element strides.
 struct EpiView {
