@@ -277,7 +277,9 @@ constexpr int LEAN_TAB = 16;   // nt <= 256: <= 16 column items
 // most na + acc_stages tiles ahead of the epilogue.
 struct TileInfo {
   long long o_off, b_off, p_off;   // output, residual, fused-pool view offsets
-  int rc0, z0, sc0, nt0, dummy, pad[5];
+  int rc0, z0, sc0, nt0, dummy;
+  int ns, slot0;   // streamed fold: slices to finish and the ring slot of the first
+  int pad[3];
 };
 constexpr int TINFO = 16;
 static_assert(6 + MAX_ACC < TINFO, "TileInfo ring: the producer runs <= na + acc stages ahead");
@@ -516,8 +518,95 @@ __device__ __forceinline__ void mma_group_fold_pair(
   }
 }
 
+// Streamed fold (TcParams::stream): one slab of `cnt` <= 8 input slices jmin
+// .. jmin + cnt - 1 (halo coordinates) of a column.  Input slice j carries the
+// taps d in [dlo, dhi] = [max(0, j - S + 1), min(2, j)] to the output slices
+// j - d; their accumulators are consecutive slots of a ring of `slots` TMEM
+// slices starting at (rb + j - dhi) mod slots, so one MMA of N = (dhi - dlo
+// + 1) nt serves them (two where the range wraps around the ring).  Every MMA
+// accumulates: the epilogue leaves each slot zeroed after reading it.  The
+// per-slice operands are worked out once per slab (StreamTab, registers);
+// within a K step the input slices go in stride-3 order so that consecutive
+// MMAs never touch the same slots (no accumulator read-after-write stalls).
+struct StreamCtx {
+  int jmin, cnt, j0, S, rb, slots;
+};
+constexpr int STREAM_BX = 8;
+struct StreamTab {
+  uint32_t d[STREAM_BX], b[STREAM_BX], id[STREAM_BX];   // main MMA: D column, B block offset, idesc
+  // at most two input slices of a slab wrap around the ring: their second
+  // MMA (D column 0): A slice offset, B block offset, idesc (0 = none)
+  uint32_t wa[2], wb[2], wid[2];
+};
+__device__ __forceinline__ void stream_table(const StreamCtx &sc, const uint32_t d0,
+                                             const uint32_t nt, const uint32_t blk_inc,
+                                             const uint32_t slice_inc,
+                                             const uint32_t id1, const uint32_t id2,
+                                             const uint32_t id3, StreamTab &tb) {
+  const int mask = sc.slots - 1;
+  tb.wid[0] = tb.wid[1] = 0u;
+  tb.wa[0] = tb.wa[1] = tb.wb[0] = tb.wb[1] = 0u;
+  int nw = 0;
+#pragma unroll
+  for (int i = 0; i < STREAM_BX; ++i) {
+    const int j = sc.jmin + i;
+    const int dhi = min(2, j), dlo = max(0, j - sc.S + 1);
+    const int nn = dhi - dlo + 1;
+    const int r = (sc.rb + j - dhi) & mask;
+    const int n1 = min(nn, sc.slots - r);
+    tb.d[i] = d0 + r * nt;
+    tb.b[i] = (2 - dhi) * blk_inc;
+    tb.id[i] = n1 == 1 ? id1 : (n1 == 2 ? id2 : id3);
+    if (i < sc.cnt && n1 < nn) {
+      const uint32_t wid = nn - n1 == 1 ? id1 : id2;
+      const uint32_t wb = (2 - dhi + n1) * blk_inc, wa = i * slice_inc;
+      if (nw == 0) {
+        tb.wid[0] = wid;
+        tb.wb[0] = wb;
+        tb.wa[0] = wa;
+      } else {
+        tb.wid[1] = wid;
+        tb.wb[1] = wb;
+        tb.wa[1] = wa;
+      }
+      ++nw;
+    }
+  }
+}
+template <int CNT>
+__device__ __forceinline__ void mma_group_stream(
+    const uint32_t a_lo0, const uint32_t a_hi, const uint32_t b_base0, const uint32_t b_stage_bytes,
+    const uint32_t b_hi, const uint32_t slab_inc, const uint32_t slice_inc, const uint32_t d0,
+    const int steps, const int tz_n, const uint32_t dz_step, const uint32_t a_wrap,
+    const MmaCtx &cx, const StreamTab &tb, int &b_st) {
+  int tz = 0;
+  uint32_t off = 0;
+  for (int s0 = 0; s0 < steps; s0 += cx.bsteps) {
+    const int n = min(cx.bsteps, steps - s0);
+    if (cx.first_tile_iter) mbar_wait(&cx.b_full[b_st], 0);   // resident weights
+    tc_fence_after();
+    uint32_t b_lo = desc_lo(b_base0 + b_st * b_stage_bytes, 128u);
+    for (int i0 = 0; i0 < n; ++i0) {
+      const uint32_t a_lo = a_lo0 + off;
+      umma_stream_step<CNT>(a_lo, a_hi, b_lo, b_hi, slice_inc, tb.d, tb.b, tb.id);
+      if (tb.wid[0]) {
+        umma_bf16_lohi_elect(d0, a_lo + tb.wa[0], a_hi, b_lo + tb.wb[0], b_hi, tb.wid[0], 1u);
+        if (tb.wid[1])
+          umma_bf16_lohi_elect(d0, a_lo + tb.wa[1], a_hi, b_lo + tb.wb[1], b_hi, tb.wid[1], 1u);
+      }
+      b_lo += slab_inc;
+      off += dz_step;
+      if (++tz == tz_n) {
+        tz = 0;
+        off += a_wrap;
+      }
+    }
+    ++b_st;
+  }
+}
+
 template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN, bool POOL = false,
-          bool HEAD = false, bool LEAN = false>
+          bool HEAD = false, bool LEAN = false, bool STREAM = false>
 __global__ void __maxnreg__(VXB_TC_MAXNREG)
     conv3d_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -642,7 +731,66 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
 
   if (warp == 0) {
     // ===================== A producer: halo tiles (TMA 4-D boxes) ==========
-    if (lane == 0) {
+    if (STREAM && lane == 0) {
+      // streamed fold: whole columns, slab by slab along x (no x halo)
+      int a_st = 0, a_ph = 0, pit = 0, rb = 0;
+      const int smask = p.st_slots - 1;
+      for (int col = blockIdx.x; col < p.st_ncols; col += gridDim.x) {
+        const int tz = col % p.tiles_z, q1 = col / p.tiles_z;
+        const int ty = q1 % p.tiles_y, b = q1 / p.tiles_y;
+        const int y0 = ty * TILE_Y, z0 = tz * TILE_Z;
+        int dprev = -1;   // last output slice handed to the epilogue so far
+        for (int t = 0; t < p.st_nslab; ++t, ++pit) {
+          const int jmin = p.st_j0 + t * p.bx;
+          const int cnt = min(p.bx, p.st_nin - t * p.bx);
+          // output slices complete after this slab: all whose last input
+          // slice (s + 2) lies in it, the rest of the column after the last
+          const int dhi = t == p.st_nslab - 1 ? p.ox - 1 : min(p.ox - 1, jmin + cnt - 3);
+          const int dlo = dprev + 1;
+          TileInfo ti;
+          ti.rc0 = y0;
+          ti.z0 = z0;
+          ti.sc0 = dlo;
+          ti.nt0 = 0;
+          ti.dummy = 0;
+          ti.ns = max(0, dhi - dlo + 1);
+          ti.slot0 = (rb + dlo) & smask;
+          dprev = max(dprev, dhi);
+          ti.o_off = b * p.out.s[0] + static_cast<long long>(y0) * p.out.s[3] +
+                     static_cast<long long>(z0) * p.out.s[4] +
+                     static_cast<long long>(dlo) * p.out.s[2] + p.out_rep_off[0];
+          ti.b_off = b * p.base.s[0] + static_cast<long long>(y0) * p.base.s[3] +
+                     static_cast<long long>(z0) * p.base.s[4] +
+                     static_cast<long long>(dlo) * p.base.s[2] + p.base_rep_off[0];
+          ti.p_off = 0;
+          if (p.pool)
+            ti.p_off = b * p.pool_out.s[0] + static_cast<long long>(dlo) * p.pool_out.s[2] +
+                       static_cast<long long>(y0 >> 1) * p.pool_out.s[3] +
+                       static_cast<long long>(z0 >> 1) * p.pool_out.s[4];
+          for (int i = 0; i < 3; ++i) ti.pad[i] = 0;
+          tinfo[pit & (TINFO - 1)] = ti;
+          mbar_arrive(&info_full[pit & (TINFO - 1)]);
+          for (int g = 0; g < p.n_groups; ++g) {
+            GroupInfo gi = group_info(p, g);
+            mbar_wait_sleep(&a_empty[a_st], a_ph ^ 1);
+            if (g == 0) dbg_mark(p, pit, 0);
+            mbar_expect_tx(&a_full[a_st], gi.nch * p.chunk_bytes);
+            const int *off = p.seg_off[gi.seg];
+            const int cx = jmin - p.pad[0] + off[0];
+            const int cy = y0 - p.pad[1] + off[1];
+            const int cz = (z0 - p.pad[2] + off[2]) * LANES;
+            for (int ci = 0; ci < gi.nch; ++ci)
+              tma_load_4d(a_buf + a_st * p.a_stage_bytes + ci * p.chunk_stride, &maps.m[gi.seg],
+                          &a_full[a_st], cz, cy, cx, b * p.seg_bstride[gi.seg] + gi.chunk0 + ci);
+            if (++a_st == p.na) {
+              a_st = 0;
+              a_ph ^= 1;
+            }
+          }
+        }
+        rb = (rb + p.ox) & smask;
+      }
+    } else if (lane == 0) {
       int a_st = 0, a_ph = 0, s_st = 0, s_ph = 0;
       int pit = 0;
       for (int tile = first_tile; tile < p.total_tiles; tile += tile_step, ++pit) {
@@ -669,7 +817,8 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
                        static_cast<long long>(ti.rc0 >> 1) * p.pool_out.s[3] +
                        static_cast<long long>(ti.z0 >> 1) * p.pool_out.s[4] +
                        (ti.nt0 >> 3) * p.pool_out.s[1];
-          for (int i = 0; i < 5; ++i) ti.pad[i] = 0;
+          ti.ns = ti.slot0 = 0;
+          for (int i = 0; i < 3; ++i) ti.pad[i] = 0;
           tinfo[pit & (TINFO - 1)] = ti;
           mbar_arrive(&info_full[pit & (TINFO - 1)]);   // release: the epilogue acquires
         }
@@ -747,7 +896,7 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       const uint32_t slab = static_cast<uint32_t>(p.slab_bytes);
       for (int tile = first_tile; tile < p.total_tiles; tile += tile_step) {
         if (p.resident && tile != first_tile) break;   // resident bank: loaded once
-        TileCoord tc = decode_tile(p, tile);
+        TileCoord tc = decode_tile(p, STREAM ? 0 : tile);
         const uint8_t *wbase = p.w + tc.rep * p.w_rep_stride + tc.nt * p.w_ntile_stride;
         long long step_base = 0;
         for (int g = 0; g < p.n_groups; ++g) {
@@ -824,7 +973,13 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       // divergent, and every MMA operand then goes through R2UR.BROADCAST
       // (~5 extra instructions per MMA, which bounded the N = 128 convs).
       const int my_tiles =
-          first_tile < p.total_tiles ? (p.total_tiles - first_tile + tile_step - 1) / tile_step : 0;
+          STREAM ? (static_cast<int>(blockIdx.x) < p.st_ncols
+                        ? (p.st_ncols - static_cast<int>(blockIdx.x) + tile_step - 1) / tile_step *
+                              p.st_nslab
+                        : 0)
+                 : (first_tile < p.total_tiles
+                        ? (p.total_tiles - first_tile + tile_step - 1) / tile_step
+                        : 0);
       const bool no_mma = (p.dbg_mode & 8) && p.resident;   // debug: epilogue-only timing
       // The tile loop is instantiated per (walk, tile width): the dispatch
       // happens once per kernel, not once per K group (per-group work in the
@@ -834,7 +989,28 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
         constexpr int KIND = decltype(kind_c)::value;   // 0 plain, 1 folded, 2 folded pair
         // accumulator stage of tile `it`: it % acc_stages, phase (it / acc_stages) & 1
         int acc = -1, acc_ph = 1;
+        StreamCtx sc;   // streamed fold: slab within the column, ring base
+        sc.j0 = p.st_j0;
+        sc.S = p.ox;
+        sc.rb = 0;
+        sc.slots = p.st_slots;
+        int st_t = 0;
+        StreamTab stab;
+        if constexpr (KIND == 3) {
+          // the epilogue warps zeroed the accumulator ring (t_full[MAX_ACC - 1])
+          if (my_tiles > 0) mbar_wait(&t_full[MAX_ACC - 1], 0);
+          tc_fence_after();
+        }
         for (int it = 0; it < my_tiles; ++it) {
+          if constexpr (KIND == 3) {
+            // (the slab's operand table was worked out while the previous
+            // slab's MMAs drained: see the end of the loop body)
+            if (it == 0) {
+              sc.jmin = p.st_j0;
+              sc.cnt = min(p.bx, p.st_nin);
+              stream_table(sc, tmem_base, p.nt, blk_inc, slice_inc, id1, id2, id3, stab);
+            }
+          }
           if (++acc == p.acc_stages) acc = 0;
           if (acc == 0) acc_ph ^= 1;
           mbar_wait(&t_empty[acc], acc_ph ^ 1);
@@ -857,7 +1033,23 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
             const uint32_t a_lo0 =
                 desc_lo(a_base0 + a_st * p.a_stage_bytes, pair ? p.chunk_stride : 16u);
             if (!no_mma) {
-              if constexpr (KIND == 2) {
+              if constexpr (KIND == 3) {
+                auto run = [&](auto cnt_c) {
+                  mma_group_stream<decltype(cnt_c)::value>(
+                      a_lo0, a_hi, b_base0, p.b_stage_bytes, b_hi, b_inc, slice_inc, tmem_base,
+                      gi.steps, tz_n, dz_step, fold_stride - tz_n * dz_step, cx, stab, b_st);
+                };
+                switch (sc.cnt) {
+                  case 1: run(std::integral_constant<int, 1>{}); break;
+                  case 2: run(std::integral_constant<int, 2>{}); break;
+                  case 3: run(std::integral_constant<int, 3>{}); break;
+                  case 4: run(std::integral_constant<int, 4>{}); break;
+                  case 5: run(std::integral_constant<int, 5>{}); break;
+                  case 6: run(std::integral_constant<int, 6>{}); break;
+                  case 7: run(std::integral_constant<int, 7>{}); break;
+                  default: run(std::integral_constant<int, 8>{}); break;
+                }
+              } else if constexpr (KIND == 2) {
                 mma_group_fold_pair<BXV>(a_lo0, a_hi, b_base0, p.b_stage_bytes, b_hi, b_inc,
                                          slice_inc, d_base, p.nt, idp, gi.steps, tz_n, dz_step,
                                          fold_stride - tz_n * dz_step, cx, b_st, b_ph, first);
@@ -889,6 +1081,16 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
             dbg_mark(p, it, 2);
             dbg_clock(p, it, 6);
           }
+          if constexpr (KIND == 3) {
+            if (++st_t == p.st_nslab) {
+              st_t = 0;
+              sc.rb = (sc.rb + p.ox) & (p.st_slots - 1);
+            }
+            sc.jmin = p.st_j0 + st_t * p.bx;
+            sc.cnt = min(p.bx, p.st_nin - st_t * p.bx);
+            if (!(p.dbg_mode & 4096))   // (debug: keep the first slab's table)
+              stream_table(sc, tmem_base, p.nt, blk_inc, slice_inc, id1, id2, id3, stab);
+          }
         }
       };
       using I1 = std::integral_constant<int, 1>;
@@ -900,7 +1102,10 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       using K0 = std::integral_constant<int, 0>;
       using K1 = std::integral_constant<int, 1>;
       using K2 = std::integral_constant<int, 2>;
-      if (p.fold) {
+      using K3 = std::integral_constant<int, 3>;
+      if constexpr (STREAM) {
+        tiles(I1{}, K3{});
+      } else if (p.fold) {
         auto folded = [&](auto kind_c) {
           switch (p.bx) {
             case 1: tiles(I1{}, kind_c); break;
@@ -1031,7 +1236,17 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
           const int j = i / cpad, c = i - j * cpad;
           s_head[i] = (j < p.head_cout && c < p.cout) ? p.head_w[j * p.cout + c] : 0.f;
         }
+      if constexpr (STREAM) {
+        // streamed fold: every MMA accumulates, so the ring starts zeroed
+        // (and the epilogue zeroes each slot again after reading it)
+        const uint32_t tq = tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+        for (int u = (warp - 3) >> 2; u < (p.st_slots * p.nt) >> 4; u += EPI_WARPS / 4)
+          tmem_st16_zero(tq + u * 16);
+        tmem_wait_st();
+        tc_fence_before();
+      }
       named_bar_sync(2, 32 * EPI_WARPS);
+      if (STREAM && warp == 3 && lane == 0) mbar_arrive(&t_full[MAX_ACC - 1]);
     }
     const int q = warp & 3;                   // TMEM lane quarter this warp may access
     const int sub = (warp - 3) >> 2;          // which share of the work items
@@ -1058,9 +1273,20 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
     const long long ra_bo = LEAN && BASE ? ra * bvw.s[ra_dim] + zz * bvw.s[4] : 0;
     // lean + fused pool: lanes with (y, z) both even store the 2x2 max
     const long long ra_po = LEAN ? (ra >> 1) * p.pool_out.s[3] + (zz >> 1) * p.pool_out.s[4] : 0;
-    for (int tile = first_tile; tile < p.total_tiles; tile += tile_step, ++it) {
+    // (streamed fold: the CTA's columns x slabs, in the producer's order)
+    const int n_items =
+        STREAM ? (static_cast<int>(blockIdx.x) < p.st_ncols
+                      ? (p.st_ncols - static_cast<int>(blockIdx.x) + tile_step - 1) / tile_step *
+                            p.st_nslab
+                      : 0)
+               : (first_tile < p.total_tiles
+                      ? (p.total_tiles - first_tile + tile_step - 1) / tile_step
+                      : 0);
+    for (; it < n_items; ++it) {
+      const int tile = first_tile + it * tile_step;
       TileCoord tc;
       int rc, z, sc0;
+      int st_ns = 0, st_slot0 = 0;
       bool yz_ok;
       long long lo_off = 0, lb_off = 0, lp_off = 0;
       int nt0;
@@ -1077,6 +1303,8 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
         lo_off = ti.o_off + ra_oo;
         lb_off = ti.b_off + ra_bo;
         lp_off = ti.p_off + ra_po;
+        st_ns = ti.ns;
+        st_slot0 = ti.slot0;
         tc.rep = 0;
         tc.nt = 0;
         tc.b = 0;
@@ -1095,7 +1323,7 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       const int slim = p.slice_y ? p.oy : p.ox;
       // only the tile's slices inside the output are finished (a last tile
       // along the slice axis may hold fewer than bx; 18 = 8 + 8 + 2)
-      const int nsv = tc.dummy ? 0 : min(p.bx, slim - sc0);
+      const int nsv = STREAM ? st_ns : (tc.dummy ? 0 : min(p.bx, slim - sc0));
       const int items = nsv * col_items;
       // (replica offsets are added per item: with taps in N (rep_n) every
       // 16-column item belongs to one tap)
@@ -1131,6 +1359,8 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       auto taddr_of = [&](int item) {
         int s, cc;
         split_item(item, s, cc);
+        if constexpr (STREAM)   // slice s of this slab: slot (slot0 + s) of the TMEM ring
+          return tbase + ((st_slot0 + s) & (p.st_slots - 1)) * p.nt + cc;
         return tbase + s * p.nt + cc;
       };
       // residual operand: bf16 blocked bases are prefetched raw two items
@@ -1543,6 +1773,7 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       while (item < items) {
         const int nxt = item + NSUB;
         tmem_wait_ld16(ra);
+        if constexpr (STREAM) tmem_st16_zero(taddr_of(item));
         if (warp == 3 && lane == 0 && item == sub) dbg_mark(p, it, 7);
         if (nxt < items) tmem_ld16_issue(taddr_of(nxt), rb);
         if (BASE) base_get(item, qa, bv);
@@ -1551,12 +1782,14 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
         if (nxt >= items) break;
         const int nn = nxt + NSUB;
         tmem_wait_ld16(rb);
+        if constexpr (STREAM) tmem_st16_zero(taddr_of(nxt));
         if (nn < items) tmem_ld16_issue(taddr_of(nn), ra);
         if (BASE) base_get(nxt, qb, bv);
         if (!(p.dbg_mode & 256)) finish(nxt, rb, bv);
         if (braw && nxt + 2 * NSUB < items) base_issue(nxt + 2 * NSUB, qb);
         item = nn;
       }
+      if constexpr (STREAM) tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -1591,10 +1824,10 @@ size_t tc_smem_bytes(const TcParams &p) {
 }
 
 template <int ACT, bool FASTOUT, bool BASE, bool PAIR, bool F32IN = false, bool POOL = false,
-          bool HEAD = false, bool LEAN = false>
+          bool HEAD = false, bool LEAN = false, bool STREAM = false>
 static int launch_variant(const TcParams &p, const TcMaps &maps, int grid, cudaStream_t stream,
                           size_t smem) {
-  auto kern = conv3d_tc_kernel<ACT, FASTOUT, BASE, PAIR, F32IN, POOL, HEAD, LEAN>;
+  auto kern = conv3d_tc_kernel<ACT, FASTOUT, BASE, PAIR, F32IN, POOL, HEAD, LEAN, STREAM>;
   if (int rc = ensure_smem_attr(kern, 232448, "cudaFuncSetAttribute(conv3d_tc)")) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1665,6 +1898,20 @@ static int launch_act(const TcParams &p, const TcMaps &maps, int grid, cudaStrea
   if (!fast) {
     if (PAIR) return set_error(VXB_EUNSUPPORTED, "pair mode needs a blocked bf16 output");
     return launch_variant<-1, false, BASE, false>(p, maps, grid, s, smem);
+  }
+  if (p.lean && p.stream) {
+    if (PAIR) return set_error(VXB_EUNSUPPORTED, "streamed fold: single-CTA tiles");
+    switch (p.act) {
+      case VXB_ACT_RELU:
+        return launch_variant<VXB_ACT_RELU, true, BASE, false, false, false, false, true, true>(
+            p, maps, grid, s, smem);
+      case VXB_ACT_ELU:
+        return launch_variant<VXB_ACT_ELU, true, BASE, false, false, false, false, true, true>(
+            p, maps, grid, s, smem);
+      default:
+        return launch_variant<VXB_ACT_NONE, true, BASE, false, false, false, false, true, true>(
+            p, maps, grid, s, smem);
+    }
   }
   if (p.lean) {
     // bf16 blocked output (and residual): the lean epilogue (tc_lean_ok)

@@ -298,7 +298,8 @@ static int tc_tmem_cols(int bx, int nt, int acc, bool fold_pair) {
 // streamed weights); fold_pair: it is a folded conv that pairs (TMEM layout)
 static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, long long other_tiles,
                         int sms, int reps, int reserved, bool f32in, bool can_pair,
-                        int pair_mode, bool fold_pair, TcConfig &c, int reserved_per_slice = 0) {
+                        int pair_mode, bool fold_pair, TcConfig &c, int reserved_per_slice = 0,
+                        int stream_bx = 0) {
   // room for bias/scale/barriers, plus the fp32-input staging ring if any
   // (and per-slice epilogue scratch: the fused head's partials)
   const int budget0 = 227 * 1024 - 6144 - reserved;
@@ -329,7 +330,11 @@ static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, lon
       c.bx = cand;
     }
   }
-  if (tc_tmem_cols(c.bx, L.nt, c.acc, fold_pair) > 512)
+  // streamed fold (run_tc): the slab width is given, the accumulators are a
+  // TMEM ring, the A box has no halo along the slice axis and the weights
+  // must stay resident
+  if (stream_bx) c.bx = stream_bx;
+  if (!stream_bx && tc_tmem_cols(c.bx, L.nt, c.acc, fold_pair) > 512)
     return set_error(VXB_EUNSUPPORTED, "TMEM overflow");
   bool any_pair = false;
   int max_steps = 1;
@@ -344,7 +349,7 @@ static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, lon
   for (;;) {
     const int budget = budget0 - c.bx * reserved_per_slice;
     const int sx = L.fold == 2 ? TILE_Y : c.bx, sy = L.fold == 2 ? c.bx : TILE_Y;
-    const int hx = sx + k[0] - 1, hy = sy + k[1] - 1, hz = TILE_Z + k[2] - 1;
+    const int hx = sx + (stream_bx ? 0 : k[0] - 1), hy = sy + k[1] - 1, hz = TILE_Z + k[2] - 1;
     c.chunk_bytes = hx * hy * hz * 16;
     c.chunk_stride = round_up(c.chunk_bytes + 128, 128);
     c.chunk_slots = any_pair ? 2 : 1;
@@ -393,7 +398,9 @@ static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, lon
         c.nb = std::min(c.pair ? 6 : 4, avail / c.b_stage);
       }
     }
-    if (c.nb >= 1 && (c.resident || c.nb >= 2)) break;
+    if (stream_bx && c.resident) break;
+    if (stream_bx && na_cap <= 2) return VXB_EUNSUPPORTED;   // caller falls back (no error text)
+    if (!stream_bx && c.nb >= 1 && (c.resident || c.nb >= 2)) break;
     if (na_cap > 2) {
       --na_cap;
       continue;
@@ -407,7 +414,8 @@ static int tc_configure(const TcLayout &L, const int k[3], int slice_extent, lon
   // of max(MMA, epilogue) (C28 1x3x3 on 18x768x768: MMAs alone 249 us,
   // epilogue alone 226 us, together 338 us).  Small tiles leave TMEM columns
   // free: use them for more stages (VXB_TC_ACC_MAX, default 4).
-  if (c.acc == 2) {
+  if (stream_bx) c.acc = 2;
+  if (c.acc == 2 && !stream_bx) {
     const int acc_max = std::min(MAX_ACC, env_int("VXB_TC_ACC_MAX", 4));
     while (c.acc < acc_max && tc_tmem_cols(c.bx, L.nt, c.acc + 1, fold_pair) <= 512) ++c.acc;
   }
@@ -584,9 +592,58 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
   // one float4 partial per row and column item of a tile (<= 8 slices)
   const int head_smem = a.head_cout ? 4 * L.n_tiles * L.nt * 4 + 16 : 0;
   const int head_slice = a.head_cout ? (L.nt / 16) * 128 * 16 : 0;
-  int rc = tc_configure(L, a.k, slice_y ? a.oy : a.ox, other_tiles, sms, a.reps,
-                        stg_bytes + head_smem, f32in, can_pair && !(fold_pair && a.head_cout), pair_env,
-                        fold_pair && !a.head_cout, c, head_slice);
+  // Streamed fold (TcParams::stream), experimental and off by default:
+  // x-folded convs with a lean epilogue whose columns fill the SMs (one batch
+  // entry's columns decide, so batched launches stay bit-identical to single
+  // ones).  VXB_TC_STREAM: 0 off (default), 1 = nt == 32 convs, 2 = every
+  // eligible conv.  Measured (C28 3x3x3, 16 patches of 18x192x192): a slab's
+  // MMA phase is 15 % shorter than a tile's (no fold edges) but the per-slab
+  // operand table costs ~0.7 us of uniform-datapath work and the total N
+  // work is the same: 538 us vs 510 us tiled at x = 18, 403 vs 438 at x = 14.
+  const bool lean_ok = env_int("VXB_TC_LEAN", 1) && !f32in && !a.head_cout &&
+                       (!a.pool || (a.pool_out.dtype == VXB_BF16 && a.pool_out.blocked)) &&
+                       a.out.dtype == VXB_BF16 && a.out.blocked &&
+                       (!a.has_base || (a.base.dtype == VXB_BF16 && a.base.blocked)) &&
+                       (a.act == VXB_ACT_NONE || a.act == VXB_ACT_RELU || a.act == VXB_ACT_ELU);
+  const int st_env = env_int("VXB_TC_STREAM", 0);
+  int st_bx = 0, st_j0 = 0, st_nin = 0, st_nslab = 0, st_slots = 0;
+  if (st_env && L.fold == 1 && lean_ok && a.reps == 1 && !a.rep_n && L.n_tiles == 1 && a.k[0] == 3) {
+    st_slots = 1;
+    while (st_slots * 2 * L.nt <= 512) st_slots *= 2;
+    // input slices (halo coordinates j: x_in = j - pad + off) that can be non-zero
+    int j0 = 0, j1 = a.ox + 1;
+    bool same = true;
+    for (int sg = 0; sg < 2; ++sg) {
+      if (!a.in[sg]) continue;
+      const int lo = std::max(0, a.pad[0] - a.off[sg][0]);
+      const int hi = std::min(a.ox + 1, a.in[sg]->x - 1 + a.pad[0] - a.off[sg][0]);
+      if (sg == 0) {
+        j0 = lo;
+        j1 = hi;
+      } else if (lo != j0 || hi != j1) {
+        same = false;
+      }
+    }
+    const int bx_max = std::min(8, (st_slots - 2) / 2);
+    const long long cols_one = static_cast<long long>(ceil_div(a.oy, TILE_Y)) * ceil_div(a.oz, TILE_Z);
+    if (same && j0 <= 2 && j1 >= a.ox - 1 && j1 >= j0 && bx_max >= 1 &&
+        (st_env == 2 || (L.nt == 32 && cols_one >= sms))) {
+      st_j0 = j0;
+      st_nin = j1 - j0 + 1;
+      st_nslab = ceil_div(st_nin, bx_max);
+      st_bx = ceil_div(st_nin, st_nslab);
+    }
+  }
+  int rc = VXB_EUNSUPPORTED;
+  if (st_bx) {
+    rc = tc_configure(L, a.k, a.ox, other_tiles, sms, a.reps, stg_bytes + head_smem, f32in, false,
+                      pair_env, false, c, head_slice, st_bx);
+    if (rc) st_bx = 0;   // weights do not stay resident beside the A ring: tiled walk
+  }
+  if (!st_bx)
+    rc = tc_configure(L, a.k, slice_y ? a.oy : a.ox, other_tiles, sms, a.reps,
+                      stg_bytes + head_smem, f32in, can_pair && !(fold_pair && a.head_cout),
+                      pair_env, fold_pair && !a.head_cout, c, head_slice);
   if (rc) return rc;
   TcParams p;
   memset(&p, 0, sizeof(p));
@@ -628,7 +685,7 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
   p.kx = a.k[0];
   p.ky = a.k[1];
   p.kz = a.k[2];
-  p.hx = p.ex + a.k[0] - 1;
+  p.hx = p.ex + (st_bx ? 0 : a.k[0] - 1);
   p.hy = p.ey + a.k[1] - 1;
   p.hz = TILE_Z + a.k[2] - 1;
   p.a_slice_inc = (slice_y ? p.hz : p.hy * p.hz) * 16;
@@ -777,7 +834,19 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
   const bool fp = p.pair && p.fold;
   p.acc_stride = (fp ? p.bx + 2 : p.bx) * p.nt;
   p.slice0_col = fp ? 2 * p.nt : 0;
-  const int cols = tc_tmem_cols(p.bx, p.nt, p.acc_stages, fp);
+  int cols = tc_tmem_cols(p.bx, p.nt, p.acc_stages, fp);
+  if (st_bx) {
+    p.stream = 1;
+    p.st_j0 = st_j0;
+    p.st_nin = st_nin;
+    p.st_nslab = st_nslab;
+    p.st_slots = st_slots;
+    p.st_ncols = p.tiles_y * p.tiles_z * p.nb;
+    p.acc_stride = 0;
+    cols = st_slots * p.nt;
+    total = static_cast<long long>(p.st_ncols) * st_nslab;
+    p.total_tiles = static_cast<int>(total);
+  }
   p.tmem_cols = 32;
   while (p.tmem_cols < cols) p.tmem_cols <<= 1;
   if (p.tmem_cols > 512) return set_error(VXB_EUNSUPPORTED, "TMEM overflow (%d columns)", cols);
@@ -785,15 +854,18 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
   if (c.smem > 227 * 1024) return set_error(VXB_EUNSUPPORTED, "conv needs %zu B smem", c.smem);
   // persistent: one CTA per SM (480 threads x ~100 registers leaves no room
   // for a second one, and the smem ring is sized for the whole SM)
-  int grid = static_cast<int>(std::min<long long>(total, static_cast<long long>(sms)));
+  int grid = static_cast<int>(std::min<long long>(p.stream ? p.st_ncols : total,
+                                                 static_cast<long long>(sms)));
   grid = std::max(p.cluster, grid / p.cluster * p.cluster);
   if (env_int("VXB_PRINT", 0))
     fprintf(stderr,
             "conv3d_tc cin %d+%d cout %d k %d%d%d out %dx%dx%d: nt %d ntiles %d fold %d pair %d "
-            "bx %d acc %d na %d nb %d bsteps %d resident %d tiles %d grid %d smem %zu tmem %d\n",
+            "bx %d acc %d na %d nb %d bsteps %d resident %d tiles %d grid %d smem %zu tmem %d "
+            "stream %d (j0 %d nin %d slabs %d slots %d)\n",
             a.cin0, a.cin1, a.cout, a.k[0], a.k[1], a.k[2], a.ox, a.oy, a.oz, p.nt, p.n_tiles,
             L.fold, p.pair, p.bx, p.acc_stages, p.na, p.nb_stages, p.bsteps, p.resident,
-            p.total_tiles, grid, c.smem, p.tmem_cols);
+            p.total_tiles, grid, c.smem, p.tmem_cols, p.stream, p.st_j0, p.st_nin, p.st_nslab,
+            p.st_slots);
   return launch_conv3d_tc(p, maps, grid, stream);
 }
 

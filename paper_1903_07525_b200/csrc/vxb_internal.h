@@ -61,6 +61,14 @@ struct TcParams {
   // tile: stage s spans slices -2..bx+1 and neighbouring stages share their
   // 2nt-column scratch band (stride (bx+2)nt, slice 0 at +2nt).
   int acc_stride, slice0_col, tmem_cols;
+  // Streamed fold (folded x taps, single CTA, resident weights, lean
+  // epilogue): a CTA walks whole columns (all x of one 16 y x 8 z block) slab
+  // by slab; the accumulators of the column's output slices live in a ring
+  // of st_slots TMEM slices, input slice j writes output slices j-2..j
+  // wherever they fall in the ring, so there are no per-tile fold edges and
+  // no x halo re-reads.  Input slices st_j0 .. st_j0 + st_nin - 1 (halo
+  // coordinates) can be non-zero; slab t holds bx of them.
+  int stream, st_j0, st_nin, st_nslab, st_slots, st_ncols;
   int kx, ky, kz;
   int hx, hy, hz;              // halo tile extents
   int pad[3];

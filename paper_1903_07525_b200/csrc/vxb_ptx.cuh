@@ -302,6 +302,19 @@ __device__ __forceinline__ void tmem_wait_ld16(uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]) : : "memory");
 }
 
+// zero 16 consecutive accumulator columns of this warp's 32 TMEM lanes
+__device__ __forceinline__ void tmem_st16_zero(uint32_t taddr) {
+  const uint32_t z = 0u;
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(z)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 // descriptor split into a low word (start address | LBO) and a high word
 // (SBO | version | layout) so loops only add to the low word
 __device__ __forceinline__ uint32_t desc_lo(uint32_t saddr, uint32_t lbo) {
@@ -451,6 +464,149 @@ __device__ __forceinline__ void umma_fold_first(uint32_t d, uint32_t a_lo, uint3
 #undef VXB_FM
 #undef VXB_FOLD_ASM
 #undef VXB_FOLD_OPS
+
+// One K step of a streamed-fold slab (conv3d_tc.cu mma_group_stream) as ONE
+// asm block: CNT MMAs, every one with its own accumulator column (%5+3k), B
+// block offset (%6+3k) and instruction descriptor (%7+3k), handed over in
+// issue order; the A start of input slice I is a_lo + I * slice_inc.  The
+// issue orders keep neighbours >= 3 input slices apart where the count
+// allows (slices i, i' share accumulator slots when |i - i'| <= 2).
+// (generated: tools/gen_stream_asm.py)
+template <int CNT>
+__device__ __forceinline__ void umma_stream_step(uint32_t a_lo, uint32_t a_hi, uint32_t b_lo,
+                                                 uint32_t b_hi, uint32_t slice_inc,
+                                                 const uint32_t (&d)[8], const uint32_t (&b)[8],
+                                                 const uint32_t (&id)[8]) {
+  static_assert(CNT >= 1 && CNT <= 8, "slab width");
+  if (CNT == 1)
+    asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b64 ad, bd;\n\t.reg .b32 al, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.eq.u32 p, %0, %0;\n\t"
+      "mad.lo.u32 al, %4, 0, %0;\n\tadd.u32 bl, %2, %6;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%5], ad, bd, %7, p;\n\t"
+      "}"
+      ::"r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(slice_inc), "r"(d[0]), "r"(b[0]), "r"(id[0])
+      : "memory");
+  if (CNT == 2)
+    asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b64 ad, bd;\n\t.reg .b32 al, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.eq.u32 p, %0, %0;\n\t"
+      "mad.lo.u32 al, %4, 0, %0;\n\tadd.u32 bl, %2, %6;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%5], ad, bd, %7, p;\n\t"
+      "mad.lo.u32 al, %4, 1, %0;\n\tadd.u32 bl, %2, %9;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%8], ad, bd, %10, p;\n\t"
+      "}"
+      ::"r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(slice_inc), "r"(d[0]), "r"(b[0]), "r"(id[0]), "r"(d[1]), "r"(b[1]), "r"(id[1])
+      : "memory");
+  if (CNT == 3)
+    asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b64 ad, bd;\n\t.reg .b32 al, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.eq.u32 p, %0, %0;\n\t"
+      "mad.lo.u32 al, %4, 0, %0;\n\tadd.u32 bl, %2, %6;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%5], ad, bd, %7, p;\n\t"
+      "mad.lo.u32 al, %4, 1, %0;\n\tadd.u32 bl, %2, %9;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%8], ad, bd, %10, p;\n\t"
+      "mad.lo.u32 al, %4, 2, %0;\n\tadd.u32 bl, %2, %12;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%11], ad, bd, %13, p;\n\t"
+      "}"
+      ::"r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(slice_inc), "r"(d[0]), "r"(b[0]), "r"(id[0]), "r"(d[1]), "r"(b[1]), "r"(id[1]), "r"(d[2]), "r"(b[2]), "r"(id[2])
+      : "memory");
+  if (CNT == 4)
+    asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b64 ad, bd;\n\t.reg .b32 al, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.eq.u32 p, %0, %0;\n\t"
+      "mad.lo.u32 al, %4, 0, %0;\n\tadd.u32 bl, %2, %6;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%5], ad, bd, %7, p;\n\t"
+      "mad.lo.u32 al, %4, 3, %0;\n\tadd.u32 bl, %2, %9;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%8], ad, bd, %10, p;\n\t"
+      "mad.lo.u32 al, %4, 1, %0;\n\tadd.u32 bl, %2, %12;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%11], ad, bd, %13, p;\n\t"
+      "mad.lo.u32 al, %4, 2, %0;\n\tadd.u32 bl, %2, %15;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%14], ad, bd, %16, p;\n\t"
+      "}"
+      ::"r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(slice_inc), "r"(d[0]), "r"(b[0]), "r"(id[0]), "r"(d[3]), "r"(b[3]), "r"(id[3]), "r"(d[1]), "r"(b[1]), "r"(id[1]), "r"(d[2]), "r"(b[2]), "r"(id[2])
+      : "memory");
+  if (CNT == 5)
+    asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b64 ad, bd;\n\t.reg .b32 al, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.eq.u32 p, %0, %0;\n\t"
+      "mad.lo.u32 al, %4, 1, %0;\n\tadd.u32 bl, %2, %6;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%5], ad, bd, %7, p;\n\t"
+      "mad.lo.u32 al, %4, 4, %0;\n\tadd.u32 bl, %2, %9;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%8], ad, bd, %10, p;\n\t"
+      "mad.lo.u32 al, %4, 0, %0;\n\tadd.u32 bl, %2, %12;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%11], ad, bd, %13, p;\n\t"
+      "mad.lo.u32 al, %4, 3, %0;\n\tadd.u32 bl, %2, %15;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%14], ad, bd, %16, p;\n\t"
+      "mad.lo.u32 al, %4, 2, %0;\n\tadd.u32 bl, %2, %18;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%17], ad, bd, %19, p;\n\t"
+      "}"
+      ::"r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(slice_inc), "r"(d[1]), "r"(b[1]), "r"(id[1]), "r"(d[4]), "r"(b[4]), "r"(id[4]), "r"(d[0]), "r"(b[0]), "r"(id[0]), "r"(d[3]), "r"(b[3]), "r"(id[3]), "r"(d[2]), "r"(b[2]), "r"(id[2])
+      : "memory");
+  if (CNT == 6)
+    asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b64 ad, bd;\n\t.reg .b32 al, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.eq.u32 p, %0, %0;\n\t"
+      "mad.lo.u32 al, %4, 2, %0;\n\tadd.u32 bl, %2, %6;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%5], ad, bd, %7, p;\n\t"
+      "mad.lo.u32 al, %4, 5, %0;\n\tadd.u32 bl, %2, %9;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%8], ad, bd, %10, p;\n\t"
+      "mad.lo.u32 al, %4, 1, %0;\n\tadd.u32 bl, %2, %12;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%11], ad, bd, %13, p;\n\t"
+      "mad.lo.u32 al, %4, 4, %0;\n\tadd.u32 bl, %2, %15;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%14], ad, bd, %16, p;\n\t"
+      "mad.lo.u32 al, %4, 0, %0;\n\tadd.u32 bl, %2, %18;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%17], ad, bd, %19, p;\n\t"
+      "mad.lo.u32 al, %4, 3, %0;\n\tadd.u32 bl, %2, %21;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%20], ad, bd, %22, p;\n\t"
+      "}"
+      ::"r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(slice_inc), "r"(d[2]), "r"(b[2]), "r"(id[2]), "r"(d[5]), "r"(b[5]), "r"(id[5]), "r"(d[1]), "r"(b[1]), "r"(id[1]), "r"(d[4]), "r"(b[4]), "r"(id[4]), "r"(d[0]), "r"(b[0]), "r"(id[0]), "r"(d[3]), "r"(b[3]), "r"(id[3])
+      : "memory");
+  if (CNT == 7)
+    asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b64 ad, bd;\n\t.reg .b32 al, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.eq.u32 p, %0, %0;\n\t"
+      "mad.lo.u32 al, %4, 3, %0;\n\tadd.u32 bl, %2, %6;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%5], ad, bd, %7, p;\n\t"
+      "mad.lo.u32 al, %4, 6, %0;\n\tadd.u32 bl, %2, %9;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%8], ad, bd, %10, p;\n\t"
+      "mad.lo.u32 al, %4, 2, %0;\n\tadd.u32 bl, %2, %12;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%11], ad, bd, %13, p;\n\t"
+      "mad.lo.u32 al, %4, 5, %0;\n\tadd.u32 bl, %2, %15;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%14], ad, bd, %16, p;\n\t"
+      "mad.lo.u32 al, %4, 1, %0;\n\tadd.u32 bl, %2, %18;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%17], ad, bd, %19, p;\n\t"
+      "mad.lo.u32 al, %4, 4, %0;\n\tadd.u32 bl, %2, %21;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%20], ad, bd, %22, p;\n\t"
+      "mad.lo.u32 al, %4, 0, %0;\n\tadd.u32 bl, %2, %24;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%23], ad, bd, %25, p;\n\t"
+      "}"
+      ::"r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(slice_inc), "r"(d[3]), "r"(b[3]), "r"(id[3]), "r"(d[6]), "r"(b[6]), "r"(id[6]), "r"(d[2]), "r"(b[2]), "r"(id[2]), "r"(d[5]), "r"(b[5]), "r"(id[5]), "r"(d[1]), "r"(b[1]), "r"(id[1]), "r"(d[4]), "r"(b[4]), "r"(id[4]), "r"(d[0]), "r"(b[0]), "r"(id[0])
+      : "memory");
+  if (CNT == 8)
+    asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b64 ad, bd;\n\t.reg .b32 al, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.eq.u32 p, %0, %0;\n\t"
+      "mad.lo.u32 al, %4, 3, %0;\n\tadd.u32 bl, %2, %6;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%5], ad, bd, %7, p;\n\t"
+      "mad.lo.u32 al, %4, 6, %0;\n\tadd.u32 bl, %2, %9;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%8], ad, bd, %10, p;\n\t"
+      "mad.lo.u32 al, %4, 2, %0;\n\tadd.u32 bl, %2, %12;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%11], ad, bd, %13, p;\n\t"
+      "mad.lo.u32 al, %4, 5, %0;\n\tadd.u32 bl, %2, %15;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%14], ad, bd, %16, p;\n\t"
+      "mad.lo.u32 al, %4, 1, %0;\n\tadd.u32 bl, %2, %18;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%17], ad, bd, %19, p;\n\t"
+      "mad.lo.u32 al, %4, 4, %0;\n\tadd.u32 bl, %2, %21;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%20], ad, bd, %22, p;\n\t"
+      "mad.lo.u32 al, %4, 0, %0;\n\tadd.u32 bl, %2, %24;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%23], ad, bd, %25, p;\n\t"
+      "mad.lo.u32 al, %4, 7, %0;\n\tadd.u32 bl, %2, %27;\n\tmov.b64 ad, {al, %1};\n\t"
+      "mov.b64 bd, {bl, %3};\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%26], ad, bd, %28, p;\n\t"
+      "}"
+      ::"r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(slice_inc), "r"(d[3]), "r"(b[3]), "r"(id[3]), "r"(d[6]), "r"(b[6]), "r"(id[6]), "r"(d[2]), "r"(b[2]), "r"(id[2]), "r"(d[5]), "r"(b[5]), "r"(id[5]), "r"(d[1]), "r"(b[1]), "r"(id[1]), "r"(d[4]), "r"(b[4]), "r"(id[4]), "r"(d[0]), "r"(b[0]), "r"(id[0]), "r"(d[7]), "r"(b[7]), "r"(id[7])
+      : "memory");
+}
 
 // CNT cta_group::2 MMAs in one asm block: D and the A lo word advance by
 // d_inc / a_inc, B and the instruction descriptor are shared (the folded

@@ -182,6 +182,39 @@ def test_unfolded_tile_widths_bit_identical(bx, c, k, pad, sp, monkeypatch):
     assert mx < BF16_TOL and l2 < 3e-3, (mx, l2)
 
 
+@pytest.mark.parametrize("n,c,sp,pad", [(1, 28, (18, 32, 16), (1, 1, 1)),
+                                         (2, 28, (18, 20, 12), (1, 1, 1)),
+                                         (1, 32, (32, 16, 16), (1, 1, 1)),
+                                         (1, 16, (7, 16, 8), (1, 1, 1)),
+                                         (1, 28, (20, 18, 10), (0, 0, 0)),
+                                         (3, 8, (5, 33, 9), (1, 1, 1)),
+                                         (1, 48, (18, 16, 16), (1, 1, 1))])
+@pytest.mark.parametrize("use_base", [False, True])
+def test_streamed_fold_matches_oracle(n, c, sp, pad, use_base, monkeypatch):
+    """Streamed fold (VXB_TC_STREAM=2, experimental): a CTA walks whole x
+    columns slab by slab, the output slices' accumulators live in a TMEM ring
+    that the epilogue zeroes after reading.  Same sums as the tiled fold walk
+    in another fp32 order: equal to it within fp32 reordering (one bf16 ulp of
+    the stored values at most) and within the bf16 bound of the oracle.
+    Covers ring wrap-around (18 and 32 slices over 16 / 8 slots), 'valid'
+    convolutions (both halo slices real), batches, and residual operands."""
+    rng = np.random.default_rng(c + sp[0])
+    x = rng.uniform(-1, 1, (n, c) + sp).astype(np.float32)
+    w = (rng.standard_normal((c, c, 3, 3, 3)) * 0.1).astype(np.float32)
+    b = rng.standard_normal(c).astype(np.float32)
+    osp = tuple(s + 2 * p - 2 for s, p in zip(sp, pad))
+    base = rng.uniform(-1, 1, (n, c) + osp).astype(np.float32) if use_base else None
+    scale = rng.uniform(0.5, 1.5, c).astype(np.float32) if use_base else None
+    monkeypatch.setenv("VXB_TC_STREAM", "0")
+    tiled, _ = _conv_bf16(x, w, b, pad, "elu", base, scale)
+    monkeypatch.setenv("VXB_TC_STREAM", "2")
+    got, _ = _conv_bf16(x, w, b, pad, "elu", base, scale)
+    assert np.abs(got - tiled).max() <= np.abs(tiled).max() * 2.0 ** -7
+    want = _ref_bf16(x, w, b, pad, "elu", base, scale)
+    mx, l2 = R.normalized_error(got, want)
+    assert mx < BF16_TOL and l2 < 3e-3, (mx, l2)
+
+
 def test_unfolded_path_for_badly_padded_rows():
     """x = 18 makes y-sliced folding pad 14 of 32 rows: select_shape picks the
     unfolded layout, which must match the oracle (and the folded result)."""
