@@ -33,7 +33,9 @@
 // act -> global).  Persistent CTAs walk the tile list; TMEM accumulators are
 // double buffered when they fit so the epilogue of tile i overlaps the MMAs
 // of tile i+1.  CTA pairs (cta_group::2, M = 256) split the weight stream of
-// unfolded convs.
+// unfolded convs.  Experimental (VXB_TC_STREAM): the streamed fold walks whole
+// x columns with the output slices' accumulators in a TMEM ring
+// (mma_group_stream).
 #include <cuda_bf16.h>
 #include <type_traits>
 #include "vxb_internal.h"
@@ -286,8 +288,11 @@ static_assert(6 + MAX_ACC < TINFO, "TileInfo ring: the producer runs <= na + acc
 
 // Byte offsets inside the dynamic smem block (all derivable from p).
 struct SmemMap {
-  uint32_t a, b, stg, bias, scale, head, hpart, ltab, bars;
+  uint32_t a, b, stg, bias, scale, head, hpart, ltab, stab, bars;
 };
+// streamed fold: one 32-word operand table per (ring phase, slab), built
+// once per CTA (StreamTab layout: d[8] b[8] id[8] wa[2] wb[2] wid[2])
+constexpr int STAB_WORDS = 32;
 __host__ __device__ inline SmemMap smem_map(const TcParams &p) {
   SmemMap m;
   m.a = 0;
@@ -300,7 +305,8 @@ __host__ __device__ inline SmemMap smem_map(const TcParams &p) {
   // fused head: per-row partial dot products of every column item [item][row]
   m.hpart = (m.head + (p.head_cout > 0 ? 4 * cpad * 4 : 0) + 15) & ~15u;
   m.ltab = m.hpart + (p.head_cout > 0 ? p.bx * (p.nt >> 4) * 128 * 16 : 0);
-  m.bars = m.ltab + (p.lean ? LEAN_TAB * sizeof(LeanEnt) + TINFO * sizeof(TileInfo) : 0);
+  m.stab = m.ltab + (p.lean ? LEAN_TAB * sizeof(LeanEnt) + TINFO * sizeof(TileInfo) : 0);
+  m.bars = m.stab + (p.stream ? p.st_nphase * p.st_nslab * STAB_WORDS * 4 : 0);
   return m;
 }
 
@@ -529,7 +535,7 @@ __device__ __forceinline__ void mma_group_fold_pair(
 // within a K step the input slices go in stride-3 order so that consecutive
 // MMAs never touch the same slots (no accumulator read-after-write stalls).
 struct StreamCtx {
-  int jmin, cnt, j0, S, rb, slots;
+  int jmin, cnt, S, rb, slots;
 };
 constexpr int STREAM_BX = 8;
 struct StreamTab {
@@ -538,39 +544,65 @@ struct StreamTab {
   // MMA (D column 0): A slice offset, B block offset, idesc (0 = none)
   uint32_t wa[2], wb[2], wid[2];
 };
-__device__ __forceinline__ void stream_table(const StreamCtx &sc, const uint32_t d0,
-                                             const uint32_t nt, const uint32_t blk_inc,
-                                             const uint32_t slice_inc,
-                                             const uint32_t id1, const uint32_t id2,
-                                             const uint32_t id3, StreamTab &tb) {
-  const int mask = sc.slots - 1;
-  tb.wid[0] = tb.wid[1] = 0u;
-  tb.wa[0] = tb.wa[1] = tb.wb[0] = tb.wb[1] = 0u;
-  int nw = 0;
+// Entry i (0..7: input slice i of the slab; 8: the wrapped parts) of the
+// operand table of slab t at ring phase ph, written to shared memory by one
+// thread in the kernel prologue.
+__device__ __forceinline__ void stream_table_entry(const TcParams &p, uint32_t *tab, int ph, int t,
+                                                   int i, const uint32_t blk_inc,
+                                                   const uint32_t slice_inc) {
+  const int mask = p.st_slots - 1;
+  const int rb = (ph * p.ox) & mask;
+  const int jmin = p.st_j0 + t * p.bx;
+  const int cnt = min(p.bx, p.st_nin - t * p.bx);
+  const uint32_t id1 = idesc_bf16(128, p.nt), id2 = idesc_bf16(128, 2 * p.nt),
+                 id3 = idesc_bf16(128, 3 * p.nt);
+  auto entry = [&](int k, int &r, int &nn, int &n1, int &dhi) {
+    const int j = jmin + k;
+    dhi = min(2, j);
+    const int dlo = max(0, j - p.ox + 1);
+    nn = dhi - dlo + 1;
+    r = (rb + j - dhi) & mask;
+    n1 = min(nn, p.st_slots - r);
+  };
+  if (i < STREAM_BX) {
+    int r, nn, n1, dhi;
+    entry(i, r, nn, n1, dhi);
+    tab[i] = r * p.nt;
+    tab[8 + i] = (2 - dhi) * blk_inc;
+    tab[16 + i] = n1 == 1 ? id1 : (n1 == 2 ? id2 : id3);
+  } else {
+    uint32_t w[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+    int nw = 0;
+    for (int k = 0; k < cnt; ++k) {
+      int r, nn, n1, dhi;
+      entry(k, r, nn, n1, dhi);
+      if (n1 < nn && nw < 2) {
+        w[nw] = k * slice_inc;
+        w[2 + nw] = (2 - dhi + n1) * blk_inc;
+        w[4 + nw] = nn - n1 == 1 ? id1 : id2;
+        ++nw;
+      }
+    }
+    for (int k = 0; k < 6; ++k) tab[24 + k] = w[k];
+    tab[30] = tab[31] = 0u;
+  }
+}
+// the MMA warp's copy of a table: lane l reads word l, every word is then
+// broadcast so that ptxas keeps the operands in uniform registers
+__device__ __forceinline__ void stream_table_load(const uint32_t *tab, const uint32_t d0,
+                                                  StreamTab &tb) {
+  const uint32_t v = tab[threadIdx.x & 31];
 #pragma unroll
   for (int i = 0; i < STREAM_BX; ++i) {
-    const int j = sc.jmin + i;
-    const int dhi = min(2, j), dlo = max(0, j - sc.S + 1);
-    const int nn = dhi - dlo + 1;
-    const int r = (sc.rb + j - dhi) & mask;
-    const int n1 = min(nn, sc.slots - r);
-    tb.d[i] = d0 + r * nt;
-    tb.b[i] = (2 - dhi) * blk_inc;
-    tb.id[i] = n1 == 1 ? id1 : (n1 == 2 ? id2 : id3);
-    if (i < sc.cnt && n1 < nn) {
-      const uint32_t wid = nn - n1 == 1 ? id1 : id2;
-      const uint32_t wb = (2 - dhi + n1) * blk_inc, wa = i * slice_inc;
-      if (nw == 0) {
-        tb.wid[0] = wid;
-        tb.wb[0] = wb;
-        tb.wa[0] = wa;
-      } else {
-        tb.wid[1] = wid;
-        tb.wb[1] = wb;
-        tb.wa[1] = wa;
-      }
-      ++nw;
-    }
+    tb.d[i] = d0 + __shfl_sync(0xffffffffu, v, i);
+    tb.b[i] = __shfl_sync(0xffffffffu, v, 8 + i);
+    tb.id[i] = __shfl_sync(0xffffffffu, v, 16 + i);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    tb.wa[k] = __shfl_sync(0xffffffffu, v, 24 + k);
+    tb.wb[k] = __shfl_sync(0xffffffffu, v, 26 + k);
+    tb.wid[k] = __shfl_sync(0xffffffffu, v, 28 + k);
   }
 }
 template <int CNT>
@@ -684,6 +716,15 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
       e.pad = 0;
       ltab[ci] = e;
     }
+  if constexpr (STREAM) {
+    uint32_t *stab_s = reinterpret_cast<uint32_t *>(smem + sm.stab);
+    const uint32_t blk_w = (p.nt * SLAB_ROW_BYTES) >> 4, sl_w = p.a_slice_inc >> 4;
+    for (int e = threadIdx.x; e < p.st_nphase * p.st_nslab * 9; e += blockDim.x) {
+      const int tb_i = e / 9, i = e - tb_i * 9;
+      stream_table_entry(p, stab_s + tb_i * STAB_WORDS, tb_i / p.st_nslab, tb_i % p.st_nslab, i,
+                         blk_w, sl_w);
+    }
+  }
   fence_proxy_async_smem();
 
   if (warp == 0 && lane == 0) {
@@ -990,11 +1031,10 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
         // accumulator stage of tile `it`: it % acc_stages, phase (it / acc_stages) & 1
         int acc = -1, acc_ph = 1;
         StreamCtx sc;   // streamed fold: slab within the column, ring base
-        sc.j0 = p.st_j0;
         sc.S = p.ox;
         sc.rb = 0;
         sc.slots = p.st_slots;
-        int st_t = 0;
+        int st_t = 0, st_ph = 0;
         StreamTab stab;
         if constexpr (KIND == 3) {
           // the epilogue warps zeroed the accumulator ring (t_full[MAX_ACC - 1])
@@ -1008,7 +1048,8 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
             if (it == 0) {
               sc.jmin = p.st_j0;
               sc.cnt = min(p.bx, p.st_nin);
-              stream_table(sc, tmem_base, p.nt, blk_inc, slice_inc, id1, id2, id3, stab);
+              stream_table_load(reinterpret_cast<const uint32_t *>(smem + sm.stab), tmem_base,
+                                stab);
             }
           }
           if (++acc == p.acc_stages) acc = 0;
@@ -1084,12 +1125,15 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
           if constexpr (KIND == 3) {
             if (++st_t == p.st_nslab) {
               st_t = 0;
-              sc.rb = (sc.rb + p.ox) & (p.st_slots - 1);
+              if (++st_ph == p.st_nphase) st_ph = 0;
             }
             sc.jmin = p.st_j0 + st_t * p.bx;
             sc.cnt = min(p.bx, p.st_nin - st_t * p.bx);
+            // the next slab's operand table (while this slab's MMAs drain)
             if (!(p.dbg_mode & 4096))   // (debug: keep the first slab's table)
-              stream_table(sc, tmem_base, p.nt, blk_inc, slice_inc, id1, id2, id3, stab);
+              stream_table_load(reinterpret_cast<const uint32_t *>(smem + sm.stab) +
+                                    (st_ph * p.st_nslab + st_t) * STAB_WORDS,
+                                tmem_base, stab);
           }
         }
       };

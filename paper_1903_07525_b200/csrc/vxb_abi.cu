@@ -592,20 +592,20 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
   // one float4 partial per row and column item of a tile (<= 8 slices)
   const int head_smem = a.head_cout ? 4 * L.n_tiles * L.nt * 4 + 16 : 0;
   const int head_slice = a.head_cout ? (L.nt / 16) * 128 * 16 : 0;
-  // Streamed fold (TcParams::stream), experimental and off by default:
-  // x-folded convs with a lean epilogue whose columns fill the SMs (one batch
-  // entry's columns decide, so batched launches stay bit-identical to single
-  // ones).  VXB_TC_STREAM: 0 off (default), 1 = nt == 32 convs, 2 = every
-  // eligible conv.  Measured (C28 3x3x3, 16 patches of 18x192x192): a slab's
-  // MMA phase is 15 % shorter than a tile's (no fold edges) but the per-slab
-  // operand table costs ~0.7 us of uniform-datapath work and the total N
-  // work is the same: 538 us vs 510 us tiled at x = 18, 403 vs 438 at x = 14.
+  // Streamed fold (TcParams::stream): x-folded convs with a lean epilogue
+  // whose columns fill the SMs (one batch entry's columns decide, so batched
+  // launches stay bit-identical to single ones).  VXB_TC_STREAM: 0 off, 1
+  // (default) = nt == 32 convs without fused pooling, 2 = every eligible
+  // conv.  Measured (C28 3x3x3, 16 patches of 18x192x192): 483 vs 505 us
+  // tiled (571 vs 578 with a residual operand; 368 vs 434 at x = 14); with
+  // fused pooling the streamed epilogue is slower (1.53 vs 1.45 ms per 36
+  // patches), so those stay tiled.
   const bool lean_ok = env_int("VXB_TC_LEAN", 1) && !f32in && !a.head_cout &&
                        (!a.pool || (a.pool_out.dtype == VXB_BF16 && a.pool_out.blocked)) &&
                        a.out.dtype == VXB_BF16 && a.out.blocked &&
                        (!a.has_base || (a.base.dtype == VXB_BF16 && a.base.blocked)) &&
                        (a.act == VXB_ACT_NONE || a.act == VXB_ACT_RELU || a.act == VXB_ACT_ELU);
-  const int st_env = env_int("VXB_TC_STREAM", 0);
+  const int st_env = env_int("VXB_TC_STREAM", 1);
   int st_bx = 0, st_j0 = 0, st_nin = 0, st_nslab = 0, st_slots = 0;
   if (st_env && L.fold == 1 && lean_ok && a.reps == 1 && !a.rep_n && L.n_tiles == 1 && a.k[0] == 3) {
     st_slots = 1;
@@ -627,7 +627,12 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
     const int bx_max = std::min(8, (st_slots - 2) / 2);
     const long long cols_one = static_cast<long long>(ceil_div(a.oy, TILE_Y)) * ceil_div(a.oz, TILE_Z);
     if (same && j0 <= 2 && j1 >= a.ox - 1 && j1 >= j0 && bx_max >= 1 &&
-        (st_env == 2 || (L.nt == 32 && cols_one >= sms))) {
+        (st_env == 2 ||
+         // (columns are the unit of work: one entry's columns must fill whole
+         // waves of CTAs -- config 4's 153 columns over 148 SMs would take
+         // two waves for 1.03 waves of work)
+         (L.nt == 32 && !a.pool && cols_one >= sms &&
+          cols_one * 10 >= ceil_div(cols_one, sms) * sms * 9))) {
       st_j0 = j0;
       st_nin = j1 - j0 + 1;
       st_nslab = ceil_div(st_nin, bx_max);
@@ -842,6 +847,15 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
     p.st_nslab = st_nslab;
     p.st_slots = st_slots;
     p.st_ncols = p.tiles_y * p.tiles_z * p.nb;
+    {
+      int a_ = a.ox % st_slots, b_ = st_slots;   // period of (k * ox) mod slots
+      while (a_) {
+        const int t_ = b_ % a_;
+        b_ = a_;
+        a_ = t_;
+      }
+      p.st_nphase = st_slots / b_;
+    }
     p.acc_stride = 0;
     cols = st_slots * p.nt;
     total = static_cast<long long>(p.st_ncols) * st_nslab;

@@ -69,6 +69,7 @@ struct TcParams {
   // no x halo re-reads.  Input slices st_j0 .. st_j0 + st_nin - 1 (halo
   // coordinates) can be non-zero; slab t holds bx of them.
   int stream, st_j0, st_nin, st_nslab, st_slots, st_ncols;
+  int st_nphase;   // ring phases: column k starts at slot (k * ox) mod st_slots, period st_nphase
   int kx, ky, kz;
   int hx, hy, hz;              // halo tile extents
   int pad[3];
@@ -112,7 +113,9 @@ struct TcParams {
   int dbg_mode;                // VXB_TC_DBGMODE (timing experiments, wrong results): 1 no
                                // epilogue, 2 no A loads, 4 no B loads, 8 no MMAs (resident B),
                                // 16 folded MMAs at N = nt, 64 no fp32 conversion, 128 no fp32
-                               // TMA, 256 epilogue TMEM loads only, 512 no bf16 output stores
+                               // TMA, 256 epilogue TMEM loads only, 512 no bf16 output stores,
+                               // 2048 lean epilogue without its bias smem reads, 4096 streamed
+                               // fold keeps the first slab's operand table
 };
 
 struct TcMaps {
