@@ -306,7 +306,8 @@ def bench_network(cfg, args, dev, peaks, flush, *, with_cpu, with_e2e, headline=
                            "graph, in a second pass of %d flushed steps (%.4f ms per step with "
                            "the event nodes; `value` is timed on the same graph without "
                            "them)" % (steps, tot_probed / steps),
-                 "peak_source": peaks["source"] + ", burst", "traffic": ncu_traffic(dname)})
+                 "peak_source": peaks["source"] + ", burst",
+                 "traffic": ncu_traffic("%s/%s" % (dname, dn)) or ncu_traffic(dname)})
     res = {"value": vox * world / (ms * 1e-3), "unit": "output voxels/s", "ms_per_step": ms,
            "steps": steps, "tflops": flops * world / (ms * 1e-3) / 1e12,
            "workload": workload_name(cfg), "roofline": roof,
