@@ -137,10 +137,11 @@ def test_runner_graph_replay_deterministic_and_validates():
 def test_fused_input_pack_is_bit_identical(cfg, monkeypatch):
     """fuse_input=True hands the fp32 network input straight to the first
     conv (in-kernel conversion); the bf16 operands and hence the outputs are
-    identical to packing first.  (Both sides use the single-CTA MMA walk: the
-    fp32-input conv does not run as a CTA pair, whose folded walk sums in
-    another order.)"""
+    identical to packing first.  (Both sides use the single-CTA tiled MMA
+    walk: the fp32-input conv runs neither as a CTA pair nor as a streamed
+    fold, whose walks sum in another order.)"""
     monkeypatch.setenv("VXB_TC_FOLDPAIR", "0")
+    monkeypatch.setenv("VXB_TC_STREAM", "0")
     spec, store = _small(cfg)
     plan, _ = P.compile_network(spec, store, fixpoint=True, fuse_deconv_add=True)
     lo, hi = C.input_range(cfg)
