@@ -1798,7 +1798,9 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
 #pragma unroll
             for (int j = 0; j < 4; ++j)
               if (j < p.head_cout)
-                op[j * hv.s[1]] = apply_act(hsum[j] + p.head_b[j], p.head_act, p.head_alpha);
+                op[j * hv.s[1]] = p.head_act == VXB_ACT_SIGMOID
+                                      ? fast_sigmoid(hsum[j] + p.head_b[j])   // ~1e-7 absolute
+                                      : apply_act(hsum[j] + p.head_b[j], p.head_act, p.head_alpha);
           }
         }
         named_bar_sync(1, EPI_WARPS * 32);   // partials free for the next tile
