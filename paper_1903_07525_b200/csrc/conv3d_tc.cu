@@ -1541,14 +1541,16 @@ __global__ void __maxnreg__(VXB_TC_MAXNREG)
             // l+8, l+9; packed-bf16 max, NaN-propagating like np.maximum
             uint32_t m[8];
 #pragma unroll
+            // (two steps: z neighbour, then the y neighbour of that maximum:
+            // 16 shuffles per item instead of 24; shuffles share the
+            // shared-memory crossbar with the MMAs' operand reads)
             for (int i = 0; i < 8; ++i) {
               const uint32_t t1 = __shfl_down_sync(0xffffffffu, w[i], 1);
-              const uint32_t t2 = __shfl_down_sync(0xffffffffu, w[i], 8);
-              const uint32_t t3 = __shfl_down_sync(0xffffffffu, w[i], 9);
               __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162 *>(&w[i]);
               a = __hmax2_nan(a, *reinterpret_cast<const __nv_bfloat162 *>(&t1));
+              const uint32_t t2 =
+                  __shfl_down_sync(0xffffffffu, *reinterpret_cast<uint32_t *>(&a), 8);
               a = __hmax2_nan(a, *reinterpret_cast<const __nv_bfloat162 *>(&t2));
-              a = __hmax2_nan(a, *reinterpret_cast<const __nv_bfloat162 *>(&t3));
               m[i] = *reinterpret_cast<uint32_t *>(&a);
             }
             if ((lane & 9) == 0 && sc0 + s < slim && !tc.dummy && (rc >> 1) < p.pool_oy &&
