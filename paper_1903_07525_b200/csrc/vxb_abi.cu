@@ -526,6 +526,10 @@ struct TcLaunch {
   EpiView head_out;
 };
 
+// (set while a conv whose streamed configuration did not fit is configured
+// again as tiles)
+static thread_local bool g_no_stream = false;
+
 static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
   TcLaunch a = a_in;
   const int n_cols = a.rep_n ? a.reps * a.rep_n : a.cout;   // GEMM N over all taps in N
@@ -605,7 +609,7 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
                        a.out.dtype == VXB_BF16 && a.out.blocked &&
                        (!a.has_base || (a.base.dtype == VXB_BF16 && a.base.blocked)) &&
                        (a.act == VXB_ACT_NONE || a.act == VXB_ACT_RELU || a.act == VXB_ACT_ELU);
-  const int st_env = env_int("VXB_TC_STREAM", 1);
+  const int st_env = g_no_stream ? 0 : env_int("VXB_TC_STREAM", 1);
   int st_bx = 0, st_j0 = 0, st_nin = 0, st_nslab = 0, st_slots = 0;
   if (st_env && L.fold == 1 && lean_ok && a.reps == 1 && !a.rep_n && L.n_tiles == 1 && a.k[0] == 3) {
     st_slots = 1;
@@ -865,6 +869,14 @@ static int run_tc(const TcLaunch &a_in, cudaStream_t stream) {
   while (p.tmem_cols < cols) p.tmem_cols <<= 1;
   if (p.tmem_cols > 512) return set_error(VXB_EUNSUPPORTED, "TMEM overflow (%d columns)", cols);
   c.smem = tc_smem_bytes(p);
+  if (c.smem > 227 * 1024 && p.stream) {
+    // the ring's operand tables and the lean tables did not fit beside the
+    // resident weights: the tiled walk instead
+    g_no_stream = true;
+    const int rc2 = run_tc(a_in, stream);
+    g_no_stream = false;
+    return rc2;
+  }
   if (c.smem > 227 * 1024) return set_error(VXB_EUNSUPPORTED, "conv needs %zu B smem", c.smem);
   // persistent: one CTA per SM (480 threads x ~100 registers leaves no room
   // for a second one, and the smem ring is sized for the whole SM)
